@@ -1,0 +1,144 @@
+/*
+ * simtgraph_cuda.h — C ABI of libsimtgraph_cuda.so, the B200 (sm_100a)
+ * implementation of the reference simtgraph's ALB hot path.
+ *
+ * Two cuts, both taken from the reference's own interfaces:
+ *
+ *  1. Run level (the performance cut).  Replaces the body of
+ *     engine.run / engine.run_app (/root/reference/pkg/src/simtgraph/
+ *     engine.py:190-261): the whole BSP loop — inspection, huge-vertex LB
+ *     kernel, TWC bins, push/pull operator, frontier fold, edge-cut label
+ *     sync — runs on the device; the caller gets float64 labels (apps.py:63-64)
+ *     and one sg_round per BSP round (engine.py:116-163 RoundRecord).
+ *
+ *  2. Kernel level (the reference's plugin seam, kernels.py:16-41).
+ *     sg_lb_kernel / sg_twc_kernel / sg_vertex_kernel / sg_edge_kernel take
+ *     exactly the buffers of _kernels_py.lb_kernel / twc_kernel /
+ *     vertex_kernel / edge_kernel (_kernels_py.py:88-201): caller-owned host
+ *     arrays, `out`, `per_cta_edges`, `per_warp_paths` mutated in place.
+ *
+ * Conventions: every function returns 0 on success or a negative SG_E*
+ * code; sg_last_error() returns the thread-local message of the last
+ * failure.  Codes map onto the reference's exception taxonomy (errors.py).
+ * The library owns all device memory behind handles; the caller owns host
+ * buffers.  Calls are not re-entrant per handle.  No torch types anywhere.
+ */
+#ifndef SIMTGRAPH_CUDA_H
+#define SIMTGRAPH_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes -> errors.py classes */
+#define SG_OK 0
+#define SG_ECONFIG (-1)     /* ConfigError   (errors.py:16-17)  */
+#define SG_ERANGE (-2)      /* RangeError    (errors.py:12-13)  */
+#define SG_ECONVERGE (-3)   /* ConvergenceError (errors.py:36-45) */
+#define SG_ECUDA (-4)       /* SimtGraphError: CUDA failure      */
+#define SG_ENOMEM (-5)      /* SimtGraphError: device allocation */
+
+/* apps (apps.py:24; opcodes _kernels_py.py:26-29) */
+#define SG_APP_BFS 0
+#define SG_APP_SSSP 1
+#define SG_APP_CC 2
+#define SG_APP_PR 3
+#define SG_APP_KCORE 4
+
+/* scheduler kinds (schedulers.py:30) */
+#define SG_SCHED_ALB 0
+#define SG_SCHED_TWC 1
+
+typedef struct sg_graph sg_graph; /* opaque: HBM-resident CSR (+ lazy CSC / sym) */
+
+typedef struct sg_params {
+  int32_t app;        /* SG_APP_* */
+  int32_t sched;      /* SG_SCHED_ALB | SG_SCHED_TWC (twc = no huge bin) */
+  int32_t blocked;    /* huge-vertex distribution: 0 cyclic, 1 blocked (schedulers.py:191-200) */
+  int32_t devices;    /* edge-cut partitions (engine.py:64-85); >1 = simulated on this GPU */
+  int64_t source;     /* bfs / sssp (apps.py:83-95) */
+  int64_t k;          /* kcore (apps.py:204-208) */
+  double damping;     /* pr (apps.py:145-153) */
+  double tol;         /* pr */
+  int64_t threshold;  /* resolved huge threshold >= 1 (schedulers.py:58-60, worklist.py:122-128) */
+  int64_t max_rounds; /* <= 0: 10*V + 256 (engine.py:199-202) */
+  int32_t flags;      /* SG_FLAG_* */
+  int32_t reserved;
+} sg_params;
+
+#define SG_FLAG_TIMING 1 /* fill *ms_out with the CUDA-event time of the BSP loop */
+
+typedef struct sg_round { /* one BSP round (engine.py:116-163) */
+  int64_t frontier_size;  /* RoundRecord.frontier_size */
+  int64_t active_edges;   /* RoundRecord.active_edges(): operator applications */
+  int64_t huge_count;     /* |huge| after inspection (schedulers.py:291) */
+  int64_t huge_edges;     /* PrefixWork.total_edges (lb kernel edges) */
+  int64_t large_count;    /* CTA-bin vertices */
+  int64_t updated;        /* vertices whose label changed (next frontier / dying) */
+  int64_t comm_sent;      /* engine.py:225-229 (devices > 1) */
+  int64_t comm_broadcast; /* engine.py:232-234 (devices > 1) */
+} sg_round;
+
+const char *sg_last_error(void);
+int sg_device_count(int *count);
+
+/* --- graph store (graph.py:29-177) ------------------------------------- */
+/* Upload a CSR (graph.py:33-37 dtypes): offsets int64[nv+1], targets int32[ne],
+ * weights int64[ne] or NULL.  Validates like Graph._validate (graph.py:44-57). */
+int sg_graph_create(const int64_t *offsets, const int32_t *targets, const int64_t *weights,
+                    int64_t nv, int64_t ne, sg_graph **out);
+/* generate_rmat on the device (graph.py:274-298), bit-exact to numpy PCG64:
+ * pcg = {state_hi, state_lo, inc_hi, inc_lo} of np.random.PCG64(seed).state,
+ * cuts = np.cumsum(probs)[:3]. */
+int sg_graph_create_rmat(int32_t scale, int64_t edge_factor, const uint64_t pcg[4],
+                         const double cuts[3], sg_graph **out);
+/* attach_random_weights (graph.py:301-305) on the device for power-of-two
+ * ranges (high-low+1 = 2^j <= 2^32): numpy's Lemire path never rejects there. */
+int sg_graph_attach_random_weights(sg_graph *g, const uint64_t pcg[4], int64_t low, int64_t high,
+                                   sg_graph **out);
+/* Upload host weights for an existing device graph (same topology). */
+int sg_graph_with_weights(sg_graph *g, const int64_t *weights, sg_graph **out);
+int sg_graph_info(sg_graph *g, int64_t *nv, int64_t *ne, int32_t *weighted);
+/* Copy arrays back to host; any pointer may be NULL.  which: 0 CSR, 1 CSC, 2 symmetrized CSR */
+int sg_graph_download(sg_graph *g, int32_t which, int64_t *offsets, int32_t *targets,
+                      int64_t *weights);
+int sg_graph_view_size(sg_graph *g, int32_t which, int64_t *ne);
+void sg_graph_destroy(sg_graph *g);
+
+/* --- run level: engine.run (engine.py:190-246) -------------------------- */
+int sg_run(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
+           int64_t rounds_cap, int64_t *nrounds, double *ms_out);
+
+/* --- kernel level: the reference plugin API (_kernels_py.py:88-201) ------ */
+int sg_lb_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,
+                 const double *weights, int64_t nw, const int64_t *huge,
+                 const int64_t *cumulative, int64_t nhuge, const double *values, double *out,
+                 const double *aux, int64_t naux, int32_t opcode, int32_t blocked,
+                 int32_t num_ctas, int32_t threads_per_cta, int32_t warp_size,
+                 int64_t *per_cta_edges, int64_t *per_warp_paths, int64_t *accesses);
+int sg_twc_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,
+                  const double *weights, int64_t nw, const int64_t *small, int64_t nsmall,
+                  const int64_t *medium, int64_t nmedium, const int64_t *large, int64_t nlarge,
+                  const double *values, double *out, const double *aux, int64_t naux,
+                  int32_t opcode, int32_t num_ctas, int32_t threads_per_cta, int32_t warp_size,
+                  int64_t *per_cta_edges);
+int sg_vertex_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,
+                     const double *weights, int64_t nw, const int64_t *frontier, int64_t nf,
+                     const double *values, double *out, const double *aux, int64_t naux,
+                     int32_t opcode, int32_t num_ctas, int32_t threads_per_cta,
+                     int64_t *per_cta_edges);
+int sg_edge_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,
+                   const double *weights, int64_t nw, const int64_t *frontier, int64_t nf,
+                   const double *values, double *out, const double *aux, int64_t naux,
+                   int32_t opcode, int32_t num_ctas, int32_t threads_per_cta,
+                   int64_t *per_cta_edges);
+
+/* number of kernels this library launched since load (evidence counter) */
+int64_t sg_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,118 @@
+// sg_ctl.cuh — device-resident BSP round control.
+//
+// Every kernel of a round reads the round index, frontier size and done flag
+// from this block, so a round is a fixed sequence of launches with fixed
+// arguments (capturable in a CUDA graph) and the host never has to read a
+// count to launch the next round (it checks `done` every few rounds).
+#pragma once
+#include "sg_common.cuh"
+
+namespace sg {
+
+struct Ctl {
+  int32_t round;        // index of the round being executed (engine.py:205 loop count)
+  int32_t done;         // frontier empty / pr converged / error
+  int32_t error;        // SG_ECONVERGE when max_rounds is exceeded (engine.py:206-209)
+  int32_t dense;        // current frontier is all of [0, nv) (cc / kcore round 0, pr)
+  uint32_t fsize;       // current frontier size (queue q[round & 1])
+  uint32_t nsize;       // next-frontier enqueue cursor (queue q[(round + 1) & 1])
+  uint32_t nlarge;      // CTA-bin vertices found by inspection this round
+  uint32_t nhuge;       // huge vertices found by inspection this round
+  uint32_t large_head;  // dynamic fetch cursor of the CTA-bin kernel
+  uint32_t ticket;      // last-block ticket of the advance kernels
+  uint32_t ndying;      // kcore: vertices whose count fell below k this round
+  uint32_t pad;
+  unsigned long long edges;       // active edges (sum of frontier degrees) this round
+  unsigned long long huge_edges;  // PrefixWork.total_edges
+  unsigned long long delta_bits;  // pr: max |new - old| (double bits, >= 0)
+  unsigned long long comm_sent;
+  unsigned long long comm_bcast;
+};
+
+// one record per round, layout == sg_round (include/simtgraph_cuda.h)
+struct RoundStat {
+  long long frontier_size, active_edges, huge_count, huge_edges, large_count, updated,
+      comm_sent, comm_broadcast;
+};
+static_assert(sizeof(RoundStat) == sizeof(sg_round), "RoundStat must mirror sg_round");
+
+// Per-warp staging of enqueued vertex ids in shared memory: one global
+// atomic per ~224 ids and coalesced copies out, instead of one contended
+// atomic per warp per edge chunk.
+constexpr int kWQ = 256;
+struct WarpQueue {
+  uint32_t *buf;  // kWQ shared-memory slots owned by this warp
+  uint32_t n;     // warp-uniform fill level
+  uint32_t *gq;
+  uint32_t *gcount;
+
+  __device__ __forceinline__ void flush() {
+    __syncwarp();
+    uint32_t base = 0;
+    if (lane_id() == 0 && n) base = atomicAdd(gcount, n);
+    base = __shfl_sync(kFull, base, 0);
+    for (uint32_t j = lane_id(); j < n; j += 32) gq[base + j] = buf[j];
+    __syncwarp();
+    n = 0;
+  }
+  // must be called by all 32 lanes (converged)
+  __device__ __forceinline__ void push(bool p, uint32_t v) {
+    uint32_t m = __ballot_sync(kFull, p);
+    if (!m) return;
+    if (p) buf[n + __popc(m & lanemask_lt())] = v;
+    n += __popc(m);
+    if (n > kWQ - 32) flush();
+  }
+};
+
+// warp-aggregated append of flagged lanes to a global list (rare events)
+__device__ __forceinline__ void warp_append(bool p, uint32_t v, uint32_t *list, uint32_t *count) {
+  uint32_t m = __ballot_sync(kFull, p);
+  if (!m) return;
+  uint32_t base = 0;
+  if (lane_id() == (uint32_t)(__ffs(m) - 1)) base = atomicAdd(count, (uint32_t)__popc(m));
+  base = __shfl_sync(kFull, base, __ffs(m) - 1);
+  if (p) list[base + __popc(m & lanemask_lt())] = v;
+}
+
+template <class T>
+__device__ __forceinline__ T block_sum(T x, T *smem /* >= 32 */) {
+  x = warp_sum(x);
+  __syncthreads();
+  if (lane_id() == 0) smem[threadIdx.x >> 5] = x;
+  __syncthreads();
+  T r = 0;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < (blockDim.x >> 5) ? smem[threadIdx.x] : T(0);
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+// first lane o of a warp whose inclusive prefix exceeds `slot` (prefixes non-decreasing)
+__device__ __forceinline__ int warp_owner(uint32_t incl, uint32_t slot) {
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step; step >>= 1) {
+    uint32_t iv = __shfl_sync(kFull, incl, o + step - 1);
+    if (iv <= slot) o += step;
+  }
+  return o;
+}
+
+__device__ __forceinline__ int64_t shfl64(int64_t x, int src) {
+  return (int64_t)__shfl_sync(kFull, (long long)x, src);
+}
+
+// upper_bound: first i in [0, n) with pre[i] > g (pre inclusive, increasing)
+__device__ __forceinline__ uint32_t owner_search(const int64_t *pre, uint32_t n, int64_t g) {
+  uint32_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (g < pre[mid]) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+}  // namespace sg

@@ -1,0 +1,266 @@
+// sg_graph.cu — graph construction on the device.
+//
+// Every builder reproduces the reference's host construction bit for bit:
+//   from_edges  = stable sort by source         (graph.py:63-76)
+//   csc         = stable sort by target         (graph.py:95-113)
+//   symmetrized = row v of CSR ++ row v of CSC  (graph.py:115-128: the stable sort of
+//                 concat(src,dst) by source yields exactly that order)
+//   generate_rmat / attach_random_weights: numpy PCG64 streams (graph.py:274-305)
+// The LSD radix sort (CUB) is stable, which is what makes these identical.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "sg_graph.cuh"
+
+namespace sg {
+
+namespace {
+
+__global__ void k_offsets_from_sorted(const uint32_t *__restrict__ keys, int64_t ne, int64_t nv,
+                                      int64_t *__restrict__ off) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= ne; i += stride) {
+    int64_t hi = (i < ne) ? (int64_t)keys[i] : nv;        // rows [lo+1, hi] start at i
+    int64_t lo = (i > 0) ? (int64_t)keys[i - 1] : -1;
+    for (int64_t v = lo + 1; v <= hi; ++v) off[v] = i;
+  }
+}
+
+// row id of every edge: one warp per row, coalesced writes
+__global__ void k_expand_rows(const int64_t *__restrict__ off, int64_t nv,
+                              uint32_t *__restrict__ rows) {
+  int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nv; v += warps) {
+    int64_t s = off[v], e = off[v + 1];
+    for (int64_t i = s + lane_id(); i < e; i += 32) rows[i] = (uint32_t)v;
+  }
+}
+
+__global__ void k_sym_offsets(const int64_t *__restrict__ a, const int64_t *__restrict__ b,
+                              int64_t nv, int64_t *__restrict__ out) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= nv; v += stride)
+    out[v] = a[v] + b[v];
+}
+
+__global__ void k_sym_fill(const int64_t *__restrict__ aoff, const uint32_t *__restrict__ acol,
+                           const int64_t *__restrict__ boff, const uint32_t *__restrict__ bcol,
+                           const int64_t *__restrict__ soff, int64_t nv,
+                           uint32_t *__restrict__ scol) {
+  int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nv; v += warps) {
+    int64_t o = soff[v];
+    int64_t s = aoff[v], e = aoff[v + 1];
+    for (int64_t i = s + lane_id(); i < e; i += 32) scol[o + (i - s)] = acol[i];
+    o += e - s;
+    s = boff[v], e = boff[v + 1];
+    for (int64_t i = s + lane_id(); i < e; i += 32) scol[o + (i - s)] = bcol[i];
+  }
+}
+
+// ---- numpy PCG64 (pcg_setseq_128_xsl_rr_64, step-then-output) -------------
+typedef unsigned __int128 u128;
+__host__ __device__ inline u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+}
+__host__ __device__ inline uint64_t pcg_output(u128 s) {
+  uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+  unsigned r = (unsigned)(s >> 122);
+  return (x >> r) | (x << ((64u - r) & 63u));
+}
+// affine jump: state after `delta` steps is A*state + C
+__host__ __device__ inline void pcg_jump(u128 inc, u128 delta, u128 &A, u128 &C) {
+  u128 am = 1, ap = 0, cm = pcg_mult(), cp = inc;
+  while (delta) {
+    if (delta & 1) { am *= cm; ap = ap * cm + cp; }
+    cp = (cm + 1) * cp;
+    cm *= cm;
+    delta >>= 1;
+  }
+  A = am, C = ap;
+}
+
+constexpr int kRmatPer = 16;  // edges per thread (registers hold their src/dst bits)
+
+// Level l, edge i uses draw l*E+i of the stream (graph.py:293-297):
+// u = (next64 >> 11) * 2^-53;  q = searchsorted(cuts, u, 'right')
+__global__ void __launch_bounds__(256) k_rmat(int scale, int64_t ne, uint64_t s_hi, uint64_t s_lo,
+                                              uint64_t i_hi, uint64_t i_lo, uint64_t AE_hi,
+                                              uint64_t AE_lo, uint64_t CE_hi, uint64_t CE_lo,
+                                              double c0, double c1, double c2,
+                                              uint32_t *__restrict__ src,
+                                              uint32_t *__restrict__ dst) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i0 = t * kRmatPer;
+  if (i0 >= ne) return;
+  const u128 inc = ((u128)i_hi << 64) | i_lo;
+  const u128 AE = ((u128)AE_hi << 64) | AE_lo, CE = ((u128)CE_hi << 64) | CE_lo;
+  const u128 M = pcg_mult();
+  u128 A, C;
+  pcg_jump(inc, (u128)i0, A, C);
+  u128 lvl = A * (((u128)s_hi << 64) | s_lo) + C;  // state before draw l*E + i0
+  uint32_t s[kRmatPer], d[kRmatPer];
+#pragma unroll
+  for (int j = 0; j < kRmatPer; ++j) s[j] = 0, d[j] = 0;
+  const int n = (int)min((int64_t)kRmatPer, ne - i0);
+  for (int l = 0; l < scale; ++l) {
+    u128 x = lvl;
+#pragma unroll
+    for (int j = 0; j < kRmatPer; ++j) {
+      x = x * M + inc;
+      double u = (double)(pcg_output(x) >> 11) * (1.0 / 9007199254740992.0);
+      uint32_t q = (u >= c0) + (u >= c1) + (u >= c2);
+      s[j] = (s[j] << 1) | (q >> 1);
+      d[j] = (d[j] << 1) | (q & 1u);
+    }
+    lvl = AE * lvl + CE;
+  }
+#pragma unroll
+  for (int j = 0; j < kRmatPer; ++j)
+    if (j < n) src[i0 + j] = s[j], dst[i0 + j] = d[j];
+}
+
+// rng.integers(low, low + 2^j) with dtype int64 (graph.py:304): numpy's
+// bounded path takes next_uint32 (low half of a 64-bit draw, then the high
+// half) and Lemire-scales by 2^j: out = low + (u32 >> (32 - j)); no rejections.
+__global__ void k_weights(int64_t ne, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                          int64_t low, int jbits, int64_t *__restrict__ w) {
+  int64_t pair = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * pair >= ne) return;
+  const u128 inc = ((u128)i_hi << 64) | i_lo;
+  u128 A, C;
+  pcg_jump(inc, (u128)pair + 1, A, C);
+  uint64_t r = pcg_output(A * (((u128)s_hi << 64) | s_lo) + C);
+  uint32_t lo = (uint32_t)r, hi = (uint32_t)(r >> 32);
+  auto scale = [&](uint32_t u) -> int64_t {
+    return low + (int64_t)(jbits == 0 ? 0 : (((uint64_t)u * (1ull << jbits)) >> 32));
+  };
+  w[2 * pair] = scale(lo);
+  if (2 * pair + 1 < ne) w[2 * pair + 1] = scale(hi);
+}
+
+__global__ void k_w32(const int64_t *__restrict__ w, int64_t ne, uint32_t *__restrict__ o) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += stride)
+    o[i] = (uint32_t)w[i];
+}
+
+inline int grid_for(int64_t n, int block = 256) {
+  int64_t g = (n + block - 1) / block;
+  int64_t cap = (int64_t)sm_info().sms * 16;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+void build_csr_from_pairs(View &v, int64_t nv, uint32_t *src, uint32_t *dst, int64_t ne,
+                          int key_bits) {
+  v.nv = nv;
+  v.ne = ne;
+  v.off.alloc(nv + 1);
+  v.col.alloc(ne ? ne : 1);
+  DBuf<uint32_t> keys_out(ne ? ne : 1);
+  if (ne) {
+    size_t tmp = 0;
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, src, keys_out.p, dst, v.col.p, ne, 0,
+                                            key_bits));
+    DBuf<char> t(tmp);
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, src, keys_out.p, dst, v.col.p, ne, 0,
+                                            key_bits));
+    g_launches.fetch_add(1);
+  }
+  SG_LAUNCH(k_offsets_from_sorted, grid_for(ne + 1), 256, 0, 0, keys_out.p, ne, nv, v.off.p);
+  SG_CUDA(cudaDeviceSynchronize());
+}
+
+void build_transpose(View &out, const View &in) {
+  DBuf<uint32_t> rows(in.ne ? in.ne : 1), keys(in.ne ? in.ne : 1);
+  if (in.ne) {
+    SG_LAUNCH(k_expand_rows, grid_for(in.nv * 32), 256, 0, 0, in.off.p, in.nv, rows.p);
+    SG_CUDA(cudaMemcpy(keys.p, in.col.p, sizeof(uint32_t) * in.ne, cudaMemcpyDeviceToDevice));
+  }
+  build_csr_from_pairs(out, in.nv, keys.p, rows.p, in.ne, bits_for(in.nv));
+}
+
+void build_symmetrized(View &out, const View &csr, const View &csc) {
+  out.nv = csr.nv;
+  out.ne = csr.ne + csc.ne;
+  out.off.alloc(out.nv + 1);
+  out.col.alloc(out.ne ? out.ne : 1);
+  SG_LAUNCH(k_sym_offsets, grid_for(out.nv + 1), 256, 0, 0, csr.off.p, csc.off.p, out.nv,
+            out.off.p);
+  SG_LAUNCH(k_sym_fill, grid_for(out.nv * 32), 256, 0, 0, csr.off.p, csr.col.p, csc.off.p,
+            csc.col.p, out.off.p, out.nv, out.col.p);
+  SG_CUDA(cudaDeviceSynchronize());
+}
+
+void rmat_pairs_device(int scale, int64_t ne, const uint64_t pcg[4], const double cuts[3],
+                       uint32_t *src, uint32_t *dst) {
+  u128 inc = ((u128)pcg[2] << 64) | pcg[3];
+  u128 AE, CE;
+  pcg_jump(inc, (u128)ne, AE, CE);
+  int64_t threads = (ne + kRmatPer - 1) / kRmatPer;
+  int64_t blocks = (threads + 255) / 256;
+  SG_LAUNCH(k_rmat, (unsigned)blocks, 256, 0, 0, scale, ne, pcg[0], pcg[1], pcg[2], pcg[3],
+            (uint64_t)(AE >> 64), (uint64_t)AE, (uint64_t)(CE >> 64), (uint64_t)CE, cuts[0],
+            cuts[1], cuts[2], src, dst);
+  SG_CUDA(cudaDeviceSynchronize());
+}
+
+void random_weights_device(int64_t ne, const uint64_t pcg[4], int64_t low, int j_bits,
+                           int64_t *w64) {
+  int64_t pairs = (ne + 1) / 2;
+  if (!pairs) return;
+  SG_LAUNCH(k_weights, (unsigned)((pairs + 255) / 256), 256, 0, 0, ne, pcg[0], pcg[1], pcg[2],
+            pcg[3], low, j_bits, w64);
+  SG_CUDA(cudaDeviceSynchronize());
+}
+
+void weights_finalize(Graph &g) {
+  g.weighted = true;
+  if (!g.ne) { g.wmin = g.wmax = 0; return; }
+  DBuf<int64_t> mm(2);
+  size_t tmp = 0;
+  SG_CUDA(cub::DeviceReduce::Min(nullptr, tmp, g.w64.p, mm.p, g.ne));
+  size_t tmp2 = 0;
+  SG_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, g.w64.p, mm.p + 1, g.ne));
+  DBuf<char> t(std::max(tmp, tmp2));
+  SG_CUDA(cub::DeviceReduce::Min(t.p, tmp, g.w64.p, mm.p, g.ne));
+  SG_CUDA(cub::DeviceReduce::Max(t.p, tmp2, g.w64.p, mm.p + 1, g.ne));
+  int64_t h[2];
+  SG_CUDA(cudaMemcpy(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost));
+  g.wmin = h[0], g.wmax = h[1];
+  if (g.wmin >= 0 && g.wmax < ((int64_t)1 << 32)) {
+    g.w32.alloc(g.ne);
+    SG_LAUNCH(k_w32, grid_for(g.ne), 256, 0, 0, g.w64.p, g.ne, g.w32.p);
+    SG_CUDA(cudaDeviceSynchronize());
+  }
+}
+
+const View &Graph::csc() {
+  if (!csc_) {
+    auto v = std::make_unique<View>();
+    build_transpose(*v, csr);
+    csc_ = std::move(v);
+  }
+  return *csc_;
+}
+
+const View &Graph::sym() {
+  if (!sym_) {
+    const View &c = csc();
+    auto v = std::make_unique<View>();
+    build_symmetrized(*v, csr, c);
+    sym_ = std::move(v);
+  }
+  return *sym_;
+}
+
+}  // namespace sg

@@ -1,0 +1,45 @@
+// sg_graph.cuh — the HBM-resident graph store (reference graph.py:29-177).
+#pragma once
+#include <memory>
+
+#include "sg_common.cuh"
+
+namespace sg {
+
+// One traversal view: CSR rows (push) or CSC rows (pull), int64 offsets,
+// u32 column ids (graph.py:33-34 dtypes; ids < 2^31 so u32 == int32 bits).
+struct View {
+  int64_t nv = 0, ne = 0;
+  DBuf<int64_t> off;
+  DBuf<uint32_t> col;
+};
+
+struct Graph {
+  int64_t nv = 0, ne = 0;
+  View csr;
+  bool weighted = false;
+  int64_t wmin = 0, wmax = 0;
+  DBuf<int64_t> w64;  // the reference's int64 weights (graph.py:35-37)
+  DBuf<uint32_t> w32; // compact copy used by the sssp kernels when 0 <= w < 2^32
+  std::unique_ptr<View> csc_;  // Graph.csc()         (graph.py:95-113), built lazily
+  std::unique_ptr<View> sym_;  // Graph.symmetrized() (graph.py:115-128), built lazily
+  const View &csc();
+  const View &sym();
+};
+
+// builders (sg_graph.cu)
+void build_csr_from_pairs(View &v, int64_t nv, uint32_t *src, uint32_t *dst, int64_t ne,
+                          int key_bits);
+void build_transpose(View &out, const View &in);
+void build_symmetrized(View &out, const View &csr, const View &csc);
+void rmat_pairs_device(int scale, int64_t ne, const uint64_t pcg[4], const double cuts[3],
+                       uint32_t *src, uint32_t *dst);
+void random_weights_device(int64_t ne, const uint64_t pcg[4], int64_t low, int j_bits,
+                           int64_t *w64);
+void weights_finalize(Graph &g);  // wmin / wmax / w32 from w64
+
+}  // namespace sg
+
+struct sg_graph {
+  std::shared_ptr<sg::Graph> g;
+};

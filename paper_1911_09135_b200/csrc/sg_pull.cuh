@@ -1,0 +1,290 @@
+// sg_pull.cuh — ALB pull round (pr: rank sums, kcore: surviving-neighbour counts).
+//
+// Reference: OP_PULL_ADD out[row] += aux[col[e]] (_kernels_py.py:73-75), rows of
+// the CSC view; pr folds new = (1-d) + d*acc and stops on max|new-old| <= eps
+// (apps.py:176-186); kcore counts alive neighbours of frontier vertices and
+// kills those below k (apps.py:217-232).
+// B200 mapping: rows are owned by exactly one lane / CTA in the TWC bins, so
+// their sums are formed in registers (warp-segmented shuffle scans, CTA tree
+// reduction — deterministic order) and folded in the same kernel (pr writes
+// rank and next round's aux = rank*inv_outdeg; kcore emits the dying list).
+// Only huge rows are split across CTAs by the LB kernel; their partial sums
+// are pre-reduced per warp segment and combined with one atomicAdd per segment.
+#pragma once
+#include "sg_push.cuh"
+
+namespace sg {
+
+struct PullArgs {
+  const int64_t *off;
+  const uint32_t *col;
+  uint32_t nv;
+  Ctl *ctl;
+  uint32_t *q[2];  // kcore frontier queues
+  uint32_t *largeq, *hugeq;
+  int64_t *hpre, *hstart;
+  int64_t threshold;
+  int dynamic_bins;  // 1: kcore (bins found per round); 0: pr (static bins, dense rows)
+  uint32_t *dying;   // kcore dying list (count ctl->ndying)
+  RoundStat *stats;
+};
+
+// pr: acc = sum aux[u]; new = (1-d) + d*acc (two roundings, as numpy); aux' = new*inv
+struct PrOp {
+  using A = double;
+  const double *aux0, *aux1;
+  double *next0, *next1;
+  double *rank;
+  const double *inv;
+  double d, omd;
+  const double *aux = nullptr;
+  double *auxn = nullptr;
+  double dmax = 0.0;
+  __device__ __forceinline__ void begin(uint32_t round) {
+    aux = (round & 1) ? aux1 : aux0;
+    auxn = (round & 1) ? next1 : next0;
+  }
+  __device__ __forceinline__ A load(uint32_t u) const { return __ldg(aux + u); }
+  __device__ __forceinline__ bool finish(uint32_t v, A acc) {
+    double nw = __dadd_rn(omd, __dmul_rn(d, acc));
+    double dl = fabs(__dsub_rn(nw, rank[v]));
+    dmax = dl > dmax ? dl : dmax;
+    rank[v] = nw;
+    auxn[v] = __dmul_rn(nw, inv[v]);
+    return false;
+  }
+};
+
+// kcore: count = sum alive[u] with multiplicity (integers: any order is exact)
+struct KcOp {
+  using A = uint32_t;
+  const uint8_t *alive;
+  uint32_t k;
+  double dmax = 0.0;  // unused
+  __device__ __forceinline__ void begin(uint32_t) {}
+  __device__ __forceinline__ A load(uint32_t u) const { return alive[u]; }
+  __device__ __forceinline__ bool finish(uint32_t, A acc) const { return acc < k; }
+};
+
+__device__ __forceinline__ void atomic_max_dbits(unsigned long long *p, double x) {
+  atomicMax(p, (unsigned long long)__double_as_longlong(x));  // x >= 0
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
+  __shared__ unsigned long long red[32];
+  __shared__ double redd[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t round = ctl->round;
+  op.begin(round);
+  const bool dense = !a.dynamic_bins || ctl->dense;
+  const uint32_t n = dense ? a.nv : ctl->fsize;
+  const uint32_t *list = a.q[round & 1];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  unsigned long long my_edges = 0;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsTB;
+  for (uint64_t c = (uint64_t)blockIdx.x * kWarpsTB + warp; c * 32 < n; c += nwarps) {
+    uint64_t i = c * 32 + lane;
+    uint32_t v = 0;
+    int64_t s = 0, deg = 0;
+    const bool valid = i < n;
+    if (valid) {
+      v = dense ? (uint32_t)i : list[i];
+      s = a.off[v];
+      deg = a.off[v + 1] - s;
+    }
+    my_edges += (unsigned long long)deg;
+    const bool huge = deg >= a.threshold;
+    const bool large = !huge && deg >= (int64_t)kLarge;
+    if (a.dynamic_bins) {
+      warp_append(huge, v, a.hugeq, &ctl->nhuge);
+      warp_append(large, v, a.largeq, &ctl->nlarge);
+    }
+    const bool mine = valid && !huge && !large;
+    const uint32_t gd = mine ? (uint32_t)deg : 0u;
+    const uint32_t incl = warp_incl_scan(gd);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    const uint32_t excl = incl - gd;
+    typename Op::A acc = 0;
+    for (uint32_t base = 0; base < total; base += 32) {
+      const uint32_t slot = base + lane;
+      const int o = warp_owner(incl, slot);
+      const int64_t so = shfl64(s, o);
+      const uint32_t eo = __shfl_sync(kFull, excl, o);
+      typename Op::A x = 0;
+      if (slot < total) x = op.load(ld_stream(a.col + so + (slot - eo)));
+      // segmented inclusive scan (owners are non-decreasing along the lanes)
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        typename Op::A y = __shfl_up_sync(kFull, x, dd);
+        int oo = __shfl_up_sync(kFull, o, dd);
+        if (lane >= (uint32_t)dd && oo == o) x += y;
+      }
+      // each owner lane picks up the total of its segment in this chunk
+      const uint32_t lo = excl > base ? excl : base;
+      const uint32_t hi = incl < base + 32 ? incl : base + 32;
+      typename Op::A seg = __shfl_sync(kFull, x, (int)((hi - 1 - base) & 31u));
+      if (lo < hi) acc += seg;
+    }
+    bool die = false;
+    if (mine) die = op.finish(v, acc);
+    warp_append(die, v, a.dying, &ctl->ndying);
+  }
+  if (a.dynamic_bins) {
+    unsigned long long bs = block_sum(my_edges, red);
+    if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+  }
+  if (sizeof(typename Op::A) == 8) {
+    double m = warp_max(op.dmax);
+    if (lane == 0) redd[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kWarpsTB; ++w) m = redd[w] > m ? redd[w] : m;
+      if (m > 0) atomic_max_dbits(&ctl->delta_bits, m);
+    }
+  }
+}
+
+// TWC CTA bin: one CTA per row (dynamic fetch), deterministic tree reduction
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
+  __shared__ typename Op::A red[32];
+  __shared__ uint32_t item;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  for (;;) {
+    if (threadIdx.x == 0) item = atomicAdd(&ctl->large_head, 1u);
+    __syncthreads();
+    const uint32_t idx = item;
+    __syncthreads();
+    if (idx >= n) break;
+    const uint32_t v = a.largeq[idx];
+    const int64_t s = a.off[v], e = a.off[v + 1];
+    typename Op::A x = 0;
+    for (int64_t j = s + threadIdx.x; j < e; j += kTB) x += op.load(ld_stream(a.col + j));
+    x = block_sum(x, red);
+    if (threadIdx.x == 0 && op.finish(v, x)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
+  }
+  if (sizeof(typename Op::A) == 8 && threadIdx.x == 0 && op.dmax > 0)
+    atomic_max_dbits(&ctl->delta_bits, op.dmax);
+}
+
+// PrefixWork of the huge rows (no labels needed for pull)
+__global__ void __launch_bounds__(1024) k_pull_prefix(PullArgs a) {
+  __shared__ long long red[32];
+  __shared__ long long carry;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t n = ctl->nhuge;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t b = 0; b < n; b += 1024) {
+    uint32_t i = b + threadIdx.x;
+    long long d = 0;
+    if (i < n) {
+      uint32_t v = a.hugeq[i];
+      a.hstart[i] = a.off[v];
+      d = a.off[v + 1] - a.off[v];
+    }
+    long long x = warp_incl_scan(d);
+    if (lane_id() == 31) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) red[threadIdx.x] = warp_incl_scan(red[threadIdx.x]);
+    __syncthreads();
+    long long wpre = (threadIdx.x >> 5) ? red[(threadIdx.x >> 5) - 1] : 0;
+    if (i < n) a.hpre[i] = carry + wpre + x;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += wpre + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ctl->huge_edges = (unsigned long long)carry;
+}
+
+// huge rows: cyclic / blocked over all threads, warp-segmented pre-reduction
+template <class Op, bool BLOCKED>
+__global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op::A *hacc) {
+  __shared__ int64_t spre[kHugeSmem];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t nh = ctl->nhuge;
+  if (!nh) return;
+  op.begin(ctl->round);
+  const int64_t E = (int64_t)ctl->huge_edges;
+  const int64_t *pre = a.hpre;
+  if (nh <= kHugeSmem) {
+    for (uint32_t i = threadIdx.x; i < nh; i += kTB) spre[i] = a.hpre[i];
+    __syncthreads();
+    pre = spre;
+  }
+  const uint32_t lane = lane_id();
+  const int64_t T = (int64_t)gridDim.x * kTB;
+  const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
+  const int64_t passes = (E + T - 1) / T;
+  for (int64_t p = 0; p < passes; ++p) {
+    const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
+    typename Op::A x = 0;
+    int o = -1;
+    if (g < E) {
+      o = (int)owner_search(pre, nh, g);
+      x = op.load(ld_stream(a.col + a.hstart[o] + (g - (o ? pre[o - 1] : 0))));
+    }
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      typename Op::A y = __shfl_up_sync(kFull, x, dd);
+      int oo = __shfl_up_sync(kFull, o, dd);
+      if (lane >= (uint32_t)dd && oo == o) x += y;
+    }
+    int onext = __shfl_down_sync(kFull, o, 1);
+    bool last = (lane == 31) || onext != o;
+    if (o >= 0 && last) atomicAdd(hacc + o, x);
+  }
+}
+
+// huge-row fold (single CTA; huge rows are few) — plus the pr round advance
+template <class Op, bool PR>
+__global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
+                                                      typename Op::A *hacc, double eps_stop,
+                                                      int64_t ne, int64_t max_rounds) {
+  __shared__ double redd[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t round = ctl->round;
+  op.begin(round);
+  const uint32_t nh = ctl->nhuge;
+  for (uint32_t i = threadIdx.x; i < nh; i += 1024) {
+    typename Op::A acc = hacc[i];
+    hacc[i] = 0;
+    uint32_t v = a.hugeq[i];
+    if (op.finish(v, acc)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
+  }
+  if (!PR) return;
+  double m = warp_max(op.dmax);
+  if (lane_id() == 0) redd[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 32; ++w) m = redd[w] > m ? redd[w] : m;
+    unsigned long long mb = (unsigned long long)__double_as_longlong(m);
+    unsigned long long old = atomicMax(&ctl->delta_bits, mb);
+    double delta = __longlong_as_double((long long)(old > mb ? old : mb));
+    RoundStat &st = a.stats[round];
+    st.frontier_size = a.nv;
+    st.active_edges = ne;
+    st.huge_count = nh;
+    st.huge_edges = (long long)ctl->huge_edges;
+    st.large_count = ctl->nlarge;
+    st.updated = a.nv;
+    st.comm_sent = 0;
+    st.comm_broadcast = 0;
+    ctl->delta_bits = 0;
+    ctl->large_head = 0;
+    ctl->round = round + 1;
+    if (delta <= eps_stop) ctl->done = 1;  // apps.py:183-185
+    else if ((int64_t)round + 1 >= max_rounds) ctl->error = SG_ECONVERGE, ctl->done = 1;
+  }
+}
+
+}  // namespace sg

@@ -1,0 +1,211 @@
+"""ctypes binding of libsimtgraph_cuda.so (include/simtgraph_cuda.h).
+
+The library is built in-tree (``paper_1911_09135_b200/_lib``) by
+``python -m paper_1911_09135_b200.build`` / ``__graft_entry__.build()``.
+There is no fallback: if the library or a CUDA device is missing, every
+entry point raises ``SimtGraphError`` (loud failure, never a CPU path).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import ConfigError, ConvergenceError, RangeError, SimtGraphError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsimtgraph_cuda.so"
+
+SG_OK, SG_ECONFIG, SG_ERANGE, SG_ECONVERGE, SG_ECUDA, SG_ENOMEM = 0, -1, -2, -3, -4, -5
+APP_IDS = {"bfs": 0, "sssp": 1, "cc": 2, "pr": 3, "kcore": 4}
+SCHED_IDS = {"alb": 0, "twc": 1}
+
+EXPORTS = (
+    "sg_last_error", "sg_device_count", "sg_graph_create", "sg_graph_create_rmat",
+    "sg_graph_attach_random_weights", "sg_graph_with_weights", "sg_graph_info",
+    "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_lb_kernel",
+    "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
+)
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("app", ctypes.c_int32), ("sched", ctypes.c_int32), ("blocked", ctypes.c_int32),
+                ("devices", ctypes.c_int32), ("source", ctypes.c_int64), ("k", ctypes.c_int64),
+                ("damping", ctypes.c_double), ("tol", ctypes.c_double),
+                ("threshold", ctypes.c_int64), ("max_rounds", ctypes.c_int64),
+                ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+ROUND_DTYPE = np.dtype([("frontier_size", "<i8"), ("active_edges", "<i8"), ("huge_count", "<i8"),
+                        ("huge_edges", "<i8"), ("large_count", "<i8"), ("updated", "<i8"),
+                        ("comm_sent", "<i8"), ("comm_broadcast", "<i8")])
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: Path | None = None):
+    """Load the library (once).  Raises SimtGraphError if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path or os.environ.get("SIMTGRAPH_CUDA_LIB", LIB_PATH))
+        if not p.exists():
+            raise SimtGraphError(
+                f"{p} not built: run `python -m paper_1911_09135_b200.build` (no CPU fallback)")
+        lib = ctypes.CDLL(str(p))
+        P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        pp = ctypes.POINTER(ctypes.c_void_p)
+        sig = {
+            "sg_last_error": ([], ctypes.c_char_p),
+            "sg_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+            "sg_graph_create": ([P, P, P, i64, i64, pp], ctypes.c_int),
+            "sg_graph_create_rmat": ([i32, i64, P, P, pp], ctypes.c_int),
+            "sg_graph_attach_random_weights": ([P, P, i64, i64, pp], ctypes.c_int),
+            "sg_graph_with_weights": ([P, P, pp], ctypes.c_int),
+            "sg_graph_info": ([P, P, P, P], ctypes.c_int),
+            "sg_graph_download": ([P, i32, P, P, P], ctypes.c_int),
+            "sg_graph_view_size": ([P, i32, P], ctypes.c_int),
+            "sg_graph_destroy": ([P], None),
+            "sg_run": ([P, ctypes.POINTER(Params), P, P, i64, P, P], ctypes.c_int),
+            "sg_lb_kernel": ([P, i64, P, i64, P, i64, P, P, i64, P, P, P, i64, i32, i32, i32, i32,
+                              i32, P, P, P], ctypes.c_int),
+            "sg_twc_kernel": ([P, i64, P, i64, P, i64, P, i64, P, i64, P, i64, P, P, P, i64, i32,
+                               i32, i32, i32, P], ctypes.c_int),
+            "sg_vertex_kernel": ([P, i64, P, i64, P, i64, P, i64, P, P, P, i64, i32, i32, i32, P],
+                                 ctypes.c_int),
+            "sg_edge_kernel": ([P, i64, P, i64, P, i64, P, i64, P, P, P, i64, i32, i32, i32, P],
+                               ctypes.c_int),
+            "sg_kernel_launches": ([], ctypes.c_int64),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def check(code: int):
+    if code == SG_OK:
+        return
+    msg = (load().sg_last_error() or b"").decode(errors="replace")
+    if code == SG_ECONFIG:
+        raise ConfigError(msg)
+    if code == SG_ERANGE:
+        raise RangeError(msg)
+    if code == SG_ECONVERGE:
+        raise ConvergenceError(msg)
+    raise SimtGraphError(f"CUDA backend error {code}: {msg}")
+
+
+def ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    check(load().sg_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def kernel_launches() -> int:
+    return int(load().sg_kernel_launches())
+
+
+class DeviceGraph:
+    """Owning handle of an HBM-resident graph (sg_graph*)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise SimtGraphError("device graph already released")
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h and _lib is not None:
+                _lib.sg_graph_destroy(self._h)
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
+        self._h = None
+
+    def info(self):
+        nv, ne, w = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        check(load().sg_graph_info(self.handle, ctypes.byref(nv), ctypes.byref(ne),
+                                   ctypes.byref(w)))
+        return nv.value, ne.value, bool(w.value)
+
+    @classmethod
+    def from_csr(cls, offsets, targets, weights=None):
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        targets = np.ascontiguousarray(targets, dtype=np.int32)
+        if weights is not None:
+            weights = np.ascontiguousarray(weights, dtype=np.int64)
+        h = ctypes.c_void_p()
+        check(load().sg_graph_create(ptr(offsets), ptr(targets), ptr(weights), len(offsets) - 1,
+                                     len(targets), ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def rmat(cls, scale, edge_factor, seed, probs):
+        pcg = pcg64_words(seed)
+        cuts = np.ascontiguousarray(np.cumsum(np.asarray(probs, dtype=np.float64))[:3])
+        h = ctypes.c_void_p()
+        check(load().sg_graph_create_rmat(scale, edge_factor, ptr(pcg), ptr(cuts), ctypes.byref(h)))
+        return cls(h)
+
+    def with_random_weights(self, seed, low, high):
+        pcg = pcg64_words(seed)
+        h = ctypes.c_void_p()
+        check(load().sg_graph_attach_random_weights(self.handle, ptr(pcg), low, high,
+                                                    ctypes.byref(h)))
+        return DeviceGraph(h)
+
+    def with_weights(self, weights):
+        weights = np.ascontiguousarray(weights, dtype=np.int64)
+        h = ctypes.c_void_p()
+        check(load().sg_graph_with_weights(self.handle, ptr(weights), ctypes.byref(h)))
+        return DeviceGraph(h)
+
+    def download(self, which=0, weights=False):
+        """Host copies of a view: 0 CSR, 1 CSC, 2 symmetrized CSR."""
+        nv, ne, _ = self.info()
+        vne = ctypes.c_int64()
+        check(load().sg_graph_view_size(self.handle, which, ctypes.byref(vne)))
+        off = np.empty(nv + 1, dtype=np.int64)
+        tgt = np.empty(vne.value, dtype=np.int32)
+        w = np.empty(ne, dtype=np.int64) if weights else None
+        check(load().sg_graph_download(self.handle, which, ptr(off), ptr(tgt), ptr(w)))
+        return off, tgt, w
+
+    def run(self, params: Params, rounds_cap=1 << 16):
+        nv, _, _ = self.info()
+        labels = np.empty(nv, dtype=np.float64)
+        rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
+        n = ctypes.c_int64(0)
+        ms = ctypes.c_double(0.0)
+        code = load().sg_run(self.handle, ctypes.byref(params), ptr(labels), ptr(rounds),
+                             rounds_cap, ctypes.byref(n), ctypes.byref(ms))
+        log = rounds[: min(n.value, rounds_cap)].copy()
+        if code == SG_ECONVERGE:
+            err = ConvergenceError((load().sg_last_error() or b"").decode())
+            err.metrics_log = log
+            raise err
+        check(code)
+        return labels, log, ms.value
+
+
+def pcg64_words(seed) -> np.ndarray:
+    """(state_hi, state_lo, inc_hi, inc_lo) of np.random.PCG64(seed)."""
+    st = np.random.PCG64(seed).state["state"]
+    m = (1 << 64) - 1
+    s, inc = st["state"], st["inc"]
+    return np.array([s >> 64, s & m, inc >> 64, inc & m], dtype=np.uint64)

@@ -145,8 +145,8 @@ def kernel_fixtures(g, gw):
                                                 cfg.threads_per_cta, cfg.warp_size, pce, pwp)
                     p = f"k{idx}_"
                     rec.update({p + "kind": np.array("lb"), p + "app": np.array(app),
-                                p + "huge": huge, p + "cumulative": cum, p + "values": values,
-                                p + "aux": aux, p + "opcode": np.array(a.opcode),
+                                p + "huge": huge, p + "cumulative": cum, p + "values": values.copy(),
+                                p + "aux": aux.copy(), p + "opcode": np.array(a.opcode),
                                 p + "blocked": np.array(blocked), p + "out": out,
                                 p + "per_cta_edges": pce, p + "per_warp_paths": pwp,
                                 p + "accesses": np.array(acc)})
@@ -159,7 +159,7 @@ def kernel_fixtures(g, gw):
                 p = f"k{idx}_"
                 rec.update({p + "kind": np.array("twc"), p + "app": np.array(app),
                             p + "small": bins.small, p + "medium": bins.medium,
-                            p + "large": bins.large, p + "values": values, p + "aux": aux,
+                            p + "large": bins.large, p + "values": values.copy(), p + "aux": aux.copy(),
                             p + "opcode": np.array(a.opcode), p + "out": out,
                             p + "per_cta_edges": pce})
                 idx += 1
@@ -170,7 +170,7 @@ def kernel_fixtures(g, gw):
                    a.opcode, cfg.num_ctas, cfg.threads_per_cta, pce)
                 p = f"k{idx}_"
                 rec.update({p + "kind": np.array(kind), p + "app": np.array(app),
-                            p + "frontier": frontier, p + "values": values, p + "aux": aux,
+                            p + "frontier": frontier, p + "values": values.copy(), p + "aux": aux.copy(),
                             p + "opcode": np.array(a.opcode), p + "out": out,
                             p + "per_cta_edges": pce})
                 idx += 1
@@ -189,6 +189,7 @@ def main():
               "edge_factor": 16, "seed": 1, "weights_seed": 2, "runs": {}}
     labels = {}
     plan = [
+        ("rmat10", [("vertex", None), ("edge", None)], [1]),
         ("rmat10", [("alb", None), ("alb", 64), ("twc", None), ("lb", None)], [1, 2, 4]),
         ("uniform10", [("alb", None), ("alb", 64)], [1, 3]),
         ("rmat12", [("alb", None), ("alb", 256)], [1, 2, 4, 8]),
