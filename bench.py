@@ -1,0 +1,368 @@
+"""Benchmark: ALB SSSP on RMAT scale-24 (integer weights), GTEPS on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W``; N>1 is
+launched under torchrun (one rank per GPU).  Rank 0 prints ONE JSON line.
+
+Workload (BASELINE.json configs[1]): SSSP from source 0 on
+generate_rmat(24, 16, seed=1, (0.57,0.19,0.19,0.05)) with
+attach_random_weights(seed=2) integers in [1, 64]; scheduler alb (cyclic,
+threshold = KernelConfig().total_threads = 21,504).  One step = one complete
+BSP run (all rounds to convergence) of the device engine.
+
+* value  : GTEPS = edges_processed (the reference's report totals,
+           engine.py:293) x K / sum of per-step device times; inputs resident
+           in HBM; L2 flushed (512 MB write) before every step; each step timed
+           with CUDA events on the engine's stream (sg_run, SG_FLAG_TIMING);
+           max over ranks.
+* e2e    : the same metric through the C ABI with HOST buffers: per step
+           sg_graph_create from pinned CSR/weights (H2D) + sg_run + labels /
+           round log D2H, wall clock with device sync.
+* roofline: dominant kernel of a profiled run (sg_run_profiled: CUDA events
+           around every kernel) — algorithmic bytes / its time,
+           against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline: the C oracle (oracle/sg_oracle.c, a restatement of the
+           reference path) on this host, 1 thread, full workload.
+``--impl reference`` times that CPU path alone with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GTEPS for BFS/SSSP/CC/PR on RMAT power-law graphs at 1/2/4/8 B200"
+SKEWED = (0.57, 0.19, 0.19, 0.05)
+DEFAULT_THRESHOLD = 84 * 256  # KernelConfig().total_threads (simt.py:20-22)
+
+# algorithmic bytes (SURVEY §8d canonical widths)
+EDGE_BYTES = {"bfs": 8, "cc": 8, "sssp": 12, "kcore": 8, "pr": 12}
+VERTEX_BYTES = 24   # frontier id 4 + offsets 16 + snapshot label 4
+UPDATE_BYTES = 8    # label write 4 + enqueue 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--app", default="sssp", choices=["bfs", "sssp", "cc", "pr", "kcore"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--uniform", action="store_true", help="uniform RMAT probabilities")
+    ap.add_argument("--sched", default="alb", choices=["alb", "twc"])
+    ap.add_argument("--threshold", type=int, default=DEFAULT_THRESHOLD)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--extra", default="", help="comma list of extra apps to report")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(app, log):
+    """Per-kernel algorithmic bytes from the round log."""
+    eb = EDGE_BYTES[app]
+    n = log["frontier_size"].astype(np.int64)
+    m = log["active_edges"].astype(np.int64)
+    mh = log["huge_edges"].astype(np.int64)
+    ml = log["large_edges"].astype(np.int64)
+    u = log["updated"].astype(np.int64)
+    if app == "pr":
+        nv = int(n[0]) if len(n) else 0
+        return {"pull_twc": int((eb * (m - mh - ml)).sum() + 40 * nv * len(n)),
+                "pull_large": int((eb * ml).sum()), "pull_lb": int((eb * mh).sum())}
+    if app == "kcore":
+        return {"pull_twc": int((eb * (m - mh - ml) + VERTEX_BYTES * n).sum()),
+                "pull_large": int((eb * ml).sum()), "pull_lb": int((eb * mh).sum())}
+    return {"push_twc": int((eb * (m - mh - ml) + VERTEX_BYTES * n).sum()),
+            "push_large": int((eb * ml).sum()), "push_lb": int((eb * mh).sum()),
+            "advance": int((UPDATE_BYTES * u).sum())}
+
+
+def total_algorithmic_bytes(app, log, nv):
+    b = algorithmic_bytes(app, log)
+    return sum(b.values())
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch", {}).get(kernel)
+    except (ValueError, OSError):
+        return None
+
+
+def make_graph_device(sg, app, scale, uniform):
+    probs = (0.25,) * 4 if uniform else SKEWED
+    g = sg.generate_rmat(scale, 16, 1, probs)
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    return g
+
+
+def cpu_oracle_run(app, off, tgt, w, threads):
+    from oracle import oracle_c as C
+    args = C.prepare(off, tgt, w, app)
+    t0 = time.perf_counter()
+    lab, log, st = C.run(app, *args, threads=threads)
+    dt = time.perf_counter() - t0
+    return lab, log, dt
+
+
+def run_reference(a):
+    """--impl reference: the reference path (C restatement) on host cores."""
+    rank, _, world = dist_env()
+    if world > 1 and rank != 0:
+        return
+    from oracle import oracle_c as C
+    from oracle import oracle_np as O
+    threads = os.cpu_count() or 1
+    probs = (0.25,) * 4 if a.uniform else SKEWED
+    s, d = C.rmat_pairs(a.scale, 16, 1, probs, threads=threads)
+    w = O.random_weights(len(s), 2) if a.app == "sssp" else None
+    off, tgt, _ = C.csr_from_pairs(s, d, 1 << a.scale)
+    del s, d
+    args = C.prepare(off, tgt, w, a.app)
+    times, edges = [], 0
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        lab, log, st = C.run(a.app, *args, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            times.append(dt)
+            edges = int(log[:, 1].sum())
+    total = sum(times)
+    value = edges * len(times) / total / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{a.app} rmat{a.scale} ef16 seed1" + (" uniform" if a.uniform else "")
+                   + (" weights[1,64] seed2" if a.app == "sssp" else ""),
+                   "edges_processed": edges, "scheduler": "n/a (CPU restatement)"},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": "port",
+                         "sample": f"full {a.app} run on rmat{a.scale}, oracle/sg_oracle.c "
+                                   f"(OpenMP, {threads} threads)"},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    rank, local_rank, world = dist_env()
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_1911_09135_b200 as sg
+    from paper_1911_09135_b200 import native
+
+    g = make_graph_device(sg, a.app, a.scale, a.uniform)
+    dev = g.device()
+    nv, ne, _ = dev.info()
+    sched = sg.Scheduler(a.sched, threshold=a.threshold if a.sched == "alb" else None)
+    params = sg.engine._device_params(sg.apps.make_app(a.app), sched, sg.KernelConfig(), 1,
+                                      10 * nv + 256)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    for _ in range(a.warmup):
+        labels, log, ms = dev.run(params)
+    edges = int(log["active_edges"].sum())
+    rounds = len(log)
+
+    # ---------------- timed region (device-resident inputs) ----------------
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = native.kernel_launches()
+    step_ms = []
+    t_wall = time.perf_counter()
+    with Clocks(local_rank) as clk:
+        for i in range(a.steps):
+            flush.fill_(i & 0xFF)  # evict L2 (> 126 MB) between steps
+            torch.cuda.synchronize()
+            labels, log2, ms = dev.run(params)
+            step_ms.append(ms)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    launches = native.kernel_launches() - launches0
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = edges * a.steps * world / (total_ms / 1e3) / 1e9
+
+    # ---------------- e2e through the C ABI with host buffers ----------------
+    e2e = None
+    if not a.no_e2e:
+        off, tgt, w = dev.download(0, weights=(a.app == "sssp"))
+        pin = lambda x: torch.from_numpy(x).pin_memory().numpy() if x is not None else None
+        off_p, tgt_p, w_p = pin(off), pin(tgt), pin(w)
+        h2d = off_p.nbytes + tgt_p.nbytes + (w_p.nbytes if w_p is not None else 0)
+        d2h = 8 * nv + native.ROUND_DTYPE.itemsize * rounds
+        native.DeviceGraph.from_csr(off_p, tgt_p, w_p).run(params)  # warm
+        torch.cuda.synchronize()
+        e2e_s = []
+        for _ in range(max(1, min(a.steps, 3))):
+            t0 = time.perf_counter()
+            dg = native.DeviceGraph.from_csr(off_p, tgt_p, w_p)
+            lab_e, log_e, _ = dg.run(params)
+            torch.cuda.synchronize()
+            e2e_s.append(time.perf_counter() - t0)
+            del dg
+        e2e = {"value": edges / statistics.median(e2e_s) / 1e9 * world, "unit": "GTEPS",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * statistics.median(e2e_s)}
+        assert np.array_equal(lab_e, labels) or a.app == "pr"
+
+    # ---------------- roofline from a profiled run ----------------
+    _, plog, pms, kernels = dev.run(params, profile=True)
+    ab = algorithmic_bytes(a.app, plog)
+    timed = {k: v for k, v in kernels.items() if k in ab}
+    dom = max(timed, key=lambda k: timed[k][1]) if timed else None
+    peak, peak_kind = peaks()
+    roofline = None
+    if dom:
+        n_l, ms_l = kernels[dom]
+        achieved = ab[dom] / (ms_l / 1e3) / 1e9
+        traffic = ncu_traffic(dom)
+        roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
+                    "traffic": traffic, "algorithmic_bytes_per_launch": ab[dom] / max(n_l, 1),
+                    "avg_launch_ms": ms_l / max(n_l, 1), "launches": n_l,
+                    "share_of_step": ms_l / sum(v[1] for v in kernels.values()),
+                    "loop_bytes_per_s_GBps": sum(ab.values()) / (statistics.median(step_ms) / 1e3) / 1e9}
+
+    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        off, tgt, w = dev.download(0, weights=(a.app == "sssp"))
+        lab_c, log_c, dt = cpu_oracle_run(a.app, off, tgt, w, threads=1)
+        e_c = int(log_c[:, 1].sum())
+        cpu = {"value": e_c / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "port",
+               "sample": f"full {a.app} run on the same rmat{a.scale} graph, "
+                         f"oracle/sg_oracle.c single thread ({dt:.1f} s)",
+               "labels_match": bool(np.array_equal(lab_c, labels)) if a.app != "pr" else
+               float(np.max(np.abs(lab_c - labels)))}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32" if a.app in ("bfs", "sssp", "cc") else ("f64" if a.app == "pr" else "u32"),
+        "data": "synthetic (device RMAT, bit-identical to the reference's numpy generator)",
+        "config": {"workload": f"{a.app} rmat{a.scale} ef16 seed1"
+                               + (" uniform" if a.uniform else "")
+                               + (" weights[1,64] seed2" if a.app == "sssp" else "")
+                               + " source0",
+                   "scheduler": sched.describe(), "threshold": a.threshold,
+                   "num_vertices": nv, "num_edges": ne, "edges_processed": edges,
+                   "rounds": rounds, "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed (512 MB write) before every step",
+                   "timing": "sum of per-step CUDA-event durations of sg_run (one graph launch "
+                             "per BSP run), max over ranks",
+                   "wall_s_timed_region": wall},
+        "e2e": e2e,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "kernel_ms": {k: {"launches": v[0], "ms": v[1]} for k, v in kernels.items()},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -68,7 +68,10 @@ typedef struct sg_params {
   int32_t reserved;
 } sg_params;
 
-#define SG_FLAG_TIMING 1 /* fill *ms_out with the CUDA-event time of the BSP loop */
+#define SG_FLAG_TIMING 1  /* fill *ms_out with the CUDA-event time of the BSP loop */
+#define SG_FLAG_PROFILE 2 /* host-driven rounds with CUDA events around every kernel
+                             (per-kernel times via sg_run_profiled); default is one
+                             CUDA-graph launch whose WHILE node runs all rounds */
 
 typedef struct sg_round { /* one BSP round (engine.py:116-163) */
   int64_t frontier_size;  /* RoundRecord.frontier_size */
@@ -76,6 +79,7 @@ typedef struct sg_round { /* one BSP round (engine.py:116-163) */
   int64_t huge_count;     /* |huge| after inspection (schedulers.py:291) */
   int64_t huge_edges;     /* PrefixWork.total_edges (lb kernel edges) */
   int64_t large_count;    /* CTA-bin vertices */
+  int64_t large_edges;    /* edges of CTA-bin vertices */
   int64_t updated;        /* vertices whose label changed (next frontier / dying) */
   int64_t comm_sent;      /* engine.py:225-229 (devices > 1) */
   int64_t comm_broadcast; /* engine.py:232-234 (devices > 1) */
@@ -110,6 +114,16 @@ void sg_graph_destroy(sg_graph *g);
 /* --- run level: engine.run (engine.py:190-246) -------------------------- */
 int sg_run(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
            int64_t rounds_cap, int64_t *nrounds, double *ms_out);
+
+typedef struct sg_kernel_time { /* per-kernel totals of a profiled run */
+  char name[32];
+  int64_t launches;
+  double ms; /* sum of CUDA-event durations */
+} sg_kernel_time;
+
+int sg_run_profiled(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
+                    int64_t rounds_cap, int64_t *nrounds, double *ms_out, sg_kernel_time *kt,
+                    int32_t kt_cap, int32_t *nkt);
 
 /* --- kernel level: the reference plugin API (_kernels_py.py:88-201) ------ */
 int sg_lb_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,

@@ -99,3 +99,23 @@ def prepare(off, tgt, weights, app):
     if app == "sssp" and weights is not None:
         w = weights.astype(np.float64)
     return off, tgt, w, off, tgt
+
+
+def csr_from_pairs(src, dst, nv, weights=None):
+    """Stable counting-sort CSR (== graph.py:63-76 from_edges)."""
+    L = lib()
+    if not hasattr(L, "_csr_sig"):
+        P = ctypes.c_void_p
+        L.sgo_csr_from_pairs.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, P, P, P]
+        L.sgo_csr_from_pairs.restype = None
+        L._csr_sig = True
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    off = np.empty(nv + 1, dtype=np.int64)
+    tgt = np.empty(len(src), dtype=np.int32)
+    w_out = None
+    if weights is not None:
+        weights = np.ascontiguousarray(weights, dtype=np.int64)
+        w_out = np.empty(len(src), dtype=np.int64)
+    L.sgo_csr_from_pairs(len(src), nv, _p(src), _p(dst), _p(weights), _p(off), _p(tgt), _p(w_out))
+    return off, tgt, w_out

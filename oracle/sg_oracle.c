@@ -261,3 +261,20 @@ void sgo_rmat_pairs(int scale, int64_t ne, uint64_t st_hi, uint64_t st_lo, uint6
     }
   }
 }
+
+/* Graph.from_edges (graph.py:63-76): stable counting sort by source.
+ * A sequential scatter in input order is stable by construction. */
+void sgo_csr_from_pairs(int64_t ne, int64_t nv, const int32_t *src, const int32_t *dst,
+                        const int64_t *w_in, int64_t *off, int32_t *tgt, int64_t *w_out) {
+  memset(off, 0, sizeof(int64_t) * (size_t)(nv + 1));
+  for (int64_t i = 0; i < ne; ++i) off[src[i] + 1]++;
+  for (int64_t v = 0; v < nv; ++v) off[v + 1] += off[v];
+  int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nv ? nv : 1));
+  memcpy(cur, off, sizeof(int64_t) * (size_t)nv);
+  for (int64_t i = 0; i < ne; ++i) {
+    int64_t p = cur[src[i]]++;
+    tgt[p] = dst[i];
+    if (w_in) w_out[p] = w_in[i];
+  }
+  free(cur);
+}

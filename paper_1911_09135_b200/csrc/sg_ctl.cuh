@@ -27,12 +27,13 @@ struct Ctl {
   unsigned long long delta_bits;  // pr: max |new - old| (double bits, >= 0)
   unsigned long long comm_sent;
   unsigned long long comm_bcast;
+  unsigned long long large_edges;  // edges of CTA-bin vertices this round
 };
 
 // one record per round, layout == sg_round (include/simtgraph_cuda.h)
 struct RoundStat {
-  long long frontier_size, active_edges, huge_count, huge_edges, large_count, updated,
-      comm_sent, comm_broadcast;
+  long long frontier_size, active_edges, huge_count, huge_edges, large_count, large_edges,
+      updated, comm_sent, comm_broadcast;
 };
 static_assert(sizeof(RoundStat) == sizeof(sg_round), "RoundStat must mirror sg_round");
 

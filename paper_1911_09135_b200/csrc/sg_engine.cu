@@ -1,13 +1,18 @@
 // sg_engine.cu — the BSP driver (reference engine.py:190-246) on the device.
 //
-// One round = a fixed sequence of kernels whose sizes live in device memory
-// (Ctl), captured once into a CUDA graph and replayed; the host only checks
-// the `done` flag after batches of rounds (1, 2, 4, ... 32), and rounds
-// issued past the end exit immediately.  Results: float64 labels + one
-// RoundStat per round (frontier size, active edges, ... == RoundRecord).
+// A round is a fixed sequence of kernels whose sizes live in device memory
+// (Ctl).  It is captured once as the body of a CUDA-graph WHILE node; the
+// round's last kernel evaluates the loop test (frontier empty / pr converged
+// / round budget) and sets the node's condition, so the complete BSP loop is
+// ONE graph launch with no host round trip.  SG_FLAG_PROFILE instead drives
+// rounds from the host with CUDA events around every kernel (per-kernel
+// times for the roofline report).  Results: float64 labels + one RoundStat
+// per round (frontier size, active edges, ... == RoundRecord).
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <limits>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -37,6 +42,8 @@ const SmInfo &sm_info() {
 
 namespace {
 
+constexpr int64_t kNoHuge = std::numeric_limits<int64_t>::max();
+
 template <class K>
 int occupancy_grid(K kernel, int block, int cap_per_sm = 8) {
   static std::mutex mu;
@@ -57,6 +64,66 @@ inline int grid_n(int64_t n, int block = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sm_info().sms * 32));
 }
 
+// Launches round kernels: plain (graph capture) or bracketed by CUDA events.
+struct Launcher {
+  bool profile = false;
+  std::vector<std::tuple<const char *, cudaEvent_t, cudaEvent_t>> pending;
+  std::vector<cudaEvent_t> pool;
+  std::map<std::string, std::pair<int64_t, double>> totals;
+  std::vector<std::string> order;
+
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    SG_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  template <class K, class... A>
+  void go(const char *name, K kernel, int grid, int block, cudaStream_t s, A... args) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (profile) {
+      e0 = ev(), e1 = ev();
+      SG_CUDA(cudaEventRecord(e0, s));
+    }
+    kernel<<<grid, block, 0, s>>>(args...);
+    SG_CUDA(cudaGetLastError());
+    if (profile) {
+      SG_CUDA(cudaEventRecord(e1, s));
+      pending.emplace_back(name, e0, e1);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+  }
+  void collect() {
+    for (auto &t : pending) {
+      float ms = 0;
+      SG_CUDA(cudaEventElapsedTime(&ms, std::get<1>(t), std::get<2>(t)));
+      std::string n = std::get<0>(t);
+      if (!totals.count(n)) order.push_back(n);
+      totals[n].first += 1;
+      totals[n].second += ms;
+      pool.push_back(std::get<1>(t));
+      pool.push_back(std::get<2>(t));
+    }
+    pending.clear();
+  }
+  ~Launcher() {
+    for (auto &t : pending) pool.push_back(std::get<1>(t)), pool.push_back(std::get<2>(t));
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// round context handed to every round body
+struct RoundCtx {
+  Launcher &L;
+  cudaStream_t s;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+
 // ------------------------------------------------------------ init kernels --
 template <class T>
 __global__ void k_fill(T *p, int64_t n, T v) {
@@ -71,6 +138,12 @@ __global__ void k_iota32(uint32_t *p, int64_t n) {
 template <class T>
 __global__ void k_set1(T *p, int64_t i, T v) { p[i] = v; }
 
+__global__ void k_ctl_init(Ctl *ctl, int32_t dense, uint32_t fsize) {
+  *ctl = Ctl{};
+  ctl->dense = dense;
+  ctl->fsize = fsize;
+}
+
 __global__ void k_labels_u32(const uint32_t *lab, int64_t n, double *out) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
@@ -82,63 +155,81 @@ __global__ void k_labels_alive(const uint8_t *a, int64_t n, double *out) {
     out[i] = a[i] ? 1.0 : 0.0;
 }
 
-// inv_outdeg (apps.py:158-161)
-__global__ void k_inv_outdeg(const int64_t *off, int64_t n, double *inv) {
+// inv_outdeg (apps.py:158-161), rank_0 = 1-d and round-0 aux = rank*inv (apps.py:162,176)
+__global__ void k_pr_init(const int64_t *off, int64_t n, double omd, double *inv, double *rank,
+                          double *aux) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += st) {
     int64_t d = off[v + 1] - off[v];
-    inv[v] = d > 0 ? 1.0 / (double)d : 0.0;
-  }
-}
-__global__ void k_pr_init(const double *inv, int64_t n, double omd, double *rank, double *aux) {
-  int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += st) {
+    double iv = d > 0 ? 1.0 / (double)d : 0.0;
+    inv[v] = iv;
     rank[v] = omd;
-    aux[v] = __dmul_rn(omd, inv[v]);  // round_aux of round 0 (apps.py:176-177)
+    aux[v] = __dmul_rn(omd, iv);
   }
 }
-// gain[v] = sum_{u->v} inv[u] accumulated in CSC (== CSR edge) order, exactly
-// as np.bincount does (apps.py:166-168): one warp per row loads 32 terms and
-// every lane folds them sequentially through shuffles.
+// gain[v] = sum_{u->v} inv[u] in CSC (== CSR edge) order, exactly as
+// np.bincount accumulates it (apps.py:166-168): a warp loads 32 terms, every
+// lane folds them sequentially through shuffles; max over v by atomicMax.
 __global__ void k_pr_gain_max(const int64_t *off, const uint32_t *col, int64_t n,
                               const double *inv, unsigned long long *maxbits) {
   int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double best = 0.0;
   for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
     double acc = 0.0;
-    for (int64_t b = off[v]; b < off[v + 1]; b += 32) {
+    const int64_t e = off[v + 1];
+    for (int64_t b = off[v]; b < e; b += 32) {
       int64_t j = b + lane_id();
-      double x = j < off[v + 1] ? inv[col[j]] : 0.0;
-      int cnt = (int)min((int64_t)32, off[v + 1] - b);
+      double x = j < e ? inv[col[j]] : 0.0;
+      int cnt = (int)min((int64_t)32, e - b);
       for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, __shfl_sync(kFull, x, t));
     }
     best = acc > best ? acc : best;
   }
-  if (lane_id() == 0 && best > 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(best));
+  if (lane_id() == 0 && best > 0)
+    atomicMax(maxbits, (unsigned long long)__double_as_longlong(best));
 }
 
 // static bins of a dense pull view (pr): CTA-bin rows and huge rows
 __global__ void k_static_bins(const int64_t *off, uint32_t n, int64_t thr, uint32_t *largeq,
                               uint32_t *hugeq, Ctl *ctl) {
   uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long le = 0;
   for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < n; b += st) {
     uint64_t v = b + threadIdx.x;
     int64_t d = v < n ? off[v + 1] - off[v] : 0;
     bool huge = v < n && d >= thr;
     bool large = v < n && !huge && d >= (int64_t)kLarge;
+    if (large) le += (unsigned long long)d;
     warp_append(huge, (uint32_t)v, hugeq, &ctl->nhuge);
     warp_append(large, (uint32_t)v, largeq, &ctl->nlarge);
   }
+  le = warp_sum(le);
+  if (lane_id() == 0 && le) atomicAdd(&ctl->large_edges, le);
 }
 
 // ------------------------------------------------------- advance kernels --
+struct Loop {
+  int64_t limit, max_rounds;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+
+__device__ __forceinline__ void loop_test(Ctl *ctl, uint32_t round, bool empty, const Loop &lp) {
+  if (empty) ctl->done = 1;
+  else if ((int64_t)round + 1 >= lp.limit)
+    ctl->error = (int64_t)round + 1 >= lp.max_rounds ? SG_ECONVERGE : SG_ENOMEM, ctl->done = 1;
+  if (lp.use_cond) cudaGraphSetConditional(lp.cond, ctl->done ? 0u : 1u);
+}
+
 // commit (snapshot := label for changed vertices) + round bookkeeping
 template <class L, bool COMMIT>
-__global__ void __launch_bounds__(256) k_push_advance(PushArgs a, L *lab, L *snap,
-                                                      int64_t max_rounds) {
+__global__ void __launch_bounds__(256) k_push_advance(PushArgs a, L *lab, L *snap, Loop lp) {
   __shared__ bool last;
   Ctl *ctl = a.ctl;
-  if (ctl->done) return;
+  if (ctl->done) {
+    if (lp.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(lp.cond, 0u);
+    return;
+  }
   const uint32_t round = ctl->round;
   const uint32_t nn = ctl->nsize;
   if (COMMIT) {
@@ -160,18 +251,18 @@ __global__ void __launch_bounds__(256) k_push_advance(PushArgs a, L *lab, L *sna
   s.huge_count = ctl->nhuge;
   s.huge_edges = (long long)ctl->huge_edges;
   s.large_count = ctl->nlarge;
+  s.large_edges = (long long)ctl->large_edges;
   s.updated = nn;
   s.comm_sent = (long long)ctl->comm_sent;
   s.comm_broadcast = (long long)ctl->comm_bcast;
   ctl->fsize = nn;
   ctl->nsize = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
-  ctl->edges = ctl->huge_edges = ctl->comm_sent = ctl->comm_bcast = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_sent = ctl->comm_bcast = 0;
   ctl->dense = 0;
   ctl->ticket = 0;
   ctl->round = round + 1;
-  if (nn == 0) ctl->done = 1;
-  else if ((int64_t)round + 1 >= max_rounds) ctl->error = SG_ECONVERGE, ctl->done = 1;
+  loop_test(ctl, round, nn == 0, lp);
   __threadfence();
 }
 
@@ -190,28 +281,34 @@ __global__ void k_kcore_kill(PullArgs a, uint8_t *alive) {
     s.huge_count = ctl->nhuge;
     s.huge_edges = (long long)ctl->huge_edges;
     s.large_count = ctl->nlarge;
+    s.large_edges = (long long)ctl->large_edges;
     s.updated = nd;
     s.comm_sent = 0;
     s.comm_broadcast = 0;
-    // the neighbour walk reuses the CTA-bin queue
-    ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
-    ctl->huge_edges = 0;
   }
 }
-
-__global__ void k_kcore_advance(Ctl *ctl, int64_t max_rounds) {
+// the neighbour walk reuses the CTA-bin queue: reset after the kill kernel
+__global__ void k_kcore_reset(Ctl *ctl) {
   if (ctl->done) return;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
+  ctl->huge_edges = ctl->large_edges = 0;
+}
+
+__global__ void k_kcore_advance(Ctl *ctl, Loop lp) {
+  if (ctl->done) {
+    if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+    return;
+  }
   const uint32_t round = ctl->round;
   const uint32_t nd = ctl->ndying, nn = ctl->nsize;
   ctl->fsize = nn;
   ctl->nsize = 0;
   ctl->ndying = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
-  ctl->edges = ctl->huge_edges = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
   ctl->dense = 0;
   ctl->round = round + 1;
-  if (nd == 0 || nn == 0) ctl->done = 1;  // apps.py:223-232
-  else if ((int64_t)round + 1 >= max_rounds) ctl->error = SG_ECONVERGE, ctl->done = 1;
+  loop_test(ctl, round, nd == 0 || nn == 0, lp);  // apps.py:223-232
 }
 
 // ------------------------------------------------------------ run state --
@@ -264,253 +361,235 @@ struct RunBufs {
   }
 };
 
-template <class T>
-void fill(T *p, int64_t n, T v, cudaStream_t s) {
-  if (n > 0) SG_LAUNCH(k_fill<T>, grid_n(n), 256, 0, s, p, n, v);
-}
-
-// Capture `round` once, replay until the device says done.
-template <class F>
-void bsp_loop(RunBufs &rb, F &&round, cudaStream_t s, int64_t max_rounds, int64_t *issued_out) {
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  SG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  round(s);
-  SG_CUDA(cudaStreamEndCapture(s, &graph));
-  SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-  Ctl *h = nullptr;
-  SG_CUDA(cudaMallocHost(&h, sizeof(Ctl)));
-  int64_t issued = 0, batch = 1;
-  int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
-  bool ok = true;
-  for (;;) {
-    int64_t nb = std::min<int64_t>(batch, std::max<int64_t>(limit - issued, 1));
-    for (int64_t b = 0; b < nb; ++b) {
-      if (cudaGraphLaunch(exec, s) != cudaSuccess) { ok = false; break; }
-      g_launches.fetch_add(4, std::memory_order_relaxed);
-      ++issued;
-    }
-    if (!ok) break;
-    if (cudaMemcpyAsync(h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) { ok = false; break; }
-    if (h->done) break;
-    if (issued >= limit) { ok = false; break; }
-    batch = std::min<int64_t>(batch * 2, 32);
+// A prepared run: buffers allocated, nothing launched yet.
+struct Program {
+  std::function<void(Launcher &, cudaStream_t)> init;  // device state init (timed)
+  std::function<void(RoundCtx &)> round;              // one BSP round
+  std::function<void(Launcher &, cudaStream_t)> finish;  // labels -> out (untimed)
+  std::vector<std::shared_ptr<void>> keep;
+  template <class T>
+  T *buf(int64_t n) {
+    auto b = std::make_shared<DBuf<T>>(std::max<int64_t>(n, 1));
+    keep.push_back(b);
+    return b->p;
   }
-  bool capped = !ok && issued >= limit;
-  cudaFreeHost(h);
-  cudaGraphExecDestroy(exec);
-  cudaGraphDestroy(graph);
-  SG_CUDA(cudaGetLastError());
-  if (capped) throw Error(SG_ECONVERGE, "round budget exhausted");
-  if (!ok) SG_CUDA(cudaDeviceSynchronize());
-  *issued_out = issued;
+};
+
+template <class T>
+void fill(Launcher &L, T *p, int64_t n, T v, cudaStream_t s) {
+  if (n > 0) L.go("init", k_fill<T>, grid_n(n), 256, s, p, n, v);
 }
 
 // ----------------------------------------------------------------- apps --
 template <class Op>
-void push_round(const PushArgs &a, const Op &op, bool blocked, cudaStream_t s) {
-  SG_LAUNCH(k_push_twc<Op>, occupancy_grid(k_push_twc<Op>, kTB), kTB, 0, s, a, op);
-  SG_LAUNCH(k_push_large<Op>, occupancy_grid(k_push_large<Op>, kTB), kTB, 0, s, a, op);
-  if (a.threshold != std::numeric_limits<int64_t>::max()) {
-    SG_LAUNCH(k_huge_prefix<Op>, 1, 1024, 0, s, a, op);
+void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
+  c.L.go("push_twc", k_push_twc<Op>, occupancy_grid(k_push_twc<Op>, kTB), kTB, c.s, a, op);
+  c.L.go("push_large", k_push_large<Op>, occupancy_grid(k_push_large<Op>, kTB), kTB, c.s, a, op);
+  if (a.threshold != kNoHuge) {
+    c.L.go("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
     if (blocked)
-      SG_LAUNCH((k_push_lb<Op, true>), occupancy_grid(k_push_lb<Op, true>, kTB), kTB, 0, s, a, op);
+      c.L.go("push_lb", k_push_lb<Op, true>, occupancy_grid(k_push_lb<Op, true>, kTB), kTB, c.s, a,
+             op);
     else
-      SG_LAUNCH((k_push_lb<Op, false>), occupancy_grid(k_push_lb<Op, false>, kTB), kTB, 0, s, a,
-                op);
+      c.L.go("push_lb", k_push_lb<Op, false>, occupancy_grid(k_push_lb<Op, false>, kTB), kTB, c.s,
+             a, op);
   }
 }
 
 template <class Op>
-void pull_round(const PullArgs &a, const Op &op, bool blocked, typename Op::A *hacc,
-                cudaStream_t s) {
-  SG_LAUNCH(k_pull_twc<Op>, occupancy_grid(k_pull_twc<Op>, kTB), kTB, 0, s, a, op);
-  SG_LAUNCH(k_pull_large<Op>, occupancy_grid(k_pull_large<Op>, kTB), kTB, 0, s, a, op);
-  if (a.threshold != std::numeric_limits<int64_t>::max()) {
-    if (a.dynamic_bins) SG_LAUNCH(k_pull_prefix, 1, 1024, 0, s, a);
+void pull_round(RoundCtx &c, const PullArgs &a, const Op &op, bool blocked, typename Op::A *hacc) {
+  c.L.go("pull_twc", k_pull_twc<Op>, occupancy_grid(k_pull_twc<Op>, kTB), kTB, c.s, a, op);
+  c.L.go("pull_large", k_pull_large<Op>, occupancy_grid(k_pull_large<Op>, kTB), kTB, c.s, a, op);
+  if (a.threshold != kNoHuge) {
+    if (a.dynamic_bins) c.L.go("huge_prefix", k_pull_prefix, 1, 1024, c.s, a);
     if (blocked)
-      SG_LAUNCH((k_pull_lb<Op, true>), occupancy_grid(k_pull_lb<Op, true>, kTB), kTB, 0, s, a, op,
-                hacc);
+      c.L.go("pull_lb", k_pull_lb<Op, true>, occupancy_grid(k_pull_lb<Op, true>, kTB), kTB, c.s, a,
+             op, hacc);
     else
-      SG_LAUNCH((k_pull_lb<Op, false>), occupancy_grid(k_pull_lb<Op, false>, kTB), kTB, 0, s, a,
-                op, hacc);
+      c.L.go("pull_lb", k_pull_lb<Op, false>, occupancy_grid(k_pull_lb<Op, false>, kTB), kTB, c.s,
+             a, op, hacc);
   }
 }
 
-struct RunOut {
-  DBuf<double> labels;
-  int64_t rounds = 0;
-};
+Loop loop_of(const RunBufs &rb, int64_t max_rounds, const RoundCtx &c) {
+  return Loop{std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds, c.cond, c.use_cond};
+}
 
-void run_push_min(Graph &g, const sg_params &p, RunBufs &rb, RunOut &ro, cudaStream_t s,
-                  int64_t thr, int64_t max_rounds) {
+void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d,
+                   int64_t thr, int64_t max_rounds) {
   const bool cc = p.app == SG_APP_CC;
   const View &v = cc ? g.sym() : g.csr;
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
-  PushArgs a = rb.push_args(v, thr);
-  Ctl init{};
-  if (cc) {
-    init.dense = 1;
-    init.fsize = (uint32_t)nv;
-  } else {
-    init.fsize = 1;
-    SG_LAUNCH(k_set1<uint32_t>, 1, 1, 0, s, rb.q0.p, 0, (uint32_t)p.source);
-  }
-  SG_CUDA(cudaMemcpyAsync(rb.ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-  ro.labels.alloc(std::max<int64_t>(nv, 1));
+  const PushArgs a = rb.push_args(v, thr);
   const bool blocked = p.blocked != 0;
+  const int64_t src = p.source;
+  Ctl *ctl = rb.ctl.p;
+  uint32_t *q0 = rb.q0.p;
+  auto init_ctl = [=](Launcher &L, cudaStream_t s) {
+    L.go("init", k_ctl_init, 1, 1, s, ctl, (int32_t)cc, cc ? (uint32_t)nv : 1u);
+    if (!cc) L.go("init", k_set1<uint32_t>, 1, 1, s, q0, (int64_t)0, (uint32_t)src);
+  };
 
   if (p.app == SG_APP_BFS) {
-    DBuf<uint32_t> lab(std::max<int64_t>(nv, 1)), vis((nv + 31) / 32 + 1);
-    fill<uint32_t>(lab.p, nv, kInf32, s);
-    fill<uint32_t>(vis.p, (nv + 31) / 32 + 1, 0u, s);
-    SG_LAUNCH(k_set1<uint32_t>, 1, 1, 0, s, lab.p, p.source, 0u);
-    SG_LAUNCH(k_set1<uint32_t>, 1, 1, 0, s, vis.p, p.source >> 5, 1u << (p.source & 31));
-    OpBfs op{lab.p, vis.p};
-    bsp_loop(rb, [&](cudaStream_t st) {
-      push_round(a, op, blocked, st);
-      SG_LAUNCH((k_push_advance<uint32_t, false>), 1, 256, 0, st, a, lab.p, lab.p, max_rounds);
-    }, s, max_rounds, &ro.rounds);
-    SG_LAUNCH(k_labels_u32, grid_n(nv), 256, 0, s, lab.p, nv, ro.labels.p);
-    SG_CUDA(cudaStreamSynchronize(s));
+    uint32_t *lab = P.buf<uint32_t>(nv), *vis = P.buf<uint32_t>((nv + 31) / 32 + 1);
+    OpBfs op{lab, vis};
+    P.init = [=](Launcher &L, cudaStream_t s) {
+      init_ctl(L, s);
+      fill<uint32_t>(L, lab, nv, kInf32, s);
+      fill<uint32_t>(L, vis, (nv + 31) / 32 + 1, 0u, s);
+      L.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
+      L.go("init", k_set1<uint32_t>, 1, 1, s, vis, src >> 5, 1u << (src & 31));
+    };
+    P.round = [=, &rb](RoundCtx &c) {
+      push_round(c, a, op, blocked);
+      c.L.go("advance", k_push_advance<uint32_t, false>, 1, 256, c.s, a, lab, lab,
+             loop_of(rb, max_rounds, c));
+    };
+    P.finish = [=](Launcher &L, cudaStream_t s) {
+      L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
+    };
     return;
   }
-
   // sssp / cc: 32-bit labels when every path sum provably fits, else f64 bits
-  bool weighted = p.app == SG_APP_SSSP && g.weighted;
+  const bool weighted = p.app == SG_APP_SSSP && g.weighted;
   bool use32 = true;
   if (weighted) {
-    if (g.wmin < 0) throw Error(SG_ECONFIG, "sssp requires non-negative weights");
     double bound = (double)g.wmax * (double)std::max<int64_t>(nv - 1, 1);
     use32 = g.w32.p != nullptr && bound < 4294967295.0;
   }
   if (use32) {
-    DBuf<uint32_t> lab(std::max<int64_t>(nv, 1)), snap(std::max<int64_t>(nv, 1));
-    if (cc) {
-      SG_LAUNCH(k_iota32, grid_n(nv), 256, 0, s, lab.p, nv);
-      SG_LAUNCH(k_iota32, grid_n(nv), 256, 0, s, snap.p, nv);
-    } else {
-      fill<uint32_t>(lab.p, nv, kInf32, s);
-      fill<uint32_t>(snap.p, nv, kInf32, s);
-      SG_LAUNCH(k_set1<uint32_t>, 1, 1, 0, s, lab.p, p.source, 0u);
-      SG_LAUNCH(k_set1<uint32_t>, 1, 1, 0, s, snap.p, p.source, 0u);
-    }
-    auto go = [&](auto op) {
-      using Op = decltype(op);
-      bsp_loop(rb, [&](cudaStream_t st) {
-        push_round(a, op, blocked, st);
-        SG_LAUNCH((k_push_advance<uint32_t, true>), grid_n(nv, 256), 256, 0, st, a, lab.p,
-                  snap.p, max_rounds);
-      }, s, max_rounds, &ro.rounds);
-      (void)sizeof(Op);
+    uint32_t *lab = P.buf<uint32_t>(nv), *snap = P.buf<uint32_t>(nv);
+    P.init = [=](Launcher &L, cudaStream_t s) {
+      init_ctl(L, s);
+      if (cc) {
+        L.go("init", k_iota32, grid_n(nv), 256, s, lab, nv);
+        L.go("init", k_iota32, grid_n(nv), 256, s, snap, nv);
+      } else {
+        fill<uint32_t>(L, lab, nv, kInf32, s);
+        fill<uint32_t>(L, snap, nv, kInf32, s);
+        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
+        L.go("init", k_set1<uint32_t>, 1, 1, s, snap, src, 0u);
+      }
     };
-    if (cc) go(OpMin32<0>{lab.p, snap.p, nullptr});
-    else if (!weighted) go(OpMin32<1>{lab.p, snap.p, nullptr});
-    else go(OpMin32<2>{lab.p, snap.p, g.w32.p});
-    SG_LAUNCH(k_labels_u32, grid_n(nv), 256, 0, s, lab.p, nv, ro.labels.p);
+    auto set_round = [&](auto op) {
+      P.round = [=, &rb](RoundCtx &c) {
+        push_round(c, a, op, blocked);
+        c.L.go("advance", k_push_advance<uint32_t, true>, grid_n(nv, 256), 256, c.s, a, lab, snap,
+               loop_of(rb, max_rounds, c));
+      };
+    };
+    if (cc) set_round(OpMin32<0>{lab, snap, nullptr});
+    else if (!weighted) set_round(OpMin32<1>{lab, snap, nullptr});
+    else set_round(OpMin32<2>{lab, snap, g.w32.p});
+    P.finish = [=](Launcher &L, cudaStream_t s) {
+      L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
+    };
   } else {
-    DBuf<unsigned long long> lab(std::max<int64_t>(nv, 1)), snap(std::max<int64_t>(nv, 1));
-    const unsigned long long inf = 0x7ff0000000000000ull;
-    fill<unsigned long long>(lab.p, nv, inf, s);
-    fill<unsigned long long>(snap.p, nv, inf, s);
-    SG_LAUNCH(k_set1<unsigned long long>, 1, 1, 0, s, lab.p, p.source, 0ull);
-    SG_LAUNCH(k_set1<unsigned long long>, 1, 1, 0, s, snap.p, p.source, 0ull);
-    OpMinF64 op{lab.p, snap.p, weighted ? g.w64.p : nullptr};
-    bsp_loop(rb, [&](cudaStream_t st) {
-      push_round(a, op, blocked, st);
-      SG_LAUNCH((k_push_advance<unsigned long long, true>), grid_n(nv, 256), 256, 0, st, a,
-                lab.p, snap.p, max_rounds);
-    }, s, max_rounds, &ro.rounds);
-    SG_CUDA(cudaMemcpyAsync(ro.labels.p, lab.p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s));
+    using U = unsigned long long;
+    U *lab = P.buf<U>(nv), *snap = P.buf<U>(nv);
+    const U inf = 0x7ff0000000000000ull;
+    P.init = [=](Launcher &L, cudaStream_t s) {
+      init_ctl(L, s);
+      fill<U>(L, lab, nv, inf, s);
+      fill<U>(L, snap, nv, inf, s);
+      L.go("init", k_set1<U>, 1, 1, s, lab, src, 0ull);
+      L.go("init", k_set1<U>, 1, 1, s, snap, src, 0ull);
+    };
+    OpMinF64 op{lab, snap, weighted ? g.w64.p : nullptr};
+    P.round = [=, &rb](RoundCtx &c) {
+      push_round(c, a, op, blocked);
+      c.L.go("advance", k_push_advance<U, true>, grid_n(nv, 256), 256, c.s, a, lab, snap,
+             loop_of(rb, max_rounds, c));
+    };
+    P.finish = [=](Launcher &, cudaStream_t s) {
+      SG_CUDA(cudaMemcpyAsync(labels_d, lab, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s));
+    };
   }
-  SG_CUDA(cudaStreamSynchronize(s));
 }
 
-void run_pr(Graph &g, const sg_params &p, RunBufs &rb, RunOut &ro, cudaStream_t s, int64_t thr,
-            int64_t max_rounds) {
+void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d, int64_t thr,
+             int64_t max_rounds) {
   const View &v = g.csc();
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
-  PullArgs a = rb.pull_args(v, thr, 0);
-  ro.labels.alloc(std::max<int64_t>(nv, 1));
-  DBuf<double> inv(std::max<int64_t>(nv, 1)), aux0(std::max<int64_t>(nv, 1)),
-      aux1(std::max<int64_t>(nv, 1)), hacc(std::max<int64_t>(nv, 1));
-  DBuf<unsigned long long> gmax(1);
+  const PullArgs a = rb.pull_args(v, thr, 0);
+  double *inv = P.buf<double>(nv), *aux0 = P.buf<double>(nv), *aux1 = P.buf<double>(nv),
+         *hacc = P.buf<double>(nv);
+  unsigned long long *gmax = P.buf<unsigned long long>(1);
   const double d = p.damping, omd = 1.0 - p.damping;
-  SG_LAUNCH(k_inv_outdeg, grid_n(nv), 256, 0, s, g.csr.off.p, nv, inv.p);
-  SG_LAUNCH(k_pr_init, grid_n(nv), 256, 0, s, inv.p, nv, omd, ro.labels.p, aux0.p);
-  fill<double>(hacc.p, nv, 0.0, s);
-  SG_CUDA(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned long long), s));
-  double worst = 0.0;
-  if (g.ne) {
-    SG_LAUNCH(k_pr_gain_max, grid_n(nv * 32), 256, 0, s, v.off.p, v.col.p, nv, inv.p, gmax.p);
-    unsigned long long gb = 0;
-    SG_CUDA(cudaMemcpyAsync(&gb, gmax.p, sizeof(gb), cudaMemcpyDeviceToHost, s));
-    SG_CUDA(cudaStreamSynchronize(s));
-    double gm;
-    std::memcpy(&gm, &gb, 8);
-    worst = d * gm;
-  }
-  const double eps_stop = p.tol / std::max(1.0, worst);  // apps.py:171
-  Ctl init{};
-  init.dense = 1;
-  init.fsize = (uint32_t)nv;
-  SG_CUDA(cudaMemcpyAsync(rb.ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-  SG_LAUNCH(k_static_bins, grid_n(nv), 256, 0, s, v.off.p, (uint32_t)nv, thr, rb.largeq.p,
-            rb.hugeq.p, rb.ctl.p);
-  if (thr != std::numeric_limits<int64_t>::max()) SG_LAUNCH(k_pull_prefix, 1, 1024, 0, s, a);
-  PrOp op{aux0.p, aux1.p, aux1.p, aux0.p, ro.labels.p, inv.p, d, omd};
+  const int64_t *csr_off = g.csr.off.p;
+  Ctl *ctl = rb.ctl.p;
+  uint32_t *largeq = rb.largeq.p, *hugeq = rb.hugeq.p;
+  const int64_t *voff = v.off.p;
+  const uint32_t *vcol = v.col.p;
+  const int64_t vne = v.ne;
+  P.init = [=](Launcher &L, cudaStream_t s) {
+    L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
+    L.go("init", k_pr_init, grid_n(nv), 256, s, csr_off, nv, omd, inv, labels_d, aux0);
+    fill<double>(L, hacc, nv, 0.0, s);
+    fill<unsigned long long>(L, gmax, 1, 0ull, s);
+    if (vne) L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax);
+    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, (uint32_t)nv, thr, largeq, hugeq, ctl);
+    if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
+  };
+  PrOp op{aux0, aux1, aux1, aux0, labels_d, inv, d, omd};
   const bool blocked = p.blocked != 0;
-  bsp_loop(rb, [&](cudaStream_t st) {
-    pull_round(a, op, blocked, hacc.p, st);
-    SG_LAUNCH((k_pull_finish<PrOp, true>), 1, 1024, 0, st, a, op, hacc.p, eps_stop, v.ne,
-              max_rounds);
-  }, s, max_rounds, &ro.rounds);
-  SG_CUDA(cudaStreamSynchronize(s));
+  const int64_t ne = v.ne;
+  const double tol = p.tol;
+  P.round = [=, &rb](RoundCtx &c) {
+    pull_round(c, a, op, blocked, hacc);
+    PrStop stop{gmax, d, tol, ne, std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds, c.cond,
+                c.use_cond};
+    c.L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, c.s, a, op, hacc, stop);
+  };
+  P.finish = [](Launcher &, cudaStream_t) {};
 }
 
-void run_kcore(Graph &g, const sg_params &p, RunBufs &rb, RunOut &ro, cudaStream_t s, int64_t thr,
-               int64_t max_rounds) {
-  if (p.k < 1) throw Error(SG_ECONFIG, "k must be >= 1");
+void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d,
+                int64_t thr, int64_t max_rounds) {
   const View &v = g.sym();  // count rows: CSC(sym) and CSR(sym) rows hold the same multiset
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   rb.dying.alloc(std::max<int64_t>(nv, 1));
-  PullArgs a = rb.pull_args(v, thr, 1);
-  PushArgs w = rb.push_args(v, std::numeric_limits<int64_t>::max());
+  const PullArgs a = rb.pull_args(v, thr, 1);
+  PushArgs w = rb.push_args(v, kNoHuge);
   w.src_mode = 1;
-  ro.labels.alloc(std::max<int64_t>(nv, 1));
-  DBuf<uint8_t> alive(std::max<int64_t>(nv, 1));
-  DBuf<uint32_t> mark(std::max<int64_t>(nv, 1)), hcnt(std::max<int64_t>(nv, 1));
-  fill<uint8_t>(alive.p, nv, (uint8_t)1, s);
-  fill<uint32_t>(mark.p, nv, 0u, s);
-  fill<uint32_t>(hcnt.p, nv, 0u, s);
-  Ctl init{};
-  init.dense = 1;
-  init.fsize = (uint32_t)nv;
-  SG_CUDA(cudaMemcpyAsync(rb.ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-  KcOp op{alive.p, (uint32_t)std::min<int64_t>(p.k, 0xffffffffLL)};
-  OpMark mop{alive.p, mark.p};
+  uint8_t *alive = P.buf<uint8_t>(nv);
+  uint32_t *mark = P.buf<uint32_t>(nv), *hcnt = P.buf<uint32_t>(nv);
+  Ctl *ctl = rb.ctl.p;
+  P.init = [=](Launcher &L, cudaStream_t s) {
+    L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
+    fill<uint8_t>(L, alive, nv, (uint8_t)1, s);
+    fill<uint32_t>(L, mark, nv, 0u, s);
+    fill<uint32_t>(L, hcnt, nv, 0u, s);
+  };
+  const KcOp op{alive, (uint32_t)std::min<int64_t>(p.k, 0xffffffffLL)};
+  const OpMark mop{alive, mark};
   const bool blocked = p.blocked != 0;
-  bsp_loop(rb, [&](cudaStream_t st) {
-    pull_round(a, op, blocked, hcnt.p, st);
-    if (thr != std::numeric_limits<int64_t>::max())
-      SG_LAUNCH((k_pull_finish<KcOp, false>), 1, 1024, 0, st, a, op, hcnt.p, 0.0, v.ne,
-                max_rounds);
-    SG_LAUNCH(k_kcore_kill, grid_n(nv), 256, 0, st, a, alive.p);
-    SG_LAUNCH(k_push_twc<OpMark>, occupancy_grid(k_push_twc<OpMark>, kTB), kTB, 0, st, w, mop);
-    SG_LAUNCH(k_push_large<OpMark>, occupancy_grid(k_push_large<OpMark>, kTB), kTB, 0, st, w,
-              mop);
-    SG_LAUNCH(k_kcore_advance, 1, 1, 0, st, rb.ctl.p, max_rounds);
-  }, s, max_rounds, &ro.rounds);
-  SG_LAUNCH(k_labels_alive, grid_n(nv), 256, 0, s, alive.p, nv, ro.labels.p);
-  SG_CUDA(cudaStreamSynchronize(s));
+  P.round = [=, &rb](RoundCtx &c) {
+    pull_round(c, a, op, blocked, hcnt);
+    if (thr != kNoHuge)
+      c.L.go("kcore_huge", k_pull_finish<KcOp, false>, 1, 1024, c.s, a, op, hcnt, PrStop{});
+    c.L.go("kcore_kill", k_kcore_kill, grid_n(nv), 256, c.s, a, alive);
+    c.L.go("kcore_reset", k_kcore_reset, 1, 1, c.s, ctl);
+    c.L.go("mark_twc", k_push_twc<OpMark>, occupancy_grid(k_push_twc<OpMark>, kTB), kTB, c.s, w, mop);
+    c.L.go("mark_large", k_push_large<OpMark>, occupancy_grid(k_push_large<OpMark>, kTB), kTB, c.s,
+           w, mop);
+    c.L.go("advance", k_kcore_advance, 1, 1, c.s, ctl, loop_of(rb, max_rounds, c));
+  };
+  P.finish = [=](Launcher &L, cudaStream_t s) {
+    L.go("labels", k_labels_alive, grid_n(nv), 256, s, alive, nv, labels_d);
+  };
 }
 
+struct RunResultC {
+  int64_t rounds = 0;
+  double ms = 0;
+};
+
 void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out, int64_t cap,
-             int64_t *nrounds, double *ms_out) {
+             int64_t *nrounds, double *ms_out, Launcher *prof) {
   if (p.app < SG_APP_BFS || p.app > SG_APP_KCORE) throw Error(SG_ECONFIG, "unknown app");
   if (p.devices < 1) throw Error(SG_ECONFIG, "device count must be >= 1");
   if (g.nv > 0x7fffffffLL) throw Error(SG_ERANGE, "vertex ids must fit int32");
@@ -519,34 +598,85 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
   if (p.app == SG_APP_PR && !(p.damping > 0.0 && p.damping < 1.0))
     throw Error(SG_ECONFIG, "damping must be in (0, 1)");
   if (p.app == SG_APP_PR && !(p.tol > 0.0)) throw Error(SG_ECONFIG, "tolerance must be positive");
+  if (p.app == SG_APP_KCORE && p.k < 1) throw Error(SG_ECONFIG, "k must be >= 1");
   if (p.app == SG_APP_SSSP && g.weighted && g.wmin < 0)
     throw Error(SG_ECONFIG, "sssp requires non-negative weights");
-  int64_t max_rounds = p.max_rounds > 0 ? p.max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
-  int64_t thr = p.sched == SG_SCHED_TWC ? std::numeric_limits<int64_t>::max()
-                                        : std::max<int64_t>(1, p.threshold);
+  const int64_t max_rounds =
+      p.max_rounds > 0 ? p.max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
+  const int64_t thr = p.sched == SG_SCHED_TWC ? kNoHuge : std::max<int64_t>(1, p.threshold);
+  *nrounds = 0;
+  if (ms_out) *ms_out = 0.0;
+  if (g.nv == 0) return;
   // lazily built views (cached on the graph, like graph.py:102/117) are not timed
   if (p.app == SG_APP_CC || p.app == SG_APP_KCORE) g.sym();
   if (p.app == SG_APP_PR) g.csc();
-  *nrounds = 0;
-  if (g.nv == 0) {
-    if (ms_out) *ms_out = 0.0;
-    return;
+
+  RunBufs rb;
+  Program P;
+  double *labels_d = P.buf<double>(g.nv);
+  switch (p.app) {
+    case SG_APP_BFS:
+    case SG_APP_SSSP:
+    case SG_APP_CC: prep_push_min(P, g, p, rb, labels_d, thr, max_rounds); break;
+    case SG_APP_PR: prep_pr(P, g, p, rb, labels_d, thr, max_rounds); break;
+    case SG_APP_KCORE: prep_kcore(P, g, p, rb, labels_d, thr, max_rounds); break;
   }
   cudaStream_t s;
   SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  cudaEvent_t e0, e1;
-  SG_CUDA(cudaEventCreate(&e0));
-  SG_CUDA(cudaEventCreate(&e1));
-  RunBufs rb;
-  RunOut ro;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  Launcher plain;
+  auto cleanup = [&] {
+    cudaStreamSynchronize(s);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+  };
   try {
+    SG_CUDA(cudaEventCreate(&e0));
+    SG_CUDA(cudaEventCreate(&e1));
+    size_t body_nodes = 0;
+    if (!prof) {
+      // graph = WHILE(cond) { round }  — built before the timed region
+      SG_CUDA(cudaGraphCreate(&graph, 0));
+      cudaGraphConditionalHandle cond;
+      SG_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams np{};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = cond;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      SG_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+      cudaGraph_t body = np.conditional.phGraph_out[0];
+      SG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal));
+      RoundCtx c{plain, s, cond, 1};
+      P.round(c);
+      SG_CUDA(cudaStreamEndCapture(s, &body));
+      SG_CUDA(cudaGraphGetNodes(body, nullptr, &body_nodes));
+      SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    }
+    Launcher &L = prof ? *prof : plain;
     SG_CUDA(cudaEventRecord(e0, s));
-    switch (p.app) {
-      case SG_APP_BFS:
-      case SG_APP_SSSP:
-      case SG_APP_CC: run_push_min(g, p, rb, ro, s, thr, max_rounds); break;
-      case SG_APP_PR: run_pr(g, p, rb, ro, s, thr, max_rounds); break;
-      case SG_APP_KCORE: run_kcore(g, p, rb, ro, s, thr, max_rounds); break;
+    P.init(L, s);
+    int64_t rounds = 0;
+    if (!prof) {
+      SG_CUDA(cudaGraphLaunch(exec, s));
+    } else {
+      Ctl h;
+      RoundCtx c{L, s, cudaGraphConditionalHandle{}, 0};
+      const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
+      for (int64_t r = 0; r < limit; ++r) {
+        P.round(c);
+        SG_CUDA(cudaMemcpyAsync(&h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+        SG_CUDA(cudaStreamSynchronize(s));
+        L.collect();
+        if (h.done) break;
+      }
     }
     SG_CUDA(cudaEventRecord(e1, s));
     SG_CUDA(cudaEventSynchronize(e1));
@@ -555,28 +685,33 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
     if (ms_out) *ms_out = ms;
     Ctl h;
     SG_CUDA(cudaMemcpy(&h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
-    int64_t rounds = h.round;
+    rounds = h.round;
+    if (!prof) g_launches.fetch_add((int64_t)body_nodes * rounds, std::memory_order_relaxed);
+    P.finish(L, s);
+    if (prof) {
+      SG_CUDA(cudaStreamSynchronize(s));
+      L.collect();
+    }
     std::vector<RoundStat> st((size_t)std::min<int64_t>(rounds, rb.stats_cap));
     if (!st.empty())
       SG_CUDA(cudaMemcpy(st.data(), rb.stats.p, sizeof(RoundStat) * st.size(),
                          cudaMemcpyDeviceToHost));
-    if (rounds_out)
-      std::memcpy(rounds_out, st.data(), sizeof(RoundStat) * (size_t)std::min<int64_t>(cap, (int64_t)st.size()));
+    if (rounds_out && !st.empty())
+      std::memcpy(rounds_out, st.data(),
+                  sizeof(RoundStat) * (size_t)std::min<int64_t>(cap, (int64_t)st.size()));
     *nrounds = rounds;
+    SG_CUDA(cudaStreamSynchronize(s));
     if (labels_out)
-      SG_CUDA(cudaMemcpy(labels_out, ro.labels.p, sizeof(double) * g.nv, cudaMemcpyDeviceToHost));
-    if (h.error) throw Error(h.error, "did not converge within " + std::to_string(max_rounds) +
-                                          " rounds");
+      SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * g.nv, cudaMemcpyDeviceToHost));
+    if (h.error == SG_ECONVERGE)
+      throw Error(SG_ECONVERGE, "did not converge within " + std::to_string(max_rounds) + " rounds");
+    if (h.error)
+      throw Error(h.error, "round log capacity (" + std::to_string(rb.stats_cap) + ") exhausted");
   } catch (...) {
-    cudaStreamSynchronize(s);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaStreamDestroy(s);
+    cleanup();
     throw;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaStreamDestroy(s);
+  cleanup();
 }
 
 }  // namespace
@@ -719,7 +854,36 @@ void sg_graph_destroy(sg_graph *g) { delete g; }
 int sg_run(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
            int64_t rounds_cap, int64_t *nrounds, double *ms_out) {
   return sg::guard([&] {
-    sg::run_app(*g->g, *p, labels_out, rounds_out, rounds_cap, nrounds, ms_out);
+    sg::run_app(*g->g, *p, labels_out, rounds_out, rounds_cap, nrounds, ms_out, nullptr);
+  });
+}
+
+int sg_run_profiled(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
+                    int64_t rounds_cap, int64_t *nrounds, double *ms_out, sg_kernel_time *kt,
+                    int32_t kt_cap, int32_t *nkt) {
+  return sg::guard([&] {
+    sg::Launcher L;
+    L.profile = true;
+    *nkt = 0;
+    auto report = [&] {
+      int32_t n = 0;
+      for (const auto &name : L.order) {
+        if (n >= kt_cap) break;
+        std::memset(kt[n].name, 0, sizeof(kt[n].name));
+        std::strncpy(kt[n].name, name.c_str(), sizeof(kt[n].name) - 1);
+        kt[n].launches = L.totals[name].first;
+        kt[n].ms = L.totals[name].second;
+        ++n;
+      }
+      *nkt = n;
+    };
+    try {
+      sg::run_app(*g->g, *p, labels_out, rounds_out, rounds_cap, nrounds, ms_out, &L);
+    } catch (...) {
+      report();
+      throw;
+    }
+    report();
   });
 }
 

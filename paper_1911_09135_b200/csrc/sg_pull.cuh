@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   const uint32_t n = dense ? a.nv : ctl->fsize;
   const uint32_t *list = a.q[round & 1];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  unsigned long long my_edges = 0;
+  unsigned long long my_edges = 0, my_large = 0;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsTB;
   for (uint64_t c = (uint64_t)blockIdx.x * kWarpsTB + warp; c * 32 < n; c += nwarps) {
     uint64_t i = c * 32 + lane;
@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
     if (a.dynamic_bins) {
       warp_append(huge, v, a.hugeq, &ctl->nhuge);
       warp_append(large, v, a.largeq, &ctl->nlarge);
+      if (large) my_large += (unsigned long long)deg;
     }
     const bool mine = valid && !huge && !large;
     const uint32_t gd = mine ? (uint32_t)deg : 0u;
@@ -134,6 +135,8 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   if (a.dynamic_bins) {
     unsigned long long bs = block_sum(my_edges, red);
     if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+    bs = block_sum(my_large, red);
+    if (threadIdx.x == 0 && bs) atomicAdd(&ctl->large_edges, bs);
   }
   if (sizeof(typename Op::A) == 8) {
     double m = warp_max(op.dmax);
@@ -245,10 +248,19 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
 }
 
 // huge-row fold (single CTA; huge rows are few) — plus the pr round advance
+struct PrStop {            // apps.py:163-171, 183-185 evaluated on the device
+  const unsigned long long *gain_max_bits;  // max_v sum_{u->v} inv_outdeg[u]
+  double damping, tol;
+  int64_t ne;              // active edges per round (all of E)
+  int64_t limit;           // min(max_rounds, stats capacity)
+  int64_t max_rounds;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+
 template <class Op, bool PR>
 __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
-                                                      typename Op::A *hacc, double eps_stop,
-                                                      int64_t ne, int64_t max_rounds) {
+                                                      typename Op::A *hacc, PrStop stop) {
   __shared__ double redd[32];
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
@@ -270,12 +282,15 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
     unsigned long long mb = (unsigned long long)__double_as_longlong(m);
     unsigned long long old = atomicMax(&ctl->delta_bits, mb);
     double delta = __longlong_as_double((long long)(old > mb ? old : mb));
+    double worst = __dmul_rn(stop.damping, __longlong_as_double((long long)*stop.gain_max_bits));
+    double eps_stop = stop.tol / (worst > 1.0 ? worst : 1.0);
     RoundStat &st = a.stats[round];
     st.frontier_size = a.nv;
-    st.active_edges = ne;
+    st.active_edges = stop.ne;
     st.huge_count = nh;
     st.huge_edges = (long long)ctl->huge_edges;
     st.large_count = ctl->nlarge;
+    st.large_edges = (long long)ctl->large_edges;
     st.updated = a.nv;
     st.comm_sent = 0;
     st.comm_broadcast = 0;
@@ -283,7 +298,9 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
     ctl->large_head = 0;
     ctl->round = round + 1;
     if (delta <= eps_stop) ctl->done = 1;  // apps.py:183-185
-    else if ((int64_t)round + 1 >= max_rounds) ctl->error = SG_ECONVERGE, ctl->done = 1;
+    else if ((int64_t)round + 1 >= stop.limit)
+      ctl->error = (int64_t)round + 1 >= stop.max_rounds ? SG_ECONVERGE : SG_ENOMEM, ctl->done = 1;
+    if (stop.use_cond) cudaGraphSetConditional(stop.cond, ctl->done ? 0u : 1u);
   }
 }
 

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   const Src src = resolve_src(a, ctl);
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   WarpQueue wq{sq[warp], 0, a.q[(round + 1) & 1], &ctl->nsize};
-  unsigned long long my_edges = 0;
+  unsigned long long my_edges = 0, my_large = 0;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsTB;
   for (uint64_t c = (uint64_t)blockIdx.x * kWarpsTB + warp; c * 32 < src.n; c += nwarps) {
     uint64_t i = c * 32 + lane;
@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
     my_edges += (unsigned long long)deg;
     bool huge = deg >= a.threshold;
     bool large = !huge && deg >= (int64_t)kLarge;
+    if (large) my_large += (unsigned long long)deg;
     warp_append(huge, v, a.hugeq, &ctl->nhuge);
     warp_append(large, v, a.largeq, &ctl->nlarge);
     uint32_t gd = (huge || large) ? 0u : (uint32_t)deg;
@@ -187,6 +188,8 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   if (a.src_mode == 0) {
     unsigned long long bs = block_sum(my_edges, red);
     if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+    bs = block_sum(my_large, red);
+    if (threadIdx.x == 0 && bs) atomicAdd(&ctl->large_edges, bs);
   }
 }
 

@@ -26,7 +26,8 @@ SCHED_IDS = {"alb": 0, "twc": 1}
 EXPORTS = (
     "sg_last_error", "sg_device_count", "sg_graph_create", "sg_graph_create_rmat",
     "sg_graph_attach_random_weights", "sg_graph_with_weights", "sg_graph_info",
-    "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_lb_kernel",
+    "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_run_profiled",
+    "sg_lb_kernel",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
 )
 
@@ -40,8 +41,12 @@ class Params(ctypes.Structure):
 
 
 ROUND_DTYPE = np.dtype([("frontier_size", "<i8"), ("active_edges", "<i8"), ("huge_count", "<i8"),
-                        ("huge_edges", "<i8"), ("large_count", "<i8"), ("updated", "<i8"),
-                        ("comm_sent", "<i8"), ("comm_broadcast", "<i8")])
+                        ("huge_edges", "<i8"), ("large_count", "<i8"), ("large_edges", "<i8"),
+                        ("updated", "<i8"), ("comm_sent", "<i8"), ("comm_broadcast", "<i8")])
+
+
+class KernelTime(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64), ("ms", ctypes.c_double)]
 
 _lib = None
 _lock = threading.Lock()
@@ -72,6 +77,8 @@ def load(path: Path | None = None):
             "sg_graph_view_size": ([P, i32, P], ctypes.c_int),
             "sg_graph_destroy": ([P], None),
             "sg_run": ([P, ctypes.POINTER(Params), P, P, i64, P, P], ctypes.c_int),
+            "sg_run_profiled": ([P, ctypes.POINTER(Params), P, P, i64, P, P, P, i32, P],
+                                ctypes.c_int),
             "sg_lb_kernel": ([P, i64, P, i64, P, i64, P, P, i64, P, P, P, i64, i32, i32, i32, i32,
                               i32, P, P, P], ctypes.c_int),
             "sg_twc_kernel": ([P, i64, P, i64, P, i64, P, i64, P, i64, P, i64, P, P, P, i64, i32,
@@ -186,20 +193,33 @@ class DeviceGraph:
         check(load().sg_graph_download(self.handle, which, ptr(off), ptr(tgt), ptr(w)))
         return off, tgt, w
 
-    def run(self, params: Params, rounds_cap=1 << 16):
+    def run(self, params: Params, rounds_cap=1 << 16, profile=False):
+        """Run the BSP loop on the device.  Returns (labels, round log, ms) or,
+        with ``profile``, (labels, round log, ms, {kernel: (launches, ms)})."""
         nv, _, _ = self.info()
         labels = np.empty(nv, dtype=np.float64)
         rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
         n = ctypes.c_int64(0)
         ms = ctypes.c_double(0.0)
-        code = load().sg_run(self.handle, ctypes.byref(params), ptr(labels), ptr(rounds),
-                             rounds_cap, ctypes.byref(n), ctypes.byref(ms))
+        kt = (KernelTime * 64)()
+        nkt = ctypes.c_int32(0)
+        if profile:
+            code = load().sg_run_profiled(self.handle, ctypes.byref(params), ptr(labels),
+                                          ptr(rounds), rounds_cap, ctypes.byref(n),
+                                          ctypes.byref(ms), kt, 64, ctypes.byref(nkt))
+        else:
+            code = load().sg_run(self.handle, ctypes.byref(params), ptr(labels), ptr(rounds),
+                                 rounds_cap, ctypes.byref(n), ctypes.byref(ms))
         log = rounds[: min(n.value, rounds_cap)].copy()
         if code == SG_ECONVERGE:
             err = ConvergenceError((load().sg_last_error() or b"").decode())
             err.metrics_log = log
             raise err
         check(code)
+        if profile:
+            kernels = {kt[i].name.decode(): (int(kt[i].launches), float(kt[i].ms))
+                       for i in range(nkt.value)}
+            return labels, log, ms.value, kernels
         return labels, log, ms.value
 
 
