@@ -130,11 +130,6 @@ __global__ void k_fill(T *p, int64_t n, T v) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) p[i] = v;
 }
-__global__ void k_iota32(uint32_t *p, int64_t n) {
-  int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
-    p[i] = (uint32_t)i;
-}
 template <class T>
 __global__ void k_set1(T *p, int64_t i, T v) { p[i] = v; }
 
@@ -148,6 +143,27 @@ __global__ void k_labels_u32(const uint32_t *lab, int64_t n, double *out) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
     out[i] = lab[i] == kInf32 ? INFINITY : (double)lab[i];
+}
+__global__ void k_iota_pairs(uint32_t *p, int64_t n) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    reinterpret_cast<uint2 *>(p)[i] = make_uint2((uint32_t)i, (uint32_t)i);
+}
+// after R rounds the half written last, R & 1, holds every final label
+__global__ void k_labels_pair_u32(const uint32_t *lab, int64_t n, const Ctl *ctl, double *out) {
+  const uint32_t h = ctl->round & 1;
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    uint32_t x = lab[2 * i + h];
+    out[i] = x == kInf32 ? INFINITY : (double)x;
+  }
+}
+__global__ void k_labels_pair_f64(const unsigned long long *lab, int64_t n, const Ctl *ctl,
+                                  double *out) {
+  const uint32_t h = ctl->round & 1;
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = __longlong_as_double((long long)lab[2 * i + h]);
 }
 __global__ void k_labels_alive(const uint8_t *a, int64_t n, double *out) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
@@ -221,30 +237,16 @@ __device__ __forceinline__ void loop_test(Ctl *ctl, uint32_t round, bool empty, 
   if (lp.use_cond) cudaGraphSetConditional(lp.cond, ctl->done ? 0u : 1u);
 }
 
-// commit (snapshot := label for changed vertices) + round bookkeeping
-template <class L, bool COMMIT>
-__global__ void __launch_bounds__(256) k_push_advance(PushArgs a, L *lab, L *snap, Loop lp) {
-  __shared__ bool last;
+// round bookkeeping (the parity-paired labels need no commit pass)
+__global__ void k_push_advance(PushArgs a, Loop lp) {
   Ctl *ctl = a.ctl;
+  if (threadIdx.x) return;
   if (ctl->done) {
-    if (lp.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(lp.cond, 0u);
+    if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
     return;
   }
   const uint32_t round = ctl->round;
   const uint32_t nn = ctl->nsize;
-  if (COMMIT) {
-    const uint32_t *nq = a.q[(round + 1) & 1];
-    int64_t st = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += st) {
-      uint32_t v = nq[i];
-      snap[v] = lab[v];
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last || threadIdx.x) return;
   RoundStat &s = a.stats[round];
   s.frontier_size = ctl->dense ? a.nv : ctl->fsize;
   s.active_edges = (long long)ctl->edges;
@@ -443,8 +445,7 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
     };
     P.round = [=, &rb](RoundCtx &c) {
       push_round(c, a, op, blocked);
-      c.L.go("advance", k_push_advance<uint32_t, false>, 1, 256, c.s, a, lab, lab,
-             loop_of(rb, max_rounds, c));
+      c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
     };
     P.finish = [=](Launcher &L, cudaStream_t s) {
       L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
@@ -458,52 +459,44 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
     double bound = (double)g.wmax * (double)std::max<int64_t>(nv - 1, 1);
     use32 = g.w32.p != nullptr && bound < 4294967295.0;
   }
+  // parity pairs lab[2v + h]; both halves start equal
+  auto set_round = [&](auto op) {
+    P.round = [=, &rb](RoundCtx &c) {
+      push_round(c, a, op, blocked);
+      c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
+    };
+  };
   if (use32) {
-    uint32_t *lab = P.buf<uint32_t>(nv), *snap = P.buf<uint32_t>(nv);
+    uint32_t *lab = P.buf<uint32_t>(2 * nv);
     P.init = [=](Launcher &L, cudaStream_t s) {
       init_ctl(L, s);
       if (cc) {
-        L.go("init", k_iota32, grid_n(nv), 256, s, lab, nv);
-        L.go("init", k_iota32, grid_n(nv), 256, s, snap, nv);
+        L.go("init", k_iota_pairs, grid_n(nv), 256, s, lab, nv);
       } else {
-        fill<uint32_t>(L, lab, nv, kInf32, s);
-        fill<uint32_t>(L, snap, nv, kInf32, s);
-        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
-        L.go("init", k_set1<uint32_t>, 1, 1, s, snap, src, 0u);
+        fill<uint32_t>(L, lab, 2 * nv, kInf32, s);
+        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, 2 * src, 0u);
+        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, 2 * src + 1, 0u);
       }
     };
-    auto set_round = [&](auto op) {
-      P.round = [=, &rb](RoundCtx &c) {
-        push_round(c, a, op, blocked);
-        c.L.go("advance", k_push_advance<uint32_t, true>, grid_n(nv, 256), 256, c.s, a, lab, snap,
-               loop_of(rb, max_rounds, c));
-      };
-    };
-    if (cc) set_round(OpMin32<0>{lab, snap, nullptr});
-    else if (!weighted) set_round(OpMin32<1>{lab, snap, nullptr});
-    else set_round(OpMin32<2>{lab, snap, g.w32.p});
+    if (cc) set_round(OpPair<0>{lab, nullptr, nullptr});
+    else if (!weighted) set_round(OpPair<1>{lab, nullptr, nullptr});
+    else set_round(OpPair<2>{lab, g.w32.p, nullptr});
     P.finish = [=](Launcher &L, cudaStream_t s) {
-      L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
+      L.go("labels", k_labels_pair_u32, grid_n(nv), 256, s, lab, nv, ctl, labels_d);
     };
   } else {
     using U = unsigned long long;
-    U *lab = P.buf<U>(nv), *snap = P.buf<U>(nv);
+    U *lab = P.buf<U>(2 * nv);
     const U inf = 0x7ff0000000000000ull;
     P.init = [=](Launcher &L, cudaStream_t s) {
       init_ctl(L, s);
-      fill<U>(L, lab, nv, inf, s);
-      fill<U>(L, snap, nv, inf, s);
-      L.go("init", k_set1<U>, 1, 1, s, lab, src, 0ull);
-      L.go("init", k_set1<U>, 1, 1, s, snap, src, 0ull);
+      fill<U>(L, lab, 2 * nv, inf, s);
+      L.go("init", k_set1<U>, 1, 1, s, lab, 2 * src, 0ull);
+      L.go("init", k_set1<U>, 1, 1, s, lab, 2 * src + 1, 0ull);
     };
-    OpMinF64 op{lab, snap, weighted ? g.w64.p : nullptr};
-    P.round = [=, &rb](RoundCtx &c) {
-      push_round(c, a, op, blocked);
-      c.L.go("advance", k_push_advance<U, true>, grid_n(nv, 256), 256, c.s, a, lab, snap,
-             loop_of(rb, max_rounds, c));
-    };
-    P.finish = [=](Launcher &, cudaStream_t s) {
-      SG_CUDA(cudaMemcpyAsync(labels_d, lab, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s));
+    set_round(OpPair<3>{lab, nullptr, weighted ? g.w64.p : nullptr});
+    P.finish = [=](Launcher &L, cudaStream_t s) {
+      L.go("labels", k_labels_pair_f64, grid_n(nv), 256, s, lab, nv, ctl, labels_d);
     };
   }
 }

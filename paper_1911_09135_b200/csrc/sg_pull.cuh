@@ -108,25 +108,37 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
     const uint32_t total = __shfl_sync(kFull, incl, 31);
     const uint32_t excl = incl - gd;
     typename Op::A acc = 0;
-    for (uint32_t base = 0; base < total; base += 32) {
-      const uint32_t slot = base + lane;
-      const int o = warp_owner(incl, slot);
-      const int64_t so = shfl64(s, o);
-      const uint32_t eo = __shfl_sync(kFull, excl, o);
-      typename Op::A x = 0;
-      if (slot < total) x = op.load(ld_stream(a.col + so + (slot - eo)));
-      // segmented inclusive scan (owners are non-decreasing along the lanes)
+    for (uint32_t base = 0; base < total; base += 32 * kU) {
+      int o[kU];
+      uint32_t src[kU];
+      typename Op::A x[kU];
 #pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        typename Op::A y = __shfl_up_sync(kFull, x, dd);
-        int oo = __shfl_up_sync(kFull, o, dd);
-        if (lane >= (uint32_t)dd && oo == o) x += y;
+      for (int u = 0; u < kU; ++u) {  // kU adjacency loads in flight
+        const uint32_t slot = base + u * 32 + lane;
+        o[u] = warp_owner(incl, slot);
+        const int64_t so = shfl64(s, o[u]);
+        const uint32_t eo = __shfl_sync(kFull, excl, o[u]);
+        src[u] = slot < total ? ld_stream(a.col + so + (slot - eo)) : 0xffffffffu;
       }
-      // each owner lane picks up the total of its segment in this chunk
-      const uint32_t lo = excl > base ? excl : base;
-      const uint32_t hi = incl < base + 32 ? incl : base + 32;
-      typename Op::A seg = __shfl_sync(kFull, x, (int)((hi - 1 - base) & 31u));
-      if (lo < hi) acc += seg;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)  // then kU value gathers in flight
+        x[u] = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t cb = base + u * 32;
+        // segmented inclusive scan (owners are non-decreasing along the lanes)
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          typename Op::A y = __shfl_up_sync(kFull, x[u], dd);
+          int oo = __shfl_up_sync(kFull, o[u], dd);
+          if (lane >= (uint32_t)dd && oo == o[u]) x[u] += y;
+        }
+        // each owner lane picks up the total of its segment in this chunk
+        const uint32_t lo = excl > cb ? excl : cb;
+        const uint32_t hi = incl < cb + 32 ? incl : cb + 32;
+        typename Op::A seg = __shfl_sync(kFull, x[u], (int)((hi - 1 - cb) & 31u));
+        if (lo < hi) acc += seg;
+      }
     }
     bool die = false;
     if (mine) die = op.finish(v, acc);
@@ -168,7 +180,13 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
     const uint32_t v = a.largeq[idx];
     const int64_t s = a.off[v], e = a.off[v + 1];
     typename Op::A x = 0;
-    for (int64_t j = s + threadIdx.x; j < e; j += kTB) x += op.load(ld_stream(a.col + j));
+    for (int64_t b = s + threadIdx.x; b < e; b += kTB * kU) {
+      uint32_t src[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) src[u] = b + u * kTB < e ? ld_stream(a.col + b + u * kTB) : 0xffffffffu;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) x += src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+    }
     x = block_sum(x, red);
     if (threadIdx.x == 0 && op.finish(v, x)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
   }
@@ -227,23 +245,35 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
-  for (int64_t p = 0; p < passes; ++p) {
-    const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
-    typename Op::A x = 0;
-    int o = -1;
-    if (g < E) {
-      o = (int)owner_search(pre, nh, g);
-      x = op.load(ld_stream(a.col + a.hstart[o] + (g - (o ? pre[o - 1] : 0))));
+  for (int64_t p0 = 0; p0 < passes; p0 += kU) {
+    int o[kU];
+    uint32_t src[kU];
+    typename Op::A x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t p = p0 + u;
+      const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
+      o[u] = -1;
+      src[u] = 0;
+      if (p < passes && g < E) {
+        o[u] = (int)owner_search(pre, nh, g);
+        src[u] = ld_stream(a.col + a.hstart[o[u]] + (g - (o[u] ? pre[o[u] - 1] : 0)));
+      }
     }
 #pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      typename Op::A y = __shfl_up_sync(kFull, x, dd);
-      int oo = __shfl_up_sync(kFull, o, dd);
-      if (lane >= (uint32_t)dd && oo == o) x += y;
+    for (int u = 0; u < kU; ++u) x[u] = o[u] >= 0 ? op.load(src[u]) : typename Op::A(0);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        typename Op::A y = __shfl_up_sync(kFull, x[u], dd);
+        int oo = __shfl_up_sync(kFull, o[u], dd);
+        if (lane >= (uint32_t)dd && oo == o[u]) x[u] += y;
+      }
+      int onext = __shfl_down_sync(kFull, o[u], 1);
+      bool last = (lane == 31) || onext != o[u];
+      if (o[u] >= 0 && last) atomicAdd(hacc + o[u], x[u]);
     }
-    int onext = __shfl_down_sync(kFull, o, 1);
-    bool last = (lane == 31) || onext != o;
-    if (o >= 0 && last) atomicAdd(hacc + o, x);
   }
 }
 

@@ -15,14 +15,17 @@
 //     there by warp-level scan-based gathering (Merrill's fine-grained TWC: the
 //     warp's edges are numbered by a shuffle scan and lanes take consecutive
 //     edge slots, so adjacency loads are coalesced);
-//   * CTA bin: one CTA per vertex (dynamic fetch), 256 consecutive edges per step;
+//   * CTA bin: one CTA per vertex (static round robin, no barriers);
 //   * huge bin: a single-CTA scan builds the int64 prefix + snapshot labels, the
 //     LB kernel stages the prefix in shared memory and every thread of every CTA
 //     walks g cyclically: consecutive lanes read consecutive adjacency entries;
-//   * BSP: sources read the round-start snapshot, targets are lowered with
-//     atomicMin (after a plain-load pre-filter); the first lowering of a vertex
-//     in a round enqueues it exactly once (old == snapshot), so the next
-//     frontier is duplicate-free without a bitmap pass.
+//   * every lane relaxes kU edges per step, in phases (adjacency loads, label
+//     loads, atomics), so kU independent random accesses are in flight;
+//   * BSP without a commit pass: labels are parity pairs {L0, L1}; round r reads
+//     half r&1 (a snapshot nobody writes during the round) and lowers half
+//     (r+1)&1.  Frontier vertices re-sync their next half with one red.min; the
+//     first atomicMin that takes a vertex below its snapshot (old >= snapshot)
+//     enqueues it, so the next frontier is exact and duplicate-free.
 #pragma once
 #include "sg_ctl.cuh"
 
@@ -30,6 +33,7 @@ namespace sg {
 
 constexpr int kTB = 256;        // threads per CTA of the traversal kernels
 constexpr int kWarpsTB = kTB / 32;
+constexpr int kU = 4;           // edges per lane per step (memory-level parallelism)
 constexpr uint32_t kLarge = 256;  // TWC CTA-bin cut (threads_per_cta, schedulers.py:159)
 constexpr uint32_t kHugeSmem = 2048;  // huge prefixes staged in shared memory
 
@@ -60,61 +64,90 @@ __device__ __forceinline__ Src resolve_src(const PushArgs &a, const Ctl *c) {
 }
 
 // ------------------------------------------------------------------ ops --
-// bfs (OP_BFS): all frontier vertices of round r carry label r, so the source
-// value is the round index; a visited bitmap is the relaxation test
-// (label == inf <=> bit clear) and the atomicOr winner writes the label.
+// Every op relaxes kU edges at once: relax(e, valid, sv, dst, act).
+// bfs (OP_BFS): frontier vertices of round r carry label r; a visited bitmap
+// is the relaxation test (label == inf <=> bit clear); the atomicOr winner
+// writes the label.
 struct OpBfs {
   using L = uint32_t;
   uint32_t *lab, *vis;
   uint32_t r = 0;
   __device__ __forceinline__ void begin(uint32_t round) { r = round; }
   __device__ __forceinline__ L src_val(uint32_t) const { return r; }
-  __device__ __forceinline__ bool relax(int64_t, uint32_t dst, L sv) const {
-    uint32_t bit = 1u << (dst & 31u);
-    uint32_t *wp = vis + (dst >> 5);
-    if (*wp & bit) return false;
-    if (atomicOr(wp, bit) & bit) return false;
-    lab[dst] = sv + 1u;
-    return true;
+  __device__ __forceinline__ void sync_src(uint32_t, L) const {}
+  __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kU],
+                                        const bool (&ok)[kU], const L (&sv)[kU],
+                                        uint32_t (&dst)[kU], bool (&act)[kU]) const {
+    uint32_t word[kU], old[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) word[u] = ok[u] ? vis[dst[u] >> 5] : ~0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      uint32_t bit = 1u << (dst[u] & 31u);
+      old[u] = (word[u] & bit) ? bit : atomicOr(vis + (dst[u] >> 5), bit);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      act[u] = ok[u] && !(old[u] & (1u << (dst[u] & 31u)));
+      if (act[u]) lab[dst[u]] = sv[u] + 1u;
+    }
   }
 };
 
-// sssp / cc with 32-bit labels. KIND 0: cc (prop = value), 1: unit weight,
-// 2: u32 weights.  Exact: integer sums below 2^32 equal the reference's
-// float64 sums (the engine checks max_w * (V-1) < 2^32 - 1).
+// sssp / cc on parity-paired labels.  KIND 0: cc (prop = value), 1: unit
+// weight, 2: u32 weights, 3: float64 labels (bits) with int64 weights.
+// 32-bit kinds are exact: integer sums below 2^32 equal the reference's
+// float64 sums (the engine checks max_w * (V-1) < 2^32 - 1); kind 3 performs
+// the reference's float64 additions (labels >= 0, so unsigned bit order ==
+// numeric order and atomicMin on the bits is a float min).
 template <int KIND>
-struct OpMin32 {
-  using L = uint32_t;
-  uint32_t *lab;
-  const uint32_t *snap, *w;
-  __device__ __forceinline__ void begin(uint32_t) {}
-  __device__ __forceinline__ L src_val(uint32_t v) const { return snap[v]; }
-  __device__ __forceinline__ bool relax(int64_t e, uint32_t dst, L sv) const {
-    L prop = KIND == 0 ? sv : KIND == 1 ? sv + 1u : sv + __ldg(w + e);
-    L cur = lab[dst];
-    if (prop >= cur) return false;
-    L old = atomicMin(lab + dst, prop);
-    return prop < old && old == snap[dst];  // first lowering this round
+struct OpPair {
+  using L = typename std::conditional<KIND == 3, unsigned long long, uint32_t>::type;
+  L *lab;  // lab[2v + h]
+  const uint32_t *w32;
+  const int64_t *w64;  // KIND 3 (nullptr: unit weights)
+  uint32_t ch = 0, nh = 1;  // current (snapshot) / next half
+  __device__ __forceinline__ void begin(uint32_t round) { ch = round & 1u, nh = ch ^ 1u; }
+  __device__ __forceinline__ L src_val(uint32_t v) const { return lab[2 * (size_t)v + ch]; }
+  // a frontier vertex changed last round: its next half still holds the older value
+  __device__ __forceinline__ void sync_src(uint32_t v, L sv) const {
+    atomicMin(lab + 2 * (size_t)v + nh, sv);
   }
-};
-
-// sssp with float64 labels stored as their IEEE bits (labels >= 0, so
-// unsigned order == numeric order): bit-exact to the reference for any
-// non-negative int64 weights, including sums beyond 2^53.
-struct OpMinF64 {
-  using L = unsigned long long;
-  unsigned long long *lab;
-  const unsigned long long *snap;
-  const int64_t *w;  // nullptr: unit weights
-  __device__ __forceinline__ void begin(uint32_t) {}
-  __device__ __forceinline__ L src_val(uint32_t v) const { return snap[v]; }
-  __device__ __forceinline__ bool relax(int64_t e, uint32_t dst, L sv) const {
-    double p = __dadd_rn(__longlong_as_double((long long)sv), w ? (double)w[e] : 1.0);
-    L prop = (L)__double_as_longlong(p);
-    L cur = lab[dst];
-    if (prop >= cur) return false;
-    L old = atomicMin(lab + dst, prop);
-    return prop < old && old == snap[dst];
+  __device__ __forceinline__ L prop(int64_t e, L sv) const {
+    if (KIND == 0) return sv;
+    if (KIND == 1) return sv + 1u;
+    if (KIND == 2) return sv + __ldg(w32 + e);
+    double p = __dadd_rn(__longlong_as_double((long long)sv), w64 ? (double)__ldg(w64 + e) : 1.0);
+    return (L)__double_as_longlong(p);
+  }
+  __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kU],
+                                        const bool (&ok)[kU], const L (&sv)[kU],
+                                        uint32_t (&dst)[kU], bool (&act)[kU]) const {
+    L p[kU], cur[kU], nxt[kU], old[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      p[u] = ok[u] ? prop(e[u], sv[u]) : L(0);
+      if (KIND == 3) {
+        ulonglong2 pr = ok[u] ? reinterpret_cast<const ulonglong2 *>(lab)[dst[u]]
+                              : make_ulonglong2(0, 0);
+        cur[u] = ch ? pr.y : pr.x;
+        nxt[u] = ch ? pr.x : pr.y;
+      } else {
+        uint2 pr = ok[u] ? reinterpret_cast<const uint2 *>(lab)[dst[u]] : make_uint2(0, 0);
+        cur[u] = ch ? pr.y : pr.x;
+        nxt[u] = ch ? pr.x : pr.y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      bool t = ok[u] && p[u] < cur[u] && p[u] < nxt[u];
+      old[u] = t ? atomicMin(lab + 2 * (size_t)dst[u] + nh, p[u]) : L(0);
+      act[u] = t && p[u] < old[u] && old[u] >= cur[u];  // first drop below the snapshot
+    }
   }
 };
 
@@ -126,10 +159,17 @@ struct OpMark {
   uint32_t stamp = 0;
   __device__ __forceinline__ void begin(uint32_t round) { stamp = round + 1; }
   __device__ __forceinline__ L src_val(uint32_t) const { return 0; }
-  __device__ __forceinline__ bool relax(int64_t, uint32_t dst, L) const {
-    if (!alive[dst]) return false;
-    if (mark[dst] == stamp) return false;
-    return atomicExch(mark + dst, stamp) != stamp;
+  __device__ __forceinline__ void sync_src(uint32_t, L) const {}
+  __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kU],
+                                        const bool (&ok)[kU], const L (&)[kU],
+                                        uint32_t (&dst)[kU], bool (&act)[kU]) const {
+    bool t[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) t[u] = ok[u] && alive[dst[u]] && mark[dst[u]] != stamp;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) act[u] = t[u] && atomicExch(mark + dst[u], stamp) != stamp;
   }
 };
 
@@ -137,6 +177,7 @@ struct OpMark {
 // inspection + TWC (small / medium by warp gathering); appends large / huge
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
+  using L = typename Op::L;
   __shared__ uint32_t sq[kWarpsTB][kWQ];
   __shared__ unsigned long long red[32];
   Ctl *ctl = a.ctl;
@@ -144,6 +185,7 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   const uint32_t round = ctl->round;
   op.begin(round);
   const Src src = resolve_src(a, ctl);
+  const bool sync = a.src_mode == 0 && round > 0;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   WarpQueue wq{sq[warp], 0, a.q[(round + 1) & 1], &ctl->nsize};
   unsigned long long my_edges = 0, my_large = 0;
@@ -152,36 +194,43 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
     uint64_t i = c * 32 + lane;
     uint32_t v = 0;
     int64_t s = 0, deg = 0;
+    L sv = 0;
     if (i < src.n) {
       v = src.dense ? (uint32_t)i : src.list[i];
       s = a.off[v];
       deg = a.off[v + 1] - s;
+      sv = op.src_val(v);
+      if (sync) op.sync_src(v, sv);
     }
     my_edges += (unsigned long long)deg;
-    bool huge = deg >= a.threshold;
-    bool large = !huge && deg >= (int64_t)kLarge;
+    const bool huge = deg >= a.threshold;
+    const bool large = !huge && deg >= (int64_t)kLarge;
     if (large) my_large += (unsigned long long)deg;
     warp_append(huge, v, a.hugeq, &ctl->nhuge);
     warp_append(large, v, a.largeq, &ctl->nlarge);
-    uint32_t gd = (huge || large) ? 0u : (uint32_t)deg;
-    typename Op::L sv = gd ? op.src_val(v) : typename Op::L(0);
-    uint32_t incl = warp_incl_scan(gd);
-    uint32_t total = __shfl_sync(kFull, incl, 31);
-    uint32_t excl = incl - gd;
-    for (uint32_t base = 0; base < total; base += 32) {
-      uint32_t slot = base + lane;
-      int o = warp_owner(incl, slot);
-      int64_t so = shfl64(s, o);
-      uint32_t eo = __shfl_sync(kFull, excl, o);
-      typename Op::L svo = __shfl_sync(kFull, sv, o);
-      bool act = false;
-      uint32_t dst = 0;
-      if (slot < total) {
-        int64_t e = so + (slot - eo);
-        dst = ld_stream(a.col + e);
-        act = op.relax(e, dst, svo);
+    const uint32_t gd = (huge || large) ? 0u : (uint32_t)deg;
+    const uint32_t incl = warp_incl_scan(gd);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    const uint32_t excl = incl - gd;
+    for (uint32_t base = 0; base < total; base += 32 * kU) {
+      int64_t e[kU];
+      bool ok[kU];
+      L svo[kU];
+      uint32_t dst[kU];
+      bool act[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t slot = base + u * 32 + lane;
+        const int o = warp_owner(incl, slot);
+        const int64_t so = shfl64(s, o);
+        const uint32_t eo = __shfl_sync(kFull, excl, o);
+        svo[u] = __shfl_sync(kFull, sv, o);
+        ok[u] = slot < total;
+        e[u] = so + (int64_t)(slot - eo);
       }
-      wq.push(act, dst);
+      op.relax(a, e, ok, svo, dst, act);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) wq.push(act[u], dst[u]);
     }
   }
   wq.flush();
@@ -193,11 +242,11 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   }
 }
 
-// TWC CTA bin: one CTA per vertex, dynamic fetch
+// TWC CTA bin: one CTA per vertex, static round robin (no barriers)
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
+  using L = typename Op::L;
   __shared__ uint32_t sq[kWarpsTB][kWQ];
-  __shared__ uint32_t item;
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
   const uint32_t n = ctl->nlarge;
@@ -205,24 +254,25 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
   const uint32_t round = ctl->round;
   op.begin(round);
   WarpQueue wq{sq[threadIdx.x >> 5], 0, a.q[(round + 1) & 1], &ctl->nsize};
-  for (;;) {
-    if (threadIdx.x == 0) item = atomicAdd(&ctl->large_head, 1u);
-    __syncthreads();
-    const uint32_t idx = item;
-    __syncthreads();
-    if (idx >= n) break;
+  for (uint32_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
     const uint32_t v = a.largeq[idx];
-    const int64_t s = a.off[v], e = a.off[v + 1];
-    const typename Op::L sv = op.src_val(v);
-    for (int64_t b = s; b < e; b += kTB) {
-      int64_t ei = b + threadIdx.x;
-      bool act = false;
-      uint32_t dst = 0;
-      if (ei < e) {
-        dst = ld_stream(a.col + ei);
-        act = op.relax(ei, dst, sv);
+    const int64_t s = a.off[v], end = a.off[v + 1];
+    const L sv = op.src_val(v);
+    for (int64_t b = s; b < end; b += kTB * kU) {
+      int64_t e[kU];
+      bool ok[kU];
+      L svs[kU];
+      uint32_t dst[kU];
+      bool act[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        e[u] = b + u * kTB + threadIdx.x;
+        ok[u] = e[u] < end;
+        svs[u] = sv;
       }
-      wq.push(act, dst);
+      op.relax(a, e, ok, svs, dst, act);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) wq.push(act[u], dst[u]);
     }
   }
   wq.flush();
@@ -266,6 +316,7 @@ __global__ void __launch_bounds__(1024) k_huge_prefix(PushArgs a, Op op) {
 // ALB huge-vertex kernel (Algorithm 2): every thread of every CTA
 template <class Op, bool BLOCKED>
 __global__ void __launch_bounds__(kTB) k_push_lb(PushArgs a, Op op) {
+  using L = typename Op::L;
   __shared__ uint32_t sq[kWarpsTB][kWQ];
   __shared__ int64_t spre[kHugeSmem];
   Ctl *ctl = a.ctl;
@@ -285,18 +336,25 @@ __global__ void __launch_bounds__(kTB) k_push_lb(PushArgs a, Op op) {
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
-  for (int64_t p = 0; p < passes; ++p) {
-    // cyclic: g = p*T + tid (schedulers.py:191-194); blocked: g = tid*ceil(e/T) + p
-    const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
-    bool act = false;
-    uint32_t dst = 0;
-    if (g < E) {
-      uint32_t o = owner_search(pre, nh, g);
-      int64_t e = a.hstart[o] + (g - (o ? pre[o - 1] : 0));
-      dst = ld_stream(a.col + e);
-      act = op.relax(e, dst, (typename Op::L)a.hval[o]);
+  for (int64_t p0 = 0; p0 < passes; p0 += kU) {
+    int64_t e[kU];
+    bool ok[kU];
+    L sv[kU];
+    uint32_t dst[kU];
+    bool act[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      // cyclic: g = p*T + tid (schedulers.py:191-194); blocked: g = tid*ceil(e/T) + p
+      const int64_t p = p0 + u;
+      const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
+      ok[u] = p < passes && g < E;
+      uint32_t o = ok[u] ? owner_search(pre, nh, g) : 0u;
+      e[u] = ok[u] ? a.hstart[o] + (g - (o ? pre[o - 1] : 0)) : 0;
+      sv[u] = ok[u] ? (L)a.hval[o] : L(0);
     }
-    wq.push(act, dst);
+    op.relax(a, e, ok, sv, dst, act);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) wq.push(act[u], dst[u]);
   }
   wq.flush();
 }
