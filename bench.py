@@ -252,7 +252,7 @@ def main():
                                       10 * nv + 256)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
-    for _ in range(a.warmup):
+    for _ in range(max(1, a.warmup)):
         labels, log, ms = dev.run(params)
     edges = int(log["active_edges"].sum())
     rounds = len(log)

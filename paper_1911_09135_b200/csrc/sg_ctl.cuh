@@ -21,7 +21,7 @@ struct Ctl {
   uint32_t large_head;  // dynamic fetch cursor of the CTA-bin kernel
   uint32_t ticket;      // last-block ticket of the advance kernels
   uint32_t ndying;      // kcore: vertices whose count fell below k this round
-  uint32_t pad;
+  uint32_t chunk_head;  // dynamic fetch cursor of the TWC kernel (units of kChunkGrab warps)
   unsigned long long edges;       // active edges (sum of frontier degrees) this round
   unsigned long long huge_edges;  // PrefixWork.total_edges
   unsigned long long delta_bits;  // pr: max |new - old| (double bits, >= 0)

@@ -259,7 +259,7 @@ __global__ void k_push_advance(PushArgs a, Loop lp) {
   s.comm_broadcast = (long long)ctl->comm_bcast;
   ctl->fsize = nn;
   ctl->nsize = 0;
-  ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
   ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_sent = ctl->comm_bcast = 0;
   ctl->dense = 0;
   ctl->ticket = 0;
@@ -292,7 +292,7 @@ __global__ void k_kcore_kill(PullArgs a, uint8_t *alive) {
 // the neighbour walk reuses the CTA-bin queue: reset after the kill kernel
 __global__ void k_kcore_reset(Ctl *ctl) {
   if (ctl->done) return;
-  ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
   ctl->huge_edges = ctl->large_edges = 0;
 }
 
@@ -306,7 +306,7 @@ __global__ void k_kcore_advance(Ctl *ctl, Loop lp) {
   ctl->fsize = nn;
   ctl->nsize = 0;
   ctl->ndying = 0;
-  ctl->nlarge = ctl->nhuge = ctl->large_head = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
   ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
   ctl->dense = 0;
   ctl->round = round + 1;

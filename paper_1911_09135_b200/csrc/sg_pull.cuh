@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   op.begin(round);
   const bool dense = !a.dynamic_bins || ctl->dense;
   const uint32_t n = dense ? a.nv : ctl->fsize;
-  const uint32_t *list = a.q[round & 1];
+  const uint32_t *list = (round & 1) ? a.q[1] : a.q[0];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   unsigned long long my_edges = 0, my_large = 0;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsTB;

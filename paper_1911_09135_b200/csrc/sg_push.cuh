@@ -35,7 +35,9 @@ constexpr int kTB = 256;        // threads per CTA of the traversal kernels
 constexpr int kWarpsTB = kTB / 32;
 constexpr int kU = 4;           // edges per lane per step (memory-level parallelism)
 constexpr uint32_t kLarge = 256;  // TWC CTA-bin cut (threads_per_cta, schedulers.py:159)
-constexpr uint32_t kHugeSmem = 2048;  // huge prefixes staged in shared memory
+constexpr uint32_t kHugeSmem = 1024;  // huge-vertex prefix/start/label staged in shared memory
+constexpr uint32_t kChunkGrab = 4;    // TWC chunks (32 items each) per dynamic fetch
+constexpr int kBatch = 32;            // CTA-bin vertices per block-level gather batch
 
 struct PushArgs {
   const int64_t *off;
@@ -59,7 +61,7 @@ struct Src {
 };
 
 __device__ __forceinline__ Src resolve_src(const PushArgs &a, const Ctl *c) {
-  if (a.src_mode == 0) return {a.q[c->round & 1], c->dense ? a.nv : c->fsize, c->dense != 0};
+  if (a.src_mode == 0) return {((c->round & 1) ? a.q[1] : a.q[0]), c->dense ? a.nv : c->fsize, c->dense != 0};
   return {a.dying, c->ndying, false};
 }
 
@@ -142,12 +144,14 @@ struct OpPair {
         nxt[u] = ch ? pr.x : pr.y;
       }
     }
+    bool t[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      bool t = ok[u] && p[u] < cur[u] && p[u] < nxt[u];
-      old[u] = t ? atomicMin(lab + 2 * (size_t)dst[u] + nh, p[u]) : L(0);
-      act[u] = t && p[u] < old[u] && old[u] >= cur[u];  // first drop below the snapshot
+    for (int u = 0; u < kU; ++u) {  // issue all atomics before consuming any result
+      t[u] = ok[u] && p[u] < cur[u] && p[u] < nxt[u];
+      old[u] = t[u] ? atomicMin(lab + 2 * (size_t)dst[u] + nh, p[u]) : L(0);
     }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) act[u] = t[u] && old[u] >= cur[u];  // first drop below snapshot
   }
 };
 
@@ -168,8 +172,11 @@ struct OpMark {
     for (int u = 0; u < kU; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
 #pragma unroll
     for (int u = 0; u < kU; ++u) t[u] = ok[u] && alive[dst[u]] && mark[dst[u]] != stamp;
+    uint32_t old[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) act[u] = t[u] && atomicExch(mark + dst[u], stamp) != stamp;
+    for (int u = 0; u < kU; ++u) old[u] = t[u] ? atomicExch(mark + dst[u], stamp) : stamp;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) act[u] = old[u] != stamp;
   }
 };
 
@@ -187,11 +194,22 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   const Src src = resolve_src(a, ctl);
   const bool sync = a.src_mode == 0 && round > 0;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  WarpQueue wq{sq[warp], 0, a.q[(round + 1) & 1], &ctl->nsize};
+  WarpQueue wq{sq[warp], 0, ((round & 1) ? a.q[0] : a.q[1]), &ctl->nsize};
   unsigned long long my_edges = 0, my_large = 0;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsTB;
-  for (uint64_t c = (uint64_t)blockIdx.x * kWarpsTB + warp; c * 32 < src.n; c += nwarps) {
-    uint64_t i = c * 32 + lane;
+  // dynamic fetch: a warp grabs kChunkGrab chunks of 32 frontier items at a time
+  const uint32_t nchunks = (src.n + 31) / 32;
+  uint32_t c = 0, c_end = 0;
+  for (;;) {
+    if (c == c_end) {
+      uint32_t g = 0;
+      if (lane == 0) g = atomicAdd(&ctl->chunk_head, 1u);
+      g = __shfl_sync(kFull, g, 0);
+      c = g * kChunkGrab;
+      if (c >= nchunks) break;
+      c_end = min(c + kChunkGrab, nchunks);
+    }
+    uint64_t i = (uint64_t)c * 32 + lane;
+    ++c;
     uint32_t v = 0;
     int64_t s = 0, deg = 0;
     L sv = 0;
@@ -253,12 +271,39 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
   if (!n) return;
   const uint32_t round = ctl->round;
   op.begin(round);
-  WarpQueue wq{sq[threadIdx.x >> 5], 0, a.q[(round + 1) & 1], &ctl->nsize};
-  for (uint32_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
-    const uint32_t v = a.largeq[idx];
-    const int64_t s = a.off[v], end = a.off[v + 1];
-    const L sv = op.src_val(v);
-    for (int64_t b = s; b < end; b += kTB * kU) {
+  WarpQueue wq{sq[threadIdx.x >> 5], 0, ((round & 1) ? a.q[0] : a.q[1]), &ctl->nsize};
+  // Block-level gather over batches of kBatch CTA-bin vertices: the batch's
+  // edges are numbered through a shared-memory prefix and all 256 x kU slots
+  // of each step are filled, whatever the individual degrees are.
+  __shared__ int64_t bstart[kBatch];
+  __shared__ long long bexcl[kBatch + 1];
+  __shared__ L bsv[kBatch];
+  __shared__ uint32_t bhead;
+  // batch b takes queue entries b, b+NB, b+2NB, ... so that batches mix the
+  // (degree-correlated) queue order and carry similar edge totals
+  const uint32_t nb = (n + kBatch - 1) / kBatch;
+  for (;;) {
+    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    __syncthreads();
+    const uint32_t bidx = bhead;
+    if (bidx >= nb) break;
+    if (threadIdx.x < 32) {
+      const uint32_t i = bidx + threadIdx.x * nb;
+      long long d = 0;
+      if (threadIdx.x < kBatch && i < n) {
+        const uint32_t v = a.largeq[i];
+        const int64_t s = a.off[v];
+        d = a.off[v + 1] - s;
+        bstart[threadIdx.x] = s;
+        bsv[threadIdx.x] = op.src_val(v);
+      }
+      const long long incl = warp_incl_scan(d);
+      if (threadIdx.x < kBatch) bexcl[threadIdx.x + 1] = incl;
+      if (threadIdx.x == 0) bexcl[0] = 0;
+    }
+    __syncthreads();
+    const long long total = bexcl[kBatch];
+    for (long long b = 0; b < total; b += kTB * kU) {
       int64_t e[kU];
       bool ok[kU];
       L svs[kU];
@@ -266,14 +311,20 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
       bool act[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        e[u] = b + u * kTB + threadIdx.x;
-        ok[u] = e[u] < end;
-        svs[u] = sv;
+        const long long slot = b + u * kTB + threadIdx.x;
+        ok[u] = slot < total;
+        uint32_t lo = 0;  // owner: last o with bexcl[o] <= slot (branchless, kBatch == 32)
+#pragma unroll
+        for (uint32_t step = kBatch / 2; step; step >>= 1)
+          lo = bexcl[lo + step] <= slot ? lo + step : lo;
+        e[u] = bstart[lo] + (slot - bexcl[lo]);
+        svs[u] = bsv[lo];
       }
       op.relax(a, e, ok, svs, dst, act);
 #pragma unroll
       for (int u = 0; u < kU; ++u) wq.push(act[u], dst[u]);
     }
+    __syncthreads();
   }
   wq.flush();
 }
@@ -318,7 +369,8 @@ template <class Op, bool BLOCKED>
 __global__ void __launch_bounds__(kTB) k_push_lb(PushArgs a, Op op) {
   using L = typename Op::L;
   __shared__ uint32_t sq[kWarpsTB][kWQ];
-  __shared__ int64_t spre[kHugeSmem];
+  __shared__ int64_t spre[kHugeSmem], sstart[kHugeSmem];
+  __shared__ unsigned long long sval[kHugeSmem];
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
   const uint32_t nh = ctl->nhuge;
@@ -326,13 +378,13 @@ __global__ void __launch_bounds__(kTB) k_push_lb(PushArgs a, Op op) {
   const int64_t E = (int64_t)ctl->huge_edges;
   const uint32_t round = ctl->round;
   op.begin(round);
-  const int64_t *pre = a.hpre;
-  if (nh <= kHugeSmem) {
-    for (uint32_t i = threadIdx.x; i < nh; i += kTB) spre[i] = a.hpre[i];
+  const bool staged = nh <= kHugeSmem;
+  if (staged) {
+    for (uint32_t i = threadIdx.x; i < nh; i += kTB)
+      spre[i] = a.hpre[i], sstart[i] = a.hstart[i], sval[i] = a.hval[i];
     __syncthreads();
-    pre = spre;
   }
-  WarpQueue wq{sq[threadIdx.x >> 5], 0, a.q[(round + 1) & 1], &ctl->nsize};
+  WarpQueue wq{sq[threadIdx.x >> 5], 0, ((round & 1) ? a.q[0] : a.q[1]), &ctl->nsize};
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
@@ -348,9 +400,16 @@ __global__ void __launch_bounds__(kTB) k_push_lb(PushArgs a, Op op) {
       const int64_t p = p0 + u;
       const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
       ok[u] = p < passes && g < E;
-      uint32_t o = ok[u] ? owner_search(pre, nh, g) : 0u;
-      e[u] = ok[u] ? a.hstart[o] + (g - (o ? pre[o - 1] : 0)) : 0;
-      sv[u] = ok[u] ? (L)a.hval[o] : L(0);
+      const int64_t gg = ok[u] ? g : 0;
+      if (staged) {  // shared-memory bisection (LDS), find_owner (worklist.py:96-119)
+        const uint32_t o = owner_search(spre, nh, gg);
+        e[u] = sstart[o] + (gg - (o ? spre[o - 1] : 0));
+        sv[u] = (L)sval[o];
+      } else {
+        const uint32_t o = owner_search(a.hpre, nh, gg);
+        e[u] = a.hstart[o] + (gg - (o ? a.hpre[o - 1] : 0));
+        sv[u] = (L)a.hval[o];
+      }
     }
     op.relax(a, e, ok, sv, dst, act);
 #pragma unroll
