@@ -83,6 +83,8 @@ typedef struct sg_round { /* one BSP round (engine.py:116-163) */
   int64_t updated;        /* vertices whose label changed (next frontier / dying) */
   int64_t comm_sent;      /* engine.py:225-229 (devices > 1) */
   int64_t comm_broadcast; /* engine.py:232-234 (devices > 1) */
+  int64_t launches_twc;   /* inspect+twc launches: devices with a non-empty local frontier */
+  int64_t launches_lb;    /* lb launches: devices whose local frontier had huge vertices */
 } sg_round;
 
 const char *sg_last_error(void);
@@ -124,6 +126,15 @@ typedef struct sg_kernel_time { /* per-kernel totals of a profiled run */
 int sg_run_profiled(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
                     int64_t rounds_cap, int64_t *nrounds, double *ms_out, sg_kernel_time *kt,
                     int32_t kt_cap, int32_t *nkt);
+
+/* --- multi-GPU edge cut (engine.py:64-113): one partition per rank over NCCL.
+ * sg_nccl_unique_id on rank 0, broadcast the 128 bytes out of band (e.g.
+ * torch.distributed), then every rank calls sg_dist_run on the same graph.
+ * bfs / sssp / cc; labels_out receives the merged labels on every rank. */
+int sg_nccl_unique_id(uint8_t id_out[128]);
+int sg_dist_run(sg_graph *g, const sg_params *p, const uint8_t nccl_id[128], int32_t rank,
+                int32_t world, double *labels_out, sg_round *rounds_out, int64_t rounds_cap,
+                int64_t *nrounds, double *ms_out);
 
 /* --- kernel level: the reference plugin API (_kernels_py.py:88-201) ------ */
 int sg_lb_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,

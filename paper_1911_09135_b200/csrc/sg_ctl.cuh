@@ -28,12 +28,27 @@ struct Ctl {
   unsigned long long comm_sent;
   unsigned long long comm_bcast;
   unsigned long long large_edges;  // edges of CTA-bin vertices this round
+  uint32_t part_twc_mask;  // devices>1 accounting: partitions with a non-empty local frontier
+  uint32_t part_lb_mask;   // ... whose local frontier holds a huge vertex
 };
+
+// Edge-cut partition of a traversal view (engine.py:64-85): partition d owns
+// rows [c[d], c[d+1]).  D == 1 disables the per-partition accounting.
+constexpr int kMaxParts = 32;
+struct Cuts {
+  long long c[kMaxParts + 1];
+  int D;
+};
+__device__ __forceinline__ int owner_of(const Cuts &k, uint32_t v) {
+  int d = 0;
+  while (d + 1 < k.D && (long long)v >= k.c[d + 1]) ++d;
+  return d;
+}
 
 // one record per round, layout == sg_round (include/simtgraph_cuda.h)
 struct RoundStat {
   long long frontier_size, active_edges, huge_count, huge_edges, large_count, large_edges,
-      updated, comm_sent, comm_broadcast;
+      updated, comm_sent, comm_broadcast, launches_twc, launches_lb;
 };
 static_assert(sizeof(RoundStat) == sizeof(sg_round), "RoundStat must mirror sg_round");
 
@@ -48,6 +63,7 @@ struct WarpQueue {
   uint32_t *gcount;
 
   __device__ __forceinline__ void flush() {
+    if (!gq) return;
     __syncwarp();
     uint32_t base = 0;
     if (lane_id() == 0 && n) base = atomicAdd(gcount, n);
@@ -56,8 +72,10 @@ struct WarpQueue {
     __syncwarp();
     n = 0;
   }
-  // must be called by all 32 lanes (converged)
+  // must be called by all 32 lanes (converged); a null queue discards (partitioned
+  // runs rebuild frontiers from the exchanged labels instead)
   __device__ __forceinline__ void push(bool p, uint32_t v) {
+    if (!gq) return;
     uint32_t m = __ballot_sync(kFull, p);
     if (!m) return;
     if (p) buf[n + __popc(m & lanemask_lt())] = v;

@@ -38,6 +38,11 @@ void random_weights_device(int64_t ne, const uint64_t pcg[4], int64_t low, int j
                            int64_t *w64);
 void weights_finalize(Graph &g);  // wmin / wmax / w32 from w64
 
+// edge-cut partitioned push apps, D partitions on this GPU (sg_dist.cu)
+void run_push_local_partitions(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds,
+                               double *labels_out, sg_round *rounds_out, int64_t cap,
+                               int64_t *nrounds, double *ms_out);
+
 }  // namespace sg
 
 struct sg_graph {

@@ -27,6 +27,8 @@ struct PullArgs {
   int dynamic_bins;  // 1: kcore (bins found per round); 0: pr (static bins, dense rows)
   uint32_t *dying;   // kcore dying list (count ctl->ndying)
   RoundStat *stats;
+  Cuts cuts;                // devices > 1: partition accounting (engine.py:215-234)
+  const uint32_t *mcount;   // mirror_count per vertex (devices > 1), else nullptr
 };
 
 // pr: acc = sum aux[u]; new = (1-d) + d*acc (two roundings, as numpy); aux' = new*inv
@@ -37,9 +39,11 @@ struct PrOp {
   double *rank;
   const double *inv;
   double d, omd;
+  const uint32_t *mcount = nullptr;  // devices > 1: comm_broadcast of changed ranks
   const double *aux = nullptr;
   double *auxn = nullptr;
   double dmax = 0.0;
+  unsigned long long bcast = 0;
   __device__ __forceinline__ void begin(uint32_t round) {
     aux = (round & 1) ? aux1 : aux0;
     auxn = (round & 1) ? next1 : next0;
@@ -47,8 +51,10 @@ struct PrOp {
   __device__ __forceinline__ A load(uint32_t u) const { return __ldg(aux + u); }
   __device__ __forceinline__ bool finish(uint32_t v, A acc) {
     double nw = __dadd_rn(omd, __dmul_rn(d, acc));
-    double dl = fabs(__dsub_rn(nw, rank[v]));
+    const double old = rank[v];
+    double dl = fabs(__dsub_rn(nw, old));
     dmax = dl > dmax ? dl : dmax;
+    if (mcount && nw != old) bcast += mcount[v];  // engine.py:232-234
     rank[v] = nw;
     auxn[v] = __dmul_rn(nw, inv[v]);
     return false;
@@ -60,7 +66,8 @@ struct KcOp {
   using A = uint32_t;
   const uint8_t *alive;
   uint32_t k;
-  double dmax = 0.0;  // unused
+  double dmax = 0.0;            // unused
+  unsigned long long bcast = 0;  // unused (kcore counts broadcasts at the kill)
   __device__ __forceinline__ void begin(uint32_t) {}
   __device__ __forceinline__ A load(uint32_t u) const { return alive[u]; }
   __device__ __forceinline__ bool finish(uint32_t, A acc) const { return acc < k; }
@@ -101,6 +108,13 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
       warp_append(huge, v, a.hugeq, &ctl->nhuge);
       warp_append(large, v, a.largeq, &ctl->nlarge);
       if (large) my_large += (unsigned long long)deg;
+      if (a.cuts.D > 1) {  // which simulated devices launch inspect/twc and lb this round
+        const uint32_t bit = valid ? 1u << owner_of(a.cuts, v) : 0u;
+        const uint32_t tw = __reduce_or_sync(kFull, bit);
+        const uint32_t lb = __reduce_or_sync(kFull, huge ? bit : 0u);
+        if (lane == 0 && tw) atomicOr(&ctl->part_twc_mask, tw);
+        if (lane == 0 && lb) atomicOr(&ctl->part_lb_mask, lb);
+      }
     }
     const bool mine = valid && !huge && !large;
     const uint32_t gd = mine ? (uint32_t)deg : 0u;
@@ -158,6 +172,10 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
       for (int w = 1; w < kWarpsTB; ++w) m = redd[w] > m ? redd[w] : m;
       if (m > 0) atomic_max_dbits(&ctl->delta_bits, m);
     }
+    if (a.mcount) {
+      unsigned long long b = warp_sum(op.bcast);
+      if (lane == 0 && b) atomicAdd(&ctl->comm_bcast, b);
+    }
   }
 }
 
@@ -192,10 +210,11 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
   }
   if (sizeof(typename Op::A) == 8 && threadIdx.x == 0 && op.dmax > 0)
     atomic_max_dbits(&ctl->delta_bits, op.dmax);
+  if (threadIdx.x == 0 && op.bcast) atomicAdd(&ctl->comm_bcast, op.bcast);
 }
 
 // PrefixWork of the huge rows (no labels needed for pull)
-__global__ void __launch_bounds__(1024) k_pull_prefix(PullArgs a) {
+static __global__ void __launch_bounds__(1024) k_pull_prefix(PullArgs a) {
   __shared__ long long red[32];
   __shared__ long long carry;
   Ctl *ctl = a.ctl;
@@ -286,6 +305,7 @@ struct PrStop {            // apps.py:163-171, 183-185 evaluated on the device
   int64_t max_rounds;
   cudaGraphConditionalHandle cond;
   int use_cond;
+  int parts_nonempty;      // devices > 1: partitions with rows (each launches every round)
 };
 
 template <class Op, bool PR>
@@ -304,6 +324,11 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
     if (op.finish(v, acc)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
   }
   if (!PR) return;
+  __shared__ unsigned long long redb[32];
+  if (a.mcount) {
+    unsigned long long b = block_sum(op.bcast, redb);
+    if (threadIdx.x == 0 && b) atomicAdd(&ctl->comm_bcast, b);
+  }
   double m = warp_max(op.dmax);
   if (lane_id() == 0) redd[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -323,7 +348,10 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
     st.large_edges = (long long)ctl->large_edges;
     st.updated = a.nv;
     st.comm_sent = 0;
-    st.comm_broadcast = 0;
+    st.comm_broadcast = (long long)ctl->comm_bcast;
+    st.launches_twc = a.cuts.D > 1 ? stop.parts_nonempty : 1;
+    st.launches_lb = a.cuts.D > 1 ? __popc(ctl->part_lb_mask) : nh > 0;
+    ctl->comm_bcast = 0;
     ctl->delta_bits = 0;
     ctl->large_head = 0;
     ctl->round = round + 1;

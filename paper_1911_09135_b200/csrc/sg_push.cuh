@@ -52,17 +52,29 @@ struct PushArgs {
   int64_t threshold;      // huge threshold; INT64_MAX = twc (no huge bin)
   int src_mode;           // 0 frontier, 1 kcore dying list
   RoundStat *stats;
+  int no_enqueue;         // partitioned runs: frontiers come from the label exchange
+  uint32_t dense_lo, dense_n;  // a dense frontier is [dense_lo, dense_lo + dense_n)
 };
+
+__device__ __forceinline__ uint32_t *next_queue(const PushArgs &a, uint32_t round) {
+  return a.no_enqueue ? nullptr : ((round & 1) ? a.q[0] : a.q[1]);
+}
 
 struct Src {
   const uint32_t *list;
   uint32_t n;
   bool dense;
+  uint32_t lo;
+  __device__ __forceinline__ uint32_t at(uint64_t i) const {
+    return dense ? lo + (uint32_t)i : list[i];
+  }
 };
 
 __device__ __forceinline__ Src resolve_src(const PushArgs &a, const Ctl *c) {
-  if (a.src_mode == 0) return {((c->round & 1) ? a.q[1] : a.q[0]), c->dense ? a.nv : c->fsize, c->dense != 0};
-  return {a.dying, c->ndying, false};
+  if (a.src_mode == 0)
+    return {((c->round & 1) ? a.q[1] : a.q[0]), c->dense ? a.dense_n : c->fsize, c->dense != 0,
+            a.dense_lo};
+  return {a.dying, c->ndying, false, 0};
 }
 
 // ------------------------------------------------------------------ ops --
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   const Src src = resolve_src(a, ctl);
   const bool sync = a.src_mode == 0 && round > 0;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  WarpQueue wq{sq[warp], 0, ((round & 1) ? a.q[0] : a.q[1]), &ctl->nsize};
+  WarpQueue wq{sq[warp], 0, next_queue(a, round), &ctl->nsize};
   unsigned long long my_edges = 0, my_large = 0;
   // dynamic fetch: a warp grabs kChunkGrab chunks of 32 frontier items at a time
   const uint32_t nchunks = (src.n + 31) / 32;
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
     int64_t s = 0, deg = 0;
     L sv = 0;
     if (i < src.n) {
-      v = src.dense ? (uint32_t)i : src.list[i];
+      v = src.at(i);
       s = a.off[v];
       deg = a.off[v + 1] - s;
       sv = op.src_val(v);
@@ -271,7 +283,7 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
   if (!n) return;
   const uint32_t round = ctl->round;
   op.begin(round);
-  WarpQueue wq{sq[threadIdx.x >> 5], 0, ((round & 1) ? a.q[0] : a.q[1]), &ctl->nsize};
+  WarpQueue wq{sq[threadIdx.x >> 5], 0, next_queue(a, round), &ctl->nsize};
   // Block-level gather over batches of kBatch CTA-bin vertices: the batch's
   // edges are numbered through a shared-memory prefix and all 256 x kU slots
   // of each step are filled, whatever the individual degrees are.
@@ -384,7 +396,7 @@ __global__ void __launch_bounds__(kTB) k_push_lb(PushArgs a, Op op) {
       spre[i] = a.hpre[i], sstart[i] = a.hstart[i], sval[i] = a.hval[i];
     __syncthreads();
   }
-  WarpQueue wq{sq[threadIdx.x >> 5], 0, ((round & 1) ? a.q[0] : a.q[1]), &ctl->nsize};
+  WarpQueue wq{sq[threadIdx.x >> 5], 0, next_queue(a, round), &ctl->nsize};
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;

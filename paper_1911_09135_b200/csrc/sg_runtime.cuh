@@ -1,0 +1,477 @@
+// sg_runtime.cuh — host runtime shared by the BSP drivers (single device:
+// sg_engine.cu; edge-cut partitions: sg_dist.cu): kernel launcher (plain /
+// CUDA-event profiled), device-resident run buffers, init/advance kernels and
+// the push / pull round sequences.
+#pragma once
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <unordered_map>
+
+#include "sg_graph.cuh"
+#include "sg_pull.cuh"
+
+namespace sg {
+namespace {
+
+constexpr int64_t kNoHuge = std::numeric_limits<int64_t>::max();
+
+template <class K>
+int occupancy_grid(K kernel, int block, int cap_per_sm = 8) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find((const void *)kernel);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+  per_sm = std::max(1, std::min(per_sm, cap_per_sm));
+  int g = persistent_grid(per_sm);
+  cache[(const void *)kernel] = g;
+  return g;
+}
+
+inline int grid_n(int64_t n, int block = 256) {
+  int64_t g = (n + block - 1) / block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sm_info().sms * 32));
+}
+
+// Launches round kernels: plain (graph capture) or bracketed by CUDA events.
+struct Launcher {
+  bool profile = false;
+  std::vector<std::tuple<const char *, cudaEvent_t, cudaEvent_t>> pending;
+  std::vector<cudaEvent_t> pool;
+  std::map<std::string, std::pair<int64_t, double>> totals;
+  std::vector<std::string> order;
+
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    SG_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  template <class K, class... A>
+  void go(const char *name, K kernel, int grid, int block, cudaStream_t s, A... args) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (profile) {
+      e0 = ev(), e1 = ev();
+      SG_CUDA(cudaEventRecord(e0, s));
+    }
+    kernel<<<grid, block, 0, s>>>(args...);
+    SG_CUDA(cudaGetLastError());
+    if (profile) {
+      SG_CUDA(cudaEventRecord(e1, s));
+      pending.emplace_back(name, e0, e1);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+  }
+  void collect() {
+    for (auto &t : pending) {
+      float ms = 0;
+      SG_CUDA(cudaEventElapsedTime(&ms, std::get<1>(t), std::get<2>(t)));
+      std::string n = std::get<0>(t);
+      if (!totals.count(n)) order.push_back(n);
+      totals[n].first += 1;
+      totals[n].second += ms;
+      pool.push_back(std::get<1>(t));
+      pool.push_back(std::get<2>(t));
+    }
+    pending.clear();
+  }
+  ~Launcher() {
+    for (auto &t : pending) pool.push_back(std::get<1>(t)), pool.push_back(std::get<2>(t));
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// round context handed to every round body
+struct RoundCtx {
+  Launcher &L;
+  cudaStream_t s;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+
+// ------------------------------------------------------------ init kernels --
+template <class T>
+__global__ void k_fill(T *p, int64_t n, T v) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) p[i] = v;
+}
+template <class T>
+__global__ void k_set1(T *p, int64_t i, T v) { p[i] = v; }
+
+__global__ void k_ctl_init(Ctl *ctl, int32_t dense, uint32_t fsize) {
+  *ctl = Ctl{};
+  ctl->dense = dense;
+  ctl->fsize = fsize;
+}
+
+__global__ void k_labels_u32(const uint32_t *lab, int64_t n, double *out) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = lab[i] == kInf32 ? INFINITY : (double)lab[i];
+}
+__global__ void k_iota_pairs(uint32_t *p, int64_t n) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    reinterpret_cast<uint2 *>(p)[i] = make_uint2((uint32_t)i, (uint32_t)i);
+}
+// after R rounds the half written last, R & 1, holds every final label
+__global__ void k_labels_pair_u32(const uint32_t *lab, int64_t n, const Ctl *ctl, double *out) {
+  const uint32_t h = ctl->round & 1;
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    uint32_t x = lab[2 * i + h];
+    out[i] = x == kInf32 ? INFINITY : (double)x;
+  }
+}
+__global__ void k_labels_pair_f64(const unsigned long long *lab, int64_t n, const Ctl *ctl,
+                                  double *out) {
+  const uint32_t h = ctl->round & 1;
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = __longlong_as_double((long long)lab[2 * i + h]);
+}
+__global__ void k_labels_alive(const uint8_t *a, int64_t n, double *out) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = a[i] ? 1.0 : 0.0;
+}
+
+// inv_outdeg (apps.py:158-161), rank_0 = 1-d and round-0 aux = rank*inv (apps.py:162,176)
+__global__ void k_pr_init(const int64_t *off, int64_t n, double omd, double *inv, double *rank,
+                          double *aux) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += st) {
+    int64_t d = off[v + 1] - off[v];
+    double iv = d > 0 ? 1.0 / (double)d : 0.0;
+    inv[v] = iv;
+    rank[v] = omd;
+    aux[v] = __dmul_rn(omd, iv);
+  }
+}
+// gain[v] = sum_{u->v} inv[u] in CSC (== CSR edge) order, exactly as
+// np.bincount accumulates it (apps.py:166-168): a warp loads 32 terms, every
+// lane folds them sequentially through shuffles; max over v by atomicMax.
+__global__ void k_pr_gain_max(const int64_t *off, const uint32_t *col, int64_t n,
+                              const double *inv, unsigned long long *maxbits) {
+  int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double best = 0.0;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+    double acc = 0.0;
+    const int64_t e = off[v + 1];
+    for (int64_t b = off[v]; b < e; b += 32) {
+      int64_t j = b + lane_id();
+      double x = j < e ? inv[col[j]] : 0.0;
+      int cnt = (int)min((int64_t)32, e - b);
+      for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, __shfl_sync(kFull, x, t));
+    }
+    best = acc > best ? acc : best;
+  }
+  if (lane_id() == 0 && best > 0)
+    atomicMax(maxbits, (unsigned long long)__double_as_longlong(best));
+}
+
+// static bins of a dense pull view (pr): CTA-bin rows and huge rows
+__global__ void k_static_bins(const int64_t *off, uint32_t n, int64_t thr, uint32_t *largeq,
+                              uint32_t *hugeq, Ctl *ctl, Cuts cuts) {
+  uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long le = 0;
+  uint32_t lbm = 0;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < n; b += st) {
+    uint64_t v = b + threadIdx.x;
+    int64_t d = v < n ? off[v + 1] - off[v] : 0;
+    bool huge = v < n && d >= thr;
+    bool large = v < n && !huge && d >= (int64_t)kLarge;
+    if (large) le += (unsigned long long)d;
+    if (huge && cuts.D > 1) lbm |= 1u << owner_of(cuts, (uint32_t)v);
+    warp_append(huge, (uint32_t)v, hugeq, &ctl->nhuge);
+    warp_append(large, (uint32_t)v, largeq, &ctl->nlarge);
+  }
+  le = warp_sum(le);
+  lbm = __reduce_or_sync(kFull, lbm);
+  if (lane_id() == 0 && le) atomicAdd(&ctl->large_edges, le);
+  if (lane_id() == 0 && lbm) atomicOr(&ctl->part_lb_mask, lbm);
+}
+
+// ------------------------------------------------- edge-cut partitioning --
+// make_partition (engine.py:64-85): cut_k = searchsorted(off, round(k*E/D), 'left'),
+// kept monotone; Python's round() is round-half-even == rint() by default.
+__global__ void k_cuts(const int64_t *off, int64_t nv, int D, long long *cuts) {
+  if (threadIdx.x || blockIdx.x) return;
+  const long long E = off[nv];
+  cuts[0] = 0;
+  for (int k = 1; k < D; ++k) {
+    const long long target = (long long)rint((double)((long long)k * E) / (double)D);
+    int64_t lo = 0, hi = nv + 1;  // first i with off[i] >= target
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (off[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    cuts[k] = lo > cuts[k - 1] ? lo : cuts[k - 1];
+  }
+  cuts[D] = nv;
+}
+// mirror_count[v] = #partitions (other than v's owner) whose rows point at v
+__global__ void k_mirror_bits(const int64_t *off, const uint32_t *col, int64_t nv, Cuts cuts,
+                              uint32_t *bits) {
+  int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nv; u += warps) {
+    const int d = owner_of(cuts, (uint32_t)u);
+    const uint32_t bit = 1u << d;
+    for (int64_t e = off[u] + lane_id(); e < off[u + 1]; e += 32) {
+      const uint32_t t = col[e];
+      if ((t < cuts.c[d] || t >= cuts.c[d + 1]) && !(bits[t] & bit)) atomicOr(bits + t, bit);
+    }
+  }
+}
+__global__ void k_popc(uint32_t *bits, int64_t n) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    bits[i] = __popc(bits[i]);
+}
+
+inline Cuts make_cuts(const View &v, int D) {
+  if (D < 1 || D > kMaxParts)
+    throw Error(SG_ECONFIG, "devices must be in [1, " + std::to_string(kMaxParts) + "]");
+  Cuts c{};
+  c.D = D;
+  c.c[0] = 0, c.c[1] = v.nv;
+  if (D == 1) return c;
+  DBuf<long long> d(D + 1);
+  k_cuts<<<1, 1>>>(v.off.p, v.nv, D, d.p);
+  SG_CUDA(cudaGetLastError());
+  SG_CUDA(cudaMemcpy(c.c, d.p, sizeof(long long) * (D + 1), cudaMemcpyDeviceToHost));
+  return c;
+}
+inline void mirror_counts(const View &v, const Cuts &c, uint32_t *mc) {
+  SG_CUDA(cudaMemset(mc, 0, sizeof(uint32_t) * std::max<int64_t>(v.nv, 1)));
+  k_mirror_bits<<<grid_n(v.nv * 32), 256>>>(v.off.p, v.col.p, v.nv, c, mc);
+  SG_CUDA(cudaGetLastError());
+  k_popc<<<grid_n(v.nv), 256>>>(mc, v.nv);
+  SG_CUDA(cudaGetLastError());
+  SG_CUDA(cudaDeviceSynchronize());
+}
+
+// ------------------------------------------------------- advance kernels --
+struct Loop {
+  int64_t limit, max_rounds;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+
+__device__ __forceinline__ void loop_test(Ctl *ctl, uint32_t round, bool empty, const Loop &lp) {
+  if (empty) ctl->done = 1;
+  else if ((int64_t)round + 1 >= lp.limit)
+    ctl->error = (int64_t)round + 1 >= lp.max_rounds ? SG_ECONVERGE : SG_ENOMEM, ctl->done = 1;
+  if (lp.use_cond) cudaGraphSetConditional(lp.cond, ctl->done ? 0u : 1u);
+}
+
+// round bookkeeping (the parity-paired labels need no commit pass)
+__global__ void k_push_advance(PushArgs a, Loop lp) {
+  Ctl *ctl = a.ctl;
+  if (threadIdx.x) return;
+  if (ctl->done) {
+    if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+    return;
+  }
+  const uint32_t round = ctl->round;
+  const uint32_t nn = ctl->nsize;
+  RoundStat &s = a.stats[round];
+  s.frontier_size = ctl->dense ? a.nv : ctl->fsize;
+  s.active_edges = (long long)ctl->edges;
+  s.huge_count = ctl->nhuge;
+  s.huge_edges = (long long)ctl->huge_edges;
+  s.large_count = ctl->nlarge;
+  s.large_edges = (long long)ctl->large_edges;
+  s.updated = nn;
+  s.comm_sent = (long long)ctl->comm_sent;
+  s.comm_broadcast = (long long)ctl->comm_bcast;
+  s.launches_twc = s.frontier_size > 0;
+  s.launches_lb = ctl->nhuge > 0;
+  ctl->fsize = nn;
+  ctl->nsize = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_sent = ctl->comm_bcast = 0;
+  ctl->dense = 0;
+  ctl->ticket = 0;
+  ctl->round = round + 1;
+  loop_test(ctl, round, nn == 0, lp);
+  __threadfence();
+}
+
+// kcore: kill the dying (apps.py:225); devices > 1: their mirrors get the broadcast
+__global__ void k_kcore_kill(PullArgs a, uint8_t *alive) {
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t nd = ctl->ndying;
+  unsigned long long b = 0;
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += st) {
+    const uint32_t v = a.dying[i];
+    alive[v] = 0;
+    if (a.mcount) b += a.mcount[v];
+  }
+  b = warp_sum(b);
+  if (lane_id() == 0 && b) atomicAdd(&ctl->comm_bcast, b);
+}
+// record the count-phase stats; the neighbour walk then reuses the CTA-bin queue
+__global__ void k_kcore_reset(PullArgs a) {
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  RoundStat &s = a.stats[ctl->round];
+  s.frontier_size = ctl->dense ? a.nv : ctl->fsize;
+  s.active_edges = (long long)ctl->edges;
+  s.huge_count = ctl->nhuge;
+  s.huge_edges = (long long)ctl->huge_edges;
+  s.large_count = ctl->nlarge;
+  s.large_edges = (long long)ctl->large_edges;
+  s.updated = ctl->ndying;
+  s.comm_sent = 0;
+  s.comm_broadcast = (long long)ctl->comm_bcast;
+  s.launches_twc = a.cuts.D > 1 ? __popc(ctl->part_twc_mask) : s.frontier_size > 0;
+  s.launches_lb = a.cuts.D > 1 ? __popc(ctl->part_lb_mask) : ctl->nhuge > 0;
+  ctl->comm_bcast = 0;
+  ctl->part_twc_mask = ctl->part_lb_mask = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
+  ctl->huge_edges = ctl->large_edges = 0;
+}
+
+__global__ void k_kcore_advance(Ctl *ctl, Loop lp) {
+  if (ctl->done) {
+    if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+    return;
+  }
+  const uint32_t round = ctl->round;
+  const uint32_t nd = ctl->ndying, nn = ctl->nsize;
+  ctl->fsize = nn;
+  ctl->nsize = 0;
+  ctl->ndying = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
+  ctl->dense = 0;
+  ctl->round = round + 1;
+  loop_test(ctl, round, nd == 0 || nn == 0, lp);  // apps.py:223-232
+}
+
+// ------------------------------------------------------------ run state --
+struct RunBufs {
+  DBuf<Ctl> ctl;
+  DBuf<RoundStat> stats;
+  int64_t stats_cap = 0;
+  DBuf<uint32_t> q0, q1, largeq, hugeq, dying;
+  DBuf<int64_t> hpre, hstart;
+  DBuf<unsigned long long> hval;
+
+  void alloc_common(int64_t nv, int64_t rounds_cap) {
+    size_t n = (size_t)std::max<int64_t>(nv, 1);
+    ctl.alloc(1);
+    SG_CUDA(cudaMemset(ctl.p, 0, sizeof(Ctl)));
+    stats_cap = rounds_cap;
+    stats.alloc(rounds_cap);
+    q0.alloc(n), q1.alloc(n), largeq.alloc(n), hugeq.alloc(n);
+    hpre.alloc(n), hstart.alloc(n), hval.alloc(n);
+  }
+  PushArgs push_args(const View &v, int64_t thr) {
+    PushArgs a{};
+    a.off = v.off.p;
+    a.col = v.col.p;
+    a.nv = (uint32_t)v.nv;
+    a.ctl = ctl.p;
+    a.q[0] = q0.p, a.q[1] = q1.p;
+    a.largeq = largeq.p, a.hugeq = hugeq.p;
+    a.hpre = hpre.p, a.hstart = hstart.p, a.hval = hval.p;
+    a.dying = dying.p;
+    a.threshold = thr;
+    a.src_mode = 0;
+    a.stats = stats.p;
+    a.no_enqueue = 0;
+    a.dense_lo = 0;
+    a.dense_n = (uint32_t)v.nv;
+    return a;
+  }
+  PullArgs pull_args(const View &v, int64_t thr, int dyn) {
+    PullArgs a{};
+    a.off = v.off.p;
+    a.col = v.col.p;
+    a.nv = (uint32_t)v.nv;
+    a.ctl = ctl.p;
+    a.q[0] = q0.p, a.q[1] = q1.p;
+    a.largeq = largeq.p, a.hugeq = hugeq.p;
+    a.hpre = hpre.p, a.hstart = hstart.p;
+    a.threshold = thr;
+    a.dynamic_bins = dyn;
+    a.dying = dying.p;
+    a.stats = stats.p;
+    return a;
+  }
+};
+
+// A prepared run: buffers allocated, nothing launched yet.
+struct Program {
+  std::function<void(Launcher &, cudaStream_t)> init;  // device state init (timed)
+  std::function<void(RoundCtx &)> round;              // one BSP round
+  std::function<void(Launcher &, cudaStream_t)> finish;  // labels -> out (untimed)
+  std::vector<std::shared_ptr<void>> keep;
+  template <class T>
+  T *buf(int64_t n) {
+    auto b = std::make_shared<DBuf<T>>(std::max<int64_t>(n, 1));
+    keep.push_back(b);
+    return b->p;
+  }
+};
+
+template <class T>
+void fill(Launcher &L, T *p, int64_t n, T v, cudaStream_t s) {
+  if (n > 0) L.go("init", k_fill<T>, grid_n(n), 256, s, p, n, v);
+}
+
+// ----------------------------------------------------------------- apps --
+template <class Op>
+void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
+  c.L.go("push_twc", k_push_twc<Op>, occupancy_grid(k_push_twc<Op>, kTB), kTB, c.s, a, op);
+  c.L.go("push_large", k_push_large<Op>, occupancy_grid(k_push_large<Op>, kTB), kTB, c.s, a, op);
+  if (a.threshold != kNoHuge) {
+    c.L.go("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
+    if (blocked)
+      c.L.go("push_lb", k_push_lb<Op, true>, occupancy_grid(k_push_lb<Op, true>, kTB), kTB, c.s, a,
+             op);
+    else
+      c.L.go("push_lb", k_push_lb<Op, false>, occupancy_grid(k_push_lb<Op, false>, kTB), kTB, c.s,
+             a, op);
+  }
+}
+
+template <class Op>
+void pull_round(RoundCtx &c, const PullArgs &a, const Op &op, bool blocked, typename Op::A *hacc) {
+  c.L.go("pull_twc", k_pull_twc<Op>, occupancy_grid(k_pull_twc<Op>, kTB), kTB, c.s, a, op);
+  c.L.go("pull_large", k_pull_large<Op>, occupancy_grid(k_pull_large<Op>, kTB), kTB, c.s, a, op);
+  if (a.threshold != kNoHuge) {
+    if (a.dynamic_bins) c.L.go("huge_prefix", k_pull_prefix, 1, 1024, c.s, a);
+    if (blocked)
+      c.L.go("pull_lb", k_pull_lb<Op, true>, occupancy_grid(k_pull_lb<Op, true>, kTB), kTB, c.s, a,
+             op, hacc);
+    else
+      c.L.go("pull_lb", k_pull_lb<Op, false>, occupancy_grid(k_pull_lb<Op, false>, kTB), kTB, c.s,
+             a, op, hacc);
+  }
+}
+
+Loop loop_of(const RunBufs &rb, int64_t max_rounds, const RoundCtx &c) {
+  return Loop{std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds, c.cond, c.use_cond};
+}
+
+
+}  // namespace
+}  // namespace sg

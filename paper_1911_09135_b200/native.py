@@ -27,7 +27,7 @@ EXPORTS = (
     "sg_last_error", "sg_device_count", "sg_graph_create", "sg_graph_create_rmat",
     "sg_graph_attach_random_weights", "sg_graph_with_weights", "sg_graph_info",
     "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_run_profiled",
-    "sg_lb_kernel",
+    "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
 )
 
@@ -42,7 +42,8 @@ class Params(ctypes.Structure):
 
 ROUND_DTYPE = np.dtype([("frontier_size", "<i8"), ("active_edges", "<i8"), ("huge_count", "<i8"),
                         ("huge_edges", "<i8"), ("large_count", "<i8"), ("large_edges", "<i8"),
-                        ("updated", "<i8"), ("comm_sent", "<i8"), ("comm_broadcast", "<i8")])
+                        ("updated", "<i8"), ("comm_sent", "<i8"), ("comm_broadcast", "<i8"),
+                        ("launches_twc", "<i8"), ("launches_lb", "<i8")])
 
 
 class KernelTime(ctypes.Structure):
@@ -88,6 +89,9 @@ def load(path: Path | None = None):
             "sg_edge_kernel": ([P, i64, P, i64, P, i64, P, i64, P, P, P, i64, i32, i32, i32, P],
                                ctypes.c_int),
             "sg_kernel_launches": ([], ctypes.c_int64),
+            "sg_nccl_unique_id": ([P], ctypes.c_int),
+            "sg_dist_run": ([P, ctypes.POINTER(Params), P, i32, i32, P, P, i64, P, P],
+                            ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -221,6 +225,27 @@ class DeviceGraph:
                        for i in range(nkt.value)}
             return labels, log, ms.value, kernels
         return labels, log, ms.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    check(load().sg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def dist_run(dev: DeviceGraph, params: Params, nccl_id: bytes, rank: int, world: int,
+             rounds_cap=1 << 16):
+    """One edge-cut partition per rank over NCCL (sg_dist_run); every rank gets
+    the merged labels and the global round log."""
+    nv, _, _ = dev.info()
+    labels = np.empty(nv, dtype=np.float64)
+    rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
+    n = ctypes.c_int64(0)
+    ms = ctypes.c_double(0.0)
+    idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+    check(load().sg_dist_run(dev.handle, ctypes.byref(params), idb, rank, world, ptr(labels),
+                             ptr(rounds), rounds_cap, ctypes.byref(n), ctypes.byref(ms)))
+    return labels, rounds[: min(n.value, rounds_cap)].copy(), ms.value
 
 
 def pcg64_words(seed) -> np.ndarray:

@@ -42,11 +42,20 @@ def _sched(sg, key):
     return sg.Scheduler(kind, threshold=thr)
 
 
-def _check(sg, res, info, app):
+def _check(sg, res, info, app, launches=True):
     rounds = [[r.frontier_size, r.active_edges()] for r in res.records]
     assert rounds == [x[:2] for x in info["per_round"]], "per-round frontier / edges log"
     if app != "pr":
         assert sg.engine.labels_sha256(res.labels) == info["labels_sha256"]
+    if res.devices > 1:  # edge-cut accounting (engine.py:225-234)
+        comm = [[r.comm_sent, r.comm_broadcast] for r in res.records]
+        if app == "pr":  # pr broadcast counts depend on which ranks moved: tolerance mode
+            assert [c[0] for c in comm] == [x[2] for x in info["per_round"]]
+        else:
+            assert comm == [x[2:4] for x in info["per_round"]], "comm_sent / comm_broadcast"
+    rep = sg.report(res)
+    if launches and res.scheduler.kind == "alb":
+        assert rep["totals"]["kernel_launches"] == info["kernel_launches"]
 
 
 @pytest.mark.parametrize("gname", ["rmat10", "uniform10", "rmat12", "rmat14", "rmat16",
@@ -131,7 +140,7 @@ def test_threshold_and_distribution_invariance(sg, golden, app, thr, dist):
     if app == "sssp":
         g = sg.attach_random_weights(g, 2)
     res = sg.run_app(g, app, sg.Scheduler("alb", distribution=dist, threshold=thr))
-    _check(sg, res, info, app)
+    _check(sg, res, info, app, launches=False)
     if app == "pr":
         ref = sg.run_app(_graph(sg, "rmat12"), "pr", sg.Scheduler("twc"))
         assert np.max(np.abs(res.labels - ref.labels)) <= PR_ATOL
@@ -220,3 +229,21 @@ def test_larger_scale_vs_c_oracle(sg, scale, app):
         assert np.max(np.abs(res.labels - lab)) <= PR_ATOL
     else:
         assert np.array_equal(res.labels, lab)
+
+
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc"])
+def test_nccl_edge_cut_single_rank(sg, golden, app):
+    """The NCCL multi-GPU driver (sg_dist_run) with world size 1 on this GPU:
+    partition restriction, NCCL all-reduce(min), diff pass and the NCCL
+    counter reduction all run; labels and round log must match the reference."""
+    from paper_1911_09135_b200 import native
+    info = golden["runs"]["rmat12"][f"{app}/alb/d1"]
+    g = _graph(sg, "rmat12")
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    params = sg.engine._device_params(sg.apps.make_app(app), sg.Scheduler("alb"),
+                                      sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
+    labels, log, ms = native.dist_run(g.device(), params, native.nccl_unique_id(), 0, 1)
+    assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
+    assert [[int(r["frontier_size"]), int(r["active_edges"])] for r in log] == \
+        [x[:2] for x in info["per_round"]]

@@ -50,7 +50,7 @@ def test_library_is_sm100a_only():
 
 def test_round_struct_layout():
     import ctypes
-    assert native.ROUND_DTYPE.itemsize == 9 * 8
+    assert native.ROUND_DTYPE.itemsize == 11 * 8
     assert ctypes.sizeof(native.Params) == 4 * 4 + 8 * 2 + 8 * 2 + 8 * 2 + 4 * 2
 
 
