@@ -1,0 +1,319 @@
+// sg_bm.cuh — single-device ALB push round with a bitmap next-frontier.
+//
+// Same bins and operator as sg_push.cuh (inspection fused into TWC, CTA bin,
+// huge-vertex LB kernel; schedulers.py:252-298, _kernels_py.py:69-85), but
+// the relaxation never waits for an atomic result:
+//
+//   candidate  : p < lab[dst]  (any read during the round is <= the round-start
+//                snapshot, because labels only decrease; an L1-stale value is
+//                only ever too high, so it can add candidates, never drop one)
+//   update     : red.min(lab[dst], p); red.or(next_bitmap[dst / 32], bit)
+//
+// A candidate's label ends the round <= p < snapshot, so it changed; a vertex
+// that changed had a lowering thread whose earlier read was > p, so it was a
+// candidate.  Hence the bitmap is exactly {v : merged[v] < values[v]}, the
+// reference's next frontier (apps.py:71-74), and k_bm_compact turns it into an
+// ascending-within-warp id list plus each vertex's snapshot label.
+//
+// Why: a scattered 4-byte access costs one L1TEX wavefront per lane; the chip
+// sustains ~275 G of them per second (measured, scripts/micro/gather.cu).
+// Atomics with return values add a full round trip per step on top, so the
+// hot kernels issue only fire-and-forget reductions and keep kV independent
+// gathers in flight per lane.
+#pragma once
+#include "sg_push.cuh"
+
+namespace sg {
+
+#ifndef SG_BKV
+#define SG_BKV 8
+#endif
+constexpr int kV = SG_BKV;  // edges per lane per step in the bitmap-frontier kernels
+
+// bfs: frontier vertices of round r carry label r.  vis = visited bitmap
+// (red.or during the round); prev = vis as of the round start, so the next
+// frontier is vis & ~prev; the compaction writes label r + 1.
+struct BmBfs {
+  using L = uint32_t;
+  static constexpr bool kCarry = true;
+  uint32_t *lab, *vis, *prev;
+  uint32_t r = 0;
+  __device__ __forceinline__ void begin(uint32_t round) { r = round; }
+  __device__ __forceinline__ L src_val(uint64_t, uint32_t) const { return r; }
+  __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kV],
+                                        const bool (&ok)[kV], const L (&)[kV]) const {
+    uint32_t dst[kV], w[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kV; ++u) w[u] = ok[u] ? vis[dst[u] >> 5] : ~0u;
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const uint32_t bit = 1u << (dst[u] & 31u);
+      if (!(w[u] & bit)) atomicOr(vis + (dst[u] >> 5), bit);  // RED.OR (result unused)
+    }
+  }
+  // new bits of word wi (and advance prev)
+  __device__ __forceinline__ uint32_t take(uint32_t wi) const {
+    const uint32_t x = vis[wi], n = x & ~prev[wi];
+    if (n) prev[wi] = x;
+    return n;
+  }
+  __device__ __forceinline__ void emit(uint32_t, uint32_t v) const { lab[v] = r + 1; }
+};
+
+// sssp / cc (KIND as OpPair: 0 cc, 1 unit weight, 2 u32 weights, 3 float64 bits)
+template <int KIND>
+struct BmMin {
+  using L = typename std::conditional<KIND == 3, unsigned long long, uint32_t>::type;
+  static constexpr bool kCarry = true;
+  L *lab;
+  const uint32_t *w32;
+  const int64_t *w64;  // KIND 3 (nullptr: unit weights)
+  L *snap;             // snapshot label per frontier slot (written by k_bm_compact)
+  uint32_t *nb;        // next-frontier bitmap
+  __device__ __forceinline__ void begin(uint32_t) {}
+  __device__ __forceinline__ L src_val(uint64_t i, uint32_t) const { return snap[i]; }
+  __device__ __forceinline__ L prop(int64_t e, L sv) const {
+    if (KIND == 0) return sv;
+    if (KIND == 1) return sv + 1u;
+    if (KIND == 2) return sv + ld_stream(w32 + e);
+    double p = __dadd_rn(__longlong_as_double((long long)sv), w64 ? (double)ld_stream(w64 + e) : 1.0);
+    return (L)__double_as_longlong(p);
+  }
+  __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kV],
+                                        const bool (&ok)[kV], const L (&sv)[kV]) const {
+    uint32_t dst[kV];
+    L p[kV], cur[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kV; ++u) p[u] = ok[u] ? prop(e[u], sv[u]) : L(0);
+#pragma unroll
+    for (int u = 0; u < kV; ++u) cur[u] = ok[u] ? lab[dst[u]] : L(0);
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      if (p[u] < cur[u]) {  // ok[u] implied: cur = 0 otherwise
+        atomicMin(lab + dst[u], p[u]);                      // RED.MIN
+        atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));  // RED.OR
+      }
+    }
+  }
+  __device__ __forceinline__ uint32_t take(uint32_t wi) const {
+    const uint32_t x = nb[wi];
+    if (x) nb[wi] = 0u;
+    return x;
+  }
+  __device__ __forceinline__ void emit(uint32_t slot, uint32_t v) const { snap[slot] = lab[v]; }
+};
+
+// ---------------------------------------------------------------- kernels --
+// inspection + TWC small/medium (warp gather); huge / CTA-bin vertices are
+// queued with their snapshot label
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
+  using L = typename Op::L;
+  __shared__ unsigned long long red[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t round = ctl->round;
+  op.begin(round);
+  const Src src = resolve_src(a, ctl);
+  const uint32_t lane = lane_id();
+  unsigned long long my_edges = 0, my_large = 0;
+  const uint32_t nchunks = (src.n + 31) / 32;
+  uint32_t c = 0, c_end = 0;
+  for (;;) {
+    if (c == c_end) {
+      uint32_t g = 0;
+      if (lane == 0) g = atomicAdd(&ctl->chunk_head, 1u);
+      g = __shfl_sync(kFull, g, 0);
+      c = g * kChunkGrab;
+      if (c >= nchunks) break;
+      c_end = min(c + kChunkGrab, nchunks);
+    }
+    const uint64_t i = (uint64_t)c * 32 + lane;
+    ++c;
+    uint32_t v = 0;
+    int64_t s = 0, deg = 0;
+    L sv = 0;
+    if (i < src.n) {
+      v = src.at(i);
+      s = a.off[v];
+      deg = a.off[v + 1] - s;
+      sv = op.src_val(i, v);
+    }
+    my_edges += (unsigned long long)deg;
+    const bool huge = deg >= a.threshold;
+    const bool large = !huge && deg >= (int64_t)kLarge;
+    if (large) my_large += (unsigned long long)deg;
+    const uint32_t hslot = warp_append(huge, v, a.hugeq, &ctl->nhuge);
+    const uint32_t lslot = warp_append(large, v, a.largeq, &ctl->nlarge);
+    if (huge) a.hval[hslot] = (unsigned long long)sv;
+    if (large) a.largesv[lslot] = (unsigned long long)sv;
+    const uint32_t gd = (huge || large) ? 0u : (uint32_t)deg;
+    const uint32_t incl = warp_incl_scan(gd);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    const uint32_t excl = incl - gd;
+    for (uint32_t base = 0; base < total; base += 32 * kV) {
+      int64_t e[kV];
+      bool ok[kV];
+      L svo[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const uint32_t slot = base + u * 32 + lane;
+        const int o = warp_owner(incl, slot);
+        const int64_t so = shfl64(s, o);
+        const uint32_t eo = __shfl_sync(kFull, excl, o);
+        svo[u] = __shfl_sync(kFull, sv, o);
+        ok[u] = slot < total;
+        e[u] = so + (int64_t)(slot - eo);
+      }
+      op.relax(a, e, ok, svo);
+    }
+  }
+  unsigned long long bs = block_sum(my_edges, red);
+  if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+  bs = block_sum(my_large, red);
+  if (threadIdx.x == 0 && bs) atomicAdd(&ctl->large_edges, bs);
+}
+
+// TWC CTA bin: block-level gather over batches of kBatch queued vertices
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
+  using L = typename Op::L;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  __shared__ int64_t bstart[kBatch];
+  __shared__ long long bexcl[kBatch + 1];
+  __shared__ L bsv[kBatch];
+  __shared__ uint32_t bhead;
+  const uint32_t nb = (n + kBatch - 1) / kBatch;
+  for (;;) {
+    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    __syncthreads();
+    const uint32_t bidx = bhead;
+    if (bidx >= nb) break;
+    if (threadIdx.x < 32) {
+      const uint32_t i = bidx + threadIdx.x * nb;  // degree-mixed batch
+      long long d = 0;
+      if (threadIdx.x < kBatch && i < n) {
+        const uint32_t v = a.largeq[i];
+        const int64_t s = a.off[v];
+        d = a.off[v + 1] - s;
+        bstart[threadIdx.x] = s;
+        bsv[threadIdx.x] = (L)a.largesv[i];
+      }
+      const long long incl = warp_incl_scan(d);
+      if (threadIdx.x < kBatch) bexcl[threadIdx.x + 1] = incl;
+      if (threadIdx.x == 0) bexcl[0] = 0;
+    }
+    __syncthreads();
+    const long long total = bexcl[kBatch];
+    for (long long b = 0; b < total; b += kTB * kV) {
+      int64_t e[kV];
+      bool ok[kV];
+      L svs[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const long long slot = b + u * kTB + threadIdx.x;
+        ok[u] = slot < total;
+        uint32_t lo = 0;  // last o with bexcl[o] <= slot (kBatch == 32)
+#pragma unroll
+        for (uint32_t step = kBatch / 2; step; step >>= 1)
+          lo = bexcl[lo + step] <= slot ? lo + step : lo;
+        e[u] = bstart[lo] + (slot - bexcl[lo]);
+        svs[u] = bsv[lo];
+      }
+      op.relax(a, e, ok, svs);
+    }
+    __syncthreads();
+  }
+}
+
+// ALB huge-vertex kernel (Algorithm 2): every thread of every CTA walks the
+// huge edges cyclically (g = p*T + tid) or blocked (g = tid*ceil(e/T) + p)
+template <class Op, bool BLOCKED>
+__global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
+  using L = typename Op::L;
+  __shared__ int64_t spre[kHugeSmem], sstart[kHugeSmem];
+  __shared__ unsigned long long sval[kHugeSmem];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t nh = ctl->nhuge;
+  if (!nh) return;
+  const int64_t E = (int64_t)ctl->huge_edges;
+  op.begin(ctl->round);
+  const bool staged = nh <= kHugeSmem;
+  if (staged) {
+    for (uint32_t i = threadIdx.x; i < nh; i += kTB)
+      spre[i] = a.hpre[i], sstart[i] = a.hstart[i], sval[i] = a.hval[i];
+    __syncthreads();
+  }
+  const int64_t T = (int64_t)gridDim.x * kTB;
+  const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
+  const int64_t passes = (E + T - 1) / T;
+  for (int64_t p0 = 0; p0 < passes; p0 += kV) {
+    int64_t e[kV];
+    bool ok[kV];
+    L sv[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t p = p0 + u;
+      const int64_t g = BLOCKED ? tid * passes + p : p * T + tid;
+      ok[u] = p < passes && g < E;
+      const int64_t gg = ok[u] ? g : 0;
+      if (staged) {  // find_owner (worklist.py:96-119) over the staged prefix
+        const uint32_t o = owner_search(spre, nh, gg);
+        e[u] = sstart[o] + (gg - (o ? spre[o - 1] : 0));
+        sv[u] = (L)sval[o];
+      } else {
+        const uint32_t o = owner_search(a.hpre, nh, gg);
+        e[u] = a.hstart[o] + (gg - (o ? a.hpre[o - 1] : 0));
+        sv[u] = (L)a.hval[o];
+      }
+    }
+    op.relax(a, e, ok, sv);
+  }
+}
+
+// next frontier from the round's bitmap: ids ascending within each warp's
+// 1024-vertex range, one atomic per warp range, coalesced id / snapshot writes
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_compact(PushArgs a, Op op) {
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  op.begin(ctl->round);
+  const uint32_t nwords = (a.nv + 31) / 32, lane = lane_id();
+  const uint32_t warps = (gridDim.x * kTB) >> 5;
+  uint32_t *q = a.q[0];
+  for (uint32_t w0 = ((blockIdx.x * kTB + threadIdx.x) >> 5) * 32; w0 < nwords; w0 += warps * 32) {
+    const uint32_t wi = w0 + lane;
+    const uint32_t bits = wi < nwords ? op.take(wi) : 0u;
+    const uint32_t cnt = __popc(bits);
+    const uint32_t incl = warp_incl_scan(cnt);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (!total) continue;
+    uint32_t pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&ctl->nsize, total);
+    pos0 = __shfl_sync(kFull, pos0, 0);
+    const uint32_t excl = incl - cnt;
+    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+      const uint32_t slot = k0 + lane;
+      const int o = warp_owner(incl, slot);
+      const uint32_t bo = __shfl_sync(kFull, bits, o);
+      const uint32_t eo = __shfl_sync(kFull, excl, o);
+      if (slot < total) {
+        const uint32_t b = __fns(bo, 0, (int)(slot - eo) + 1);
+        const uint32_t v = (w0 + (uint32_t)o) * 32 + b;
+        q[pos0 + slot] = v;
+        op.emit(pos0 + slot, v);
+      }
+    }
+  }
+}
+
+}  // namespace sg

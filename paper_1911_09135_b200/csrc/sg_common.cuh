@@ -134,11 +134,31 @@ __device__ __forceinline__ T warp_max(T x) {
   return x;
 }
 
-// streaming (read-once) 32-bit load: keep the adjacency out of L1
+// streaming (read-once) loads: keep the adjacency / weights out of L1 and mark
+// them evict-first in L2, so the L2 holds the randomly accessed labels instead
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t *p) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(l2_evict_first()));
   return v;
+}
+__device__ __forceinline__ int64_t ld_stream(const int64_t *p) {
+  long long v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
+               : "=l"(v)
+               : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+// label reads that must not hit a stale L1 line of an earlier round (L2 only)
+__device__ __forceinline__ uint32_t ld_l2(const uint32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_l2(const unsigned long long *p) {
+  return __ldcg(p);
 }
 
 }  // namespace sg

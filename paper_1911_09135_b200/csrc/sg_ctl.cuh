@@ -84,14 +84,18 @@ struct WarpQueue {
   }
 };
 
-// warp-aggregated append of flagged lanes to a global list (rare events)
-__device__ __forceinline__ void warp_append(bool p, uint32_t v, uint32_t *list, uint32_t *count) {
+// warp-aggregated append of flagged lanes to a global list (rare events);
+// returns each flagged lane's slot
+__device__ __forceinline__ uint32_t warp_append(bool p, uint32_t v, uint32_t *list,
+                                                uint32_t *count) {
   uint32_t m = __ballot_sync(kFull, p);
-  if (!m) return;
+  if (!m) return 0;
   uint32_t base = 0;
   if (lane_id() == (uint32_t)(__ffs(m) - 1)) base = atomicAdd(count, (uint32_t)__popc(m));
   base = __shfl_sync(kFull, base, __ffs(m) - 1);
-  if (p) list[base + __popc(m & lanemask_lt())] = v;
+  const uint32_t slot = base + __popc(m & lanemask_lt());
+  if (p) list[slot] = v;
+  return slot;
 }
 
 template <class T>

@@ -44,30 +44,36 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   const View &v = cc ? g.sym() : g.csr;
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
-  const PushArgs a = rb.push_args(v, thr);
+  PushArgs a = rb.push_args(v, thr);
+  a.q[1] = a.q[0];  // one frontier array: k_bm_compact rewrites it after the round
   const bool blocked = p.blocked != 0;
   const int64_t src = p.source;
   Ctl *ctl = rb.ctl.p;
   uint32_t *q0 = rb.q0.p;
+  const int64_t nw = (nv + 31) / 32 + 1;
   auto init_ctl = [=](Launcher &L, cudaStream_t s) {
     L.go("init", k_ctl_init, 1, 1, s, ctl, (int32_t)cc, cc ? (uint32_t)nv : 1u);
     if (!cc) L.go("init", k_set1<uint32_t>, 1, 1, s, q0, (int64_t)0, (uint32_t)src);
   };
+  auto set_round = [&](auto op) {
+    P.round = [=, &rb](RoundCtx &c) {
+      bm_round(c, a, op, blocked);
+      c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
+    };
+  };
 
   if (p.app == SG_APP_BFS) {
-    uint32_t *lab = P.buf<uint32_t>(nv), *vis = P.buf<uint32_t>((nv + 31) / 32 + 1);
-    OpBfs op{lab, vis};
+    uint32_t *lab = P.buf<uint32_t>(nv), *vis = P.buf<uint32_t>(nw), *prev = P.buf<uint32_t>(nw);
     P.init = [=](Launcher &L, cudaStream_t s) {
       init_ctl(L, s);
       fill<uint32_t>(L, lab, nv, kInf32, s);
-      fill<uint32_t>(L, vis, (nv + 31) / 32 + 1, 0u, s);
+      fill<uint32_t>(L, vis, nw, 0u, s);
+      fill<uint32_t>(L, prev, nw, 0u, s);
       L.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
       L.go("init", k_set1<uint32_t>, 1, 1, s, vis, src >> 5, 1u << (src & 31));
+      L.go("init", k_set1<uint32_t>, 1, 1, s, prev, src >> 5, 1u << (src & 31));
     };
-    P.round = [=, &rb](RoundCtx &c) {
-      push_round(c, a, op, blocked);
-      c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
-    };
+    set_round(BmBfs{lab, vis, prev});
     P.finish = [=](Launcher &L, cudaStream_t s) {
       L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
     };
@@ -80,44 +86,41 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
     double bound = (double)g.wmax * (double)std::max<int64_t>(nv - 1, 1);
     use32 = g.w32.p != nullptr && bound < 4294967295.0;
   }
-  // parity pairs lab[2v + h]; both halves start equal
-  auto set_round = [&](auto op) {
-    P.round = [=, &rb](RoundCtx &c) {
-      push_round(c, a, op, blocked);
-      c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
-    };
-  };
+  uint32_t *nb = P.buf<uint32_t>(nw);
   if (use32) {
-    uint32_t *lab = P.buf<uint32_t>(2 * nv);
+    uint32_t *lab = P.buf<uint32_t>(nv), *snap = P.buf<uint32_t>(nv);
     P.init = [=](Launcher &L, cudaStream_t s) {
       init_ctl(L, s);
+      fill<uint32_t>(L, nb, nw, 0u, s);
       if (cc) {
-        L.go("init", k_iota_pairs, grid_n(nv), 256, s, lab, nv);
+        L.go("init", k_iota, grid_n(nv), 256, s, lab, nv);
+        L.go("init", k_iota, grid_n(nv), 256, s, snap, nv);  // dense round 0: snap[i] = i
       } else {
-        fill<uint32_t>(L, lab, 2 * nv, kInf32, s);
-        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, 2 * src, 0u);
-        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, 2 * src + 1, 0u);
+        fill<uint32_t>(L, lab, nv, kInf32, s);
+        L.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
+        L.go("init", k_set1<uint32_t>, 1, 1, s, snap, (int64_t)0, 0u);
       }
     };
-    if (cc) set_round(OpPair<0>{lab, nullptr, nullptr});
-    else if (!weighted) set_round(OpPair<1>{lab, nullptr, nullptr});
-    else set_round(OpPair<2>{lab, g.w32.p, nullptr});
+    if (cc) set_round(BmMin<0>{lab, nullptr, nullptr, snap, nb});
+    else if (!weighted) set_round(BmMin<1>{lab, nullptr, nullptr, snap, nb});
+    else set_round(BmMin<2>{lab, g.w32.p, nullptr, snap, nb});
     P.finish = [=](Launcher &L, cudaStream_t s) {
-      L.go("labels", k_labels_pair_u32, grid_n(nv), 256, s, lab, nv, ctl, labels_d);
+      L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
     };
   } else {
     using U = unsigned long long;
-    U *lab = P.buf<U>(2 * nv);
+    U *lab = P.buf<U>(nv), *snap = P.buf<U>(nv);
     const U inf = 0x7ff0000000000000ull;
     P.init = [=](Launcher &L, cudaStream_t s) {
       init_ctl(L, s);
-      fill<U>(L, lab, 2 * nv, inf, s);
-      L.go("init", k_set1<U>, 1, 1, s, lab, 2 * src, 0ull);
-      L.go("init", k_set1<U>, 1, 1, s, lab, 2 * src + 1, 0ull);
+      fill<uint32_t>(L, nb, nw, 0u, s);
+      fill<U>(L, lab, nv, inf, s);
+      L.go("init", k_set1<U>, 1, 1, s, lab, src, 0ull);
+      L.go("init", k_set1<U>, 1, 1, s, snap, (int64_t)0, 0ull);
     };
-    set_round(OpPair<3>{lab, nullptr, weighted ? g.w64.p : nullptr});
+    set_round(BmMin<3>{lab, nullptr, weighted ? g.w64.p : nullptr, snap, nb});
     P.finish = [=](Launcher &L, cudaStream_t s) {
-      L.go("labels", k_labels_pair_f64, grid_n(nv), 256, s, lab, nv, ctl, labels_d);
+      L.go("labels", k_labels_f64bits, grid_n(nv), 256, s, lab, nv, labels_d);
     };
   }
 }

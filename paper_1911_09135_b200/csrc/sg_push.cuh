@@ -33,7 +33,10 @@ namespace sg {
 
 constexpr int kTB = 256;        // threads per CTA of the traversal kernels
 constexpr int kWarpsTB = kTB / 32;
-constexpr int kU = 4;           // edges per lane per step (memory-level parallelism)
+#ifndef SG_KU
+#define SG_KU 4
+#endif
+constexpr int kU = SG_KU;       // edges per lane per step (memory-level parallelism)
 constexpr uint32_t kLarge = 256;  // TWC CTA-bin cut (threads_per_cta, schedulers.py:159)
 constexpr uint32_t kHugeSmem = 1024;  // huge-vertex prefix/start/label staged in shared memory
 constexpr uint32_t kChunkGrab = 4;    // TWC chunks (32 items each) per dynamic fetch
@@ -48,6 +51,7 @@ struct PushArgs {
   uint32_t *largeq, *hugeq;
   int64_t *hpre, *hstart;
   unsigned long long *hval;
+  unsigned long long *largesv;  // snapshot labels of the CTA-bin queue (Op::kCarry)
   const uint32_t *dying;  // src_mode 1: kcore dying list (count in ctl->ndying)
   int64_t threshold;      // huge threshold; INT64_MAX = twc (no huge bin)
   int src_mode;           // 0 frontier, 1 kcore dying list
@@ -87,7 +91,8 @@ struct OpBfs {
   uint32_t *lab, *vis;
   uint32_t r = 0;
   __device__ __forceinline__ void begin(uint32_t round) { r = round; }
-  __device__ __forceinline__ L src_val(uint32_t) const { return r; }
+  static constexpr bool kCarry = false;
+  __device__ __forceinline__ L src_val(uint64_t, uint32_t) const { return r; }
   __device__ __forceinline__ void sync_src(uint32_t, L) const {}
   __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kU],
                                         const bool (&ok)[kU], const L (&sv)[kU],
@@ -124,7 +129,10 @@ struct OpPair {
   const int64_t *w64;  // KIND 3 (nullptr: unit weights)
   uint32_t ch = 0, nh = 1;  // current (snapshot) / next half
   __device__ __forceinline__ void begin(uint32_t round) { ch = round & 1u, nh = ch ^ 1u; }
-  __device__ __forceinline__ L src_val(uint32_t v) const { return lab[2 * (size_t)v + ch]; }
+  static constexpr bool kCarry = false;
+  __device__ __forceinline__ L src_val(uint64_t, uint32_t v) const {
+    return lab[2 * (size_t)v + ch];
+  }
   // a frontier vertex changed last round: its next half still holds the older value
   __device__ __forceinline__ void sync_src(uint32_t v, L sv) const {
     atomicMin(lab + 2 * (size_t)v + nh, sv);
@@ -132,8 +140,8 @@ struct OpPair {
   __device__ __forceinline__ L prop(int64_t e, L sv) const {
     if (KIND == 0) return sv;
     if (KIND == 1) return sv + 1u;
-    if (KIND == 2) return sv + __ldg(w32 + e);
-    double p = __dadd_rn(__longlong_as_double((long long)sv), w64 ? (double)__ldg(w64 + e) : 1.0);
+    if (KIND == 2) return sv + ld_stream(w32 + e);
+    double p = __dadd_rn(__longlong_as_double((long long)sv), w64 ? (double)ld_stream(w64 + e) : 1.0);
     return (L)__double_as_longlong(p);
   }
   __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kU],
@@ -174,7 +182,8 @@ struct OpMark {
   uint32_t *mark;
   uint32_t stamp = 0;
   __device__ __forceinline__ void begin(uint32_t round) { stamp = round + 1; }
-  __device__ __forceinline__ L src_val(uint32_t) const { return 0; }
+  static constexpr bool kCarry = false;
+  __device__ __forceinline__ L src_val(uint64_t, uint32_t) const { return 0; }
   __device__ __forceinline__ void sync_src(uint32_t, L) const {}
   __device__ __forceinline__ void relax(const PushArgs &a, const int64_t (&e)[kU],
                                         const bool (&ok)[kU], const L (&)[kU],
@@ -229,15 +238,19 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
       v = src.at(i);
       s = a.off[v];
       deg = a.off[v + 1] - s;
-      sv = op.src_val(v);
+      sv = op.src_val(i, v);
       if (sync) op.sync_src(v, sv);
     }
     my_edges += (unsigned long long)deg;
     const bool huge = deg >= a.threshold;
     const bool large = !huge && deg >= (int64_t)kLarge;
     if (large) my_large += (unsigned long long)deg;
-    warp_append(huge, v, a.hugeq, &ctl->nhuge);
-    warp_append(large, v, a.largeq, &ctl->nlarge);
+    const uint32_t hslot = warp_append(huge, v, a.hugeq, &ctl->nhuge);
+    const uint32_t lslot = warp_append(large, v, a.largeq, &ctl->nlarge);
+    if (Op::kCarry) {
+      if (huge) a.hval[hslot] = (unsigned long long)sv;
+      if (large) a.largesv[lslot] = (unsigned long long)sv;
+    }
     const uint32_t gd = (huge || large) ? 0u : (uint32_t)deg;
     const uint32_t incl = warp_incl_scan(gd);
     const uint32_t total = __shfl_sync(kFull, incl, 31);
@@ -307,7 +320,7 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
         const int64_t s = a.off[v];
         d = a.off[v + 1] - s;
         bstart[threadIdx.x] = s;
-        bsv[threadIdx.x] = op.src_val(v);
+        bsv[threadIdx.x] = Op::kCarry ? (L)a.largesv[i] : op.src_val(i, v);
       }
       const long long incl = warp_incl_scan(d);
       if (threadIdx.x < kBatch) bexcl[threadIdx.x + 1] = incl;
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(1024) k_huge_prefix(PushArgs a, Op op) {
       uint32_t v = a.hugeq[i];
       a.hstart[i] = a.off[v];
       d = a.off[v + 1] - a.off[v];
-      a.hval[i] = (unsigned long long)op.src_val(v);
+      if (!Op::kCarry) a.hval[i] = (unsigned long long)op.src_val(i, v);
     }
     long long x = warp_incl_scan(d);
     if (lane_id() == 31) red[threadIdx.x >> 5] = x;

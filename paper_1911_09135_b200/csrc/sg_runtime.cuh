@@ -14,6 +14,7 @@
 #include <unordered_map>
 
 #include "sg_graph.cuh"
+#include "sg_bm.cuh"
 #include "sg_pull.cuh"
 
 namespace sg {
@@ -125,6 +126,16 @@ __global__ void k_iota_pairs(uint32_t *p, int64_t n) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
     reinterpret_cast<uint2 *>(p)[i] = make_uint2((uint32_t)i, (uint32_t)i);
+}
+__global__ void k_labels_f64bits(const unsigned long long *lab, int64_t n, double *out) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = __longlong_as_double((long long)lab[i]);
+}
+__global__ void k_iota(uint32_t *p, int64_t n) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    p[i] = (uint32_t)i;
 }
 // after R rounds the half written last, R & 1, holds every final label
 __global__ void k_labels_pair_u32(const uint32_t *lab, int64_t n, const Ctl *ctl, double *out) {
@@ -372,7 +383,7 @@ struct RunBufs {
   int64_t stats_cap = 0;
   DBuf<uint32_t> q0, q1, largeq, hugeq, dying;
   DBuf<int64_t> hpre, hstart;
-  DBuf<unsigned long long> hval;
+  DBuf<unsigned long long> hval, largesv;
 
   void alloc_common(int64_t nv, int64_t rounds_cap) {
     size_t n = (size_t)std::max<int64_t>(nv, 1);
@@ -381,7 +392,7 @@ struct RunBufs {
     stats_cap = rounds_cap;
     stats.alloc(rounds_cap);
     q0.alloc(n), q1.alloc(n), largeq.alloc(n), hugeq.alloc(n);
-    hpre.alloc(n), hstart.alloc(n), hval.alloc(n);
+    hpre.alloc(n), hstart.alloc(n), hval.alloc(n), largesv.alloc(n);
   }
   PushArgs push_args(const View &v, int64_t thr) {
     PushArgs a{};
@@ -392,6 +403,7 @@ struct RunBufs {
     a.q[0] = q0.p, a.q[1] = q1.p;
     a.largeq = largeq.p, a.hugeq = hugeq.p;
     a.hpre = hpre.p, a.hstart = hstart.p, a.hval = hval.p;
+    a.largesv = largesv.p;
     a.dying = dying.p;
     a.threshold = thr;
     a.src_mode = 0;
@@ -451,6 +463,22 @@ void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
       c.L.go("push_lb", k_push_lb<Op, false>, occupancy_grid(k_push_lb<Op, false>, kTB), kTB, c.s,
              a, op);
   }
+}
+
+// single-device push round with the bitmap next-frontier (sg_bm.cuh)
+template <class Op>
+void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
+  c.L.go("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
+  c.L.go("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
+  if (a.threshold != kNoHuge) {
+    c.L.go("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
+    if (blocked)
+      c.L.go("push_lb", k_bm_lb<Op, true>, occupancy_grid(k_bm_lb<Op, true>, kTB), kTB, c.s, a, op);
+    else
+      c.L.go("push_lb", k_bm_lb<Op, false>, occupancy_grid(k_bm_lb<Op, false>, kTB), kTB, c.s, a,
+             op);
+  }
+  c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
 }
 
 template <class Op>
