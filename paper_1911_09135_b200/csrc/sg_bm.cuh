@@ -29,6 +29,7 @@ namespace sg {
 #define SG_BKV 8
 #endif
 constexpr int kV = SG_BKV;  // edges per lane per step in the bitmap-frontier kernels
+static_assert(kV * 32 <= (int)kLarge, "k_bm_large: a warp step must span <= 2 CTA-bin vertices");
 
 // bfs: frontier vertices of round r carry label r.  vis = visited bitmap
 // (red.or during the round); prev = vis as of the round start, so the next
@@ -213,20 +214,29 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
     }
     __syncthreads();
     const long long total = bexcl[kBatch];
+    // each warp takes 32*kV consecutive slots per step; every CTA-bin vertex
+    // owns >= kLarge >= 32*kV slots, so they span at most two owners: one
+    // warp-uniform bisection (shared-memory broadcast) per step, then a
+    // compare per slot
     for (long long b = 0; b < total; b += kTB * kV) {
+      const long long wbase = b + (long long)(threadIdx.x >> 5) * (32 * kV);
+      uint32_t lo = 0;  // last o with bexcl[o] <= wbase (kBatch == 32)
+#pragma unroll
+      for (uint32_t step = kBatch / 2; step; step >>= 1)
+        lo = bexcl[lo + step] <= wbase ? lo + step : lo;
+      const long long x0 = bexcl[lo], x1 = bexcl[lo + 1];
+      const int64_t s0 = bstart[lo], s1 = lo + 1 < kBatch ? bstart[lo + 1] : 0;
+      const L v0 = bsv[lo], v1 = lo + 1 < kBatch ? bsv[lo + 1] : L(0);
       int64_t e[kV];
       bool ok[kV];
       L svs[kV];
 #pragma unroll
       for (int u = 0; u < kV; ++u) {
-        const long long slot = b + u * kTB + threadIdx.x;
+        const long long slot = wbase + u * 32 + (threadIdx.x & 31u);
         ok[u] = slot < total;
-        uint32_t lo = 0;  // last o with bexcl[o] <= slot (kBatch == 32)
-#pragma unroll
-        for (uint32_t step = kBatch / 2; step; step >>= 1)
-          lo = bexcl[lo + step] <= slot ? lo + step : lo;
-        e[u] = bstart[lo] + (slot - bexcl[lo]);
-        svs[u] = bsv[lo];
+        const bool second = slot >= x1;
+        e[u] = second ? s1 + (slot - x1) : s0 + (slot - x0);
+        svs[u] = second ? v1 : v0;
       }
       op.relax(a, e, ok, svs);
     }
