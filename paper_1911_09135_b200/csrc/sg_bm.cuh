@@ -257,15 +257,50 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
   if (!nh) return;
   const int64_t E = (int64_t)ctl->huge_edges;
   op.begin(ctl->round);
+  const int64_t T = (int64_t)gridDim.x * kTB;
+  const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
+  const int64_t passes = (E + T - 1) / T;
+  if (!BLOCKED && a.threshold >= 32 * kV) {
+    // cyclic at warp granularity: warp w takes the 32*kV consecutive edge ids
+    // of chunks w, w + W, w + 2W, ... (consecutive lanes still read
+    // consecutive adjacency entries, the point of the paper's cyclic
+    // distribution).  Every huge vertex owns >= threshold >= 32*kV edges, so
+    // a chunk spans at most two of them: find_owner (worklist.py:96-119) is
+    // one warp-uniform bisection per chunk (broadcast loads), starting at the
+    // previous chunk's owner, and no shared-memory staging is needed for any
+    // number of huge vertices.
+    constexpr int64_t CH = 32 * kV;
+    const int64_t nwarps = T >> 5, nch = (E + CH - 1) / CH;
+    const uint32_t lane = lane_id();
+    uint32_t olo = 0;
+    for (int64_t c = tid >> 5; c < nch; c += nwarps) {
+      const int64_t g0 = c * CH;
+      const uint32_t o = owner_search_from(a.hpre, olo, nh, g0);
+      olo = o;
+      const int64_t x0 = o ? a.hpre[o - 1] : 0, x1 = a.hpre[o];
+      const int64_t s0 = a.hstart[o], s1 = o + 1 < nh ? a.hstart[o + 1] : 0;
+      const L v0 = (L)a.hval[o], v1 = o + 1 < nh ? (L)a.hval[o + 1] : L(0);
+      int64_t e[kV];
+      bool ok[kV];
+      L sv[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int64_t g = g0 + u * 32 + lane;
+        ok[u] = g < E;
+        const bool second = g >= x1;
+        e[u] = second ? s1 + (g - x1) : s0 + (g - x0);
+        sv[u] = second ? v1 : v0;
+      }
+      op.relax(a, e, ok, sv);
+    }
+    return;
+  }
   const bool staged = nh <= kHugeSmem;
   if (staged) {
     for (uint32_t i = threadIdx.x; i < nh; i += kTB)
       spre[i] = a.hpre[i], sstart[i] = a.hstart[i], sval[i] = a.hval[i];
     __syncthreads();
   }
-  const int64_t T = (int64_t)gridDim.x * kTB;
-  const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
-  const int64_t passes = (E + T - 1) / T;
   for (int64_t p0 = 0; p0 < passes; p0 += kV) {
     int64_t e[kV];
     bool ok[kV];

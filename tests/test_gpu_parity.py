@@ -204,9 +204,9 @@ def test_sssp_float64_path_big_weights(sg, O):
         [[r.frontier_size, r.active_edges] for r in log]
 
 
-@pytest.mark.parametrize("scale", [18, 20])
+@pytest.mark.parametrize("scale,thr", [(18, None), (20, None), (18, 256), (18, 300)])
 @pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "kcore", "pr"])
-def test_larger_scale_vs_c_oracle(sg, scale, app):
+def test_larger_scale_vs_c_oracle(sg, scale, thr, app):
     from oracle import oracle_c as C
     g = sg.generate_rmat(scale, 16, 1)
     gw = sg.attach_random_weights(g, 2) if app == "sssp" else g
@@ -214,7 +214,7 @@ def test_larger_scale_vs_c_oracle(sg, scale, app):
     w = gw.edge_weights if app == "sssp" else None
     lab, log, st = C.run(app, *C.prepare(off, tgt, w, app), threads=8)
     assert st == 0
-    res = sg.run_app(gw, app)
+    res = sg.run_app(gw, app, sg.Scheduler("alb", threshold=thr))
     got = [[r.frontier_size, r.active_edges()] for r in res.records]
     if app == "pr":
         # tolerance-mode pr: tree-ordered sums may flip the eps_stop test by
