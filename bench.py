@@ -65,7 +65,12 @@ def parse():
     ap.add_argument("--threshold", type=int, default=DEFAULT_THRESHOLD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--extra", default="", help="comma list of extra apps to report")
+    ap.add_argument("--extra", default="bfs,cc,pr,kcore",
+                    help="comma list of extra apps reported on the same rmat graph ('' = none)")
+    ap.add_argument("--no-ablation", action="store_true",
+                    help="skip the ALB vs TWC-only (classic / batched CTA bin) ablation")
+    ap.add_argument("--cta-bin", default="batched", choices=["batched", "classic"],
+                    help="TWC CTA bin: edge-balanced batches (default) or one vertex per CTA")
     return ap.parse_args()
 
 
@@ -154,7 +159,24 @@ def algorithmic_bytes(app, log):
                 "pull_large": int((eb * ml).sum()), "pull_lb": int((eb * mh).sum())}
     return {"push_twc": int((eb * (m - mh - ml) + VERTEX_BYTES * n).sum()),
             "push_large": int((eb * ml).sum()), "push_lb": int((eb * mh).sum()),
-            "advance": int((UPDATE_BYTES * u).sum())}
+            "compact": int((UPDATE_BYTES * u).sum())}
+
+
+def kernel_edges(log):
+    """Edges (operator applications) per traversal kernel from the round log."""
+    m = log["active_edges"].astype(np.int64)
+    mh = log["huge_edges"].astype(np.int64)
+    ml = log["large_edges"].astype(np.int64)
+    return {"twc": int((m - mh - ml).sum()), "large": int(ml.sum()), "lb": int(mh.sum())}
+
+
+# profiled-run kernel names -> the CUDA kernels ncu lists
+NCU_NAME = {"push_twc": "k_bm_twc", "push_large": "k_bm_large", "push_lb": "k_bm_lb",
+            "compact": "k_bm_compact", "pull_twc": "k_pull_twc", "pull_large": "k_pull_large",
+            "pull_lb": "k_pull_lb"}
+# random 4-byte gathers per second the chip sustains (scripts/micro/gather.cu on
+# B200: 272-275 G/s, one L1TEX wavefront per scattered lane)
+GATHER_CEILING = 272e9
 
 
 def total_algorithmic_bytes(app, log, nv):
@@ -177,9 +199,30 @@ def ncu_traffic(kernel):
 def make_graph_device(sg, app, scale, uniform):
     probs = (0.25,) * 4 if uniform else SKEWED
     g = sg.generate_rmat(scale, 16, 1, probs)
-    if app == "sssp":
-        g = sg.attach_random_weights(g, 2)
-    return g
+    return (sg.attach_random_weights(g, 2) if app == "sssp" else g), g
+
+
+def run_params(sg, app, sched_kind, threshold, nv, classic=False):
+    sched = sg.Scheduler(sched_kind, threshold=threshold if sched_kind == "alb" else None)
+    p = sg.engine._device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), 1, 10 * nv + 256)
+    if classic:
+        p.flags |= 4  # SG_FLAG_TWC_CLASSIC
+    return sched, p
+
+
+def device_steps(torch, dev, params, steps, warmup, flush):
+    """W untimed + K timed BSP runs; per-run CUDA-event time of sg_run, L2 flushed before each."""
+    for _ in range(max(1, warmup)):
+        labels, log, ms = dev.run(params)
+    out = []
+    for i in range(steps):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        labels, log, ms = dev.run(params)
+        out.append(ms)
+    edges = int(log["active_edges"].sum())
+    return {"gteps": edges * len(out) / (sum(out) / 1e3) / 1e9,
+            "ms_per_step": sum(out) / len(out), "rounds": len(log), "edges_processed": edges}
 
 
 def cpu_oracle_run(app, off, tgt, w, threads):
@@ -244,12 +287,10 @@ def main():
     import paper_1911_09135_b200 as sg
     from paper_1911_09135_b200 import native
 
-    g = make_graph_device(sg, a.app, a.scale, a.uniform)
+    g, g_base = make_graph_device(sg, a.app, a.scale, a.uniform)
     dev = g.device()
     nv, ne, _ = dev.info()
-    sched = sg.Scheduler(a.sched, threshold=a.threshold if a.sched == "alb" else None)
-    params = sg.engine._device_params(sg.apps.make_app(a.app), sched, sg.KernelConfig(), 1,
-                                      10 * nv + 256)
+    sched, params = run_params(sg, a.app, a.sched, a.threshold, nv, a.cta_bin == "classic")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     nccl_id = None
     if world > 1:  # edge cut: one partition per rank, NCCL label exchange
@@ -324,13 +365,21 @@ def main():
     if dom:
         n_l, ms_l = kernels[dom]
         achieved = ab[dom] / (ms_l / 1e3) / 1e9
-        traffic = ncu_traffic(dom)
-        roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
+        traffic = ncu_traffic(NCU_NAME.get(dom, dom))
+        ke = kernel_edges(plog).get(dom.split("_")[-1], 0)
+        roofline = {"bound": "hbm", "kernel": NCU_NAME.get(dom, dom), "achieved": achieved,
+                    "peak": peak,
                     "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
                     "traffic": traffic, "algorithmic_bytes_per_launch": ab[dom] / max(n_l, 1),
                     "avg_launch_ms": ms_l / max(n_l, 1), "launches": n_l,
                     "share_of_step": ms_l / sum(v[1] for v in kernels.values()),
-                    "loop_bytes_per_s_GBps": sum(ab.values()) / (statistics.median(step_ms) / 1e3) / 1e9}
+                    "loop_bytes_per_s_GBps": sum(ab.values()) / (statistics.median(step_ms) / 1e3) / 1e9,
+                    # the bound that actually binds an irregular gather kernel
+                    "gather_ceiling": {"unit": "G random label accesses/s",
+                                       "peak": GATHER_CEILING / 1e9,
+                                       "achieved": ke / (ms_l / 1e3) / 1e9,
+                                       "frac": ke / (ms_l / 1e3) / GATHER_CEILING,
+                                       "source": "scripts/micro/gather.cu (B200, measured)"}}
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
@@ -343,6 +392,30 @@ def main():
                          f"oracle/sg_oracle.c single thread ({dt:.1f} s)",
                "labels_match": bool(np.array_equal(lab_c, labels)) if a.app != "pr" else
                float(np.max(np.abs(lab_c - labels)))}
+
+    # ------------- other apps + ALB vs TWC-only ablation (rank 0, N=1) -------------
+    extra, ablation = {}, {}
+    if rank == 0 and world == 1:
+        steps_x = max(2, min(a.steps, 3))
+        apps = [x for x in a.extra.split(",") if x]
+        for app in apps:
+            d = g.device() if app == "sssp" else g_base.device()
+            extra[app] = device_steps(torch, d, run_params(sg, app, "alb", a.threshold, nv)[1],
+                                      steps_x, 1, flush)
+        if not a.no_ablation:
+            for app in sorted(set([a.app] + apps)):
+                d = g.device() if app == "sssp" else g_base.device()
+                alb = extra[app]["gteps"] if app in extra else value
+                tw_b = device_steps(torch, d, run_params(sg, app, "twc", None, nv)[1], steps_x, 1,
+                                    flush)["gteps"]
+                tw_c = device_steps(torch, d, run_params(sg, app, "twc", None, nv, True)[1],
+                                    steps_x, 1, flush)["gteps"]
+                alb_c = device_steps(torch, d, run_params(sg, app, "alb", a.threshold, nv, True)[1],
+                                     steps_x, 1, flush)["gteps"]
+                ablation[app] = {"alb_gteps": alb, "twc_gteps": tw_b,
+                                 "alb_over_twc": alb / tw_b,
+                                 "classic_cta_bin": {"alb_gteps": alb_c, "twc_gteps": tw_c,
+                                                     "alb_over_twc": alb_c / tw_c}}
 
     if rank != 0:
         return
@@ -371,6 +444,9 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "kernel_ms": {k: {"launches": v[0], "ms": v[1]} for k, v in kernels.items()},
+        "apps": {k: {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                 for k, v in extra.items()},
+        "ablation_alb_vs_twc": ablation,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

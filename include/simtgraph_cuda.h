@@ -72,6 +72,9 @@ typedef struct sg_params {
 #define SG_FLAG_PROFILE 2 /* host-driven rounds with CUDA events around every kernel
                              (per-kernel times via sg_run_profiled); default is one
                              CUDA-graph launch whose WHILE node runs all rounds */
+#define SG_FLAG_TWC_CLASSIC 4 /* TWC CTA bin = one vertex per CTA (the reference's
+                                 twc_kernel mapping, _kernels_py.py:140-146) instead of
+                                 edge-balanced batches; for the TWC-only ablation */
 
 typedef struct sg_round { /* one BSP round (engine.py:116-163) */
   int64_t frontier_size;  /* RoundRecord.frontier_size */

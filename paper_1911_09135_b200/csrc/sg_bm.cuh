@@ -244,6 +244,44 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
   }
 }
 
+// Classic TWC CTA bin (Merrill; the reference's twc_kernel maps each large
+// vertex to one CTA, _kernels_py.py:140-146): a CTA takes one vertex at a time
+// and strides over its edges.  Used for the TWC-only ablation
+// (SG_FLAG_TWC_CLASSIC); one huge vertex pins one CTA for its whole degree.
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
+  using L = typename Op::L;
+  __shared__ uint32_t item;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  for (;;) {
+    if (threadIdx.x == 0) item = atomicAdd(&ctl->large_head, 1u);
+    __syncthreads();
+    const uint32_t idx = item;
+    __syncthreads();
+    if (idx >= n) break;
+    const uint32_t v = a.largeq[idx];
+    const int64_t s = a.off[v], deg = a.off[v + 1] - s;
+    const L sv = (L)a.largesv[idx];
+    for (int64_t b = 0; b < deg; b += kTB * kV) {
+      int64_t e[kV];
+      bool ok[kV];
+      L svs[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int64_t slot = b + u * kTB + threadIdx.x;
+        ok[u] = slot < deg;
+        e[u] = s + slot;
+        svs[u] = sv;
+      }
+      op.relax(a, e, ok, svs);
+    }
+  }
+}
+
 // ALB huge-vertex kernel (Algorithm 2): every thread of every CTA walks the
 // huge edges cyclically (g = p*T + tid) or blocked (g = tid*ceil(e/T) + p)
 template <class Op, bool BLOCKED>

@@ -40,6 +40,7 @@ namespace {
 
 void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d,
                    int64_t thr, int64_t max_rounds) {
+  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const bool cc = p.app == SG_APP_CC;
   const View &v = cc ? g.sym() : g.csr;
   const int64_t nv = v.nv;
@@ -57,7 +58,7 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   };
   auto set_round = [&](auto op) {
     P.round = [=, &rb](RoundCtx &c) {
-      bm_round(c, a, op, blocked);
+      bm_round(c, a, op, blocked, classic);
       c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
     };
   };
@@ -127,6 +128,7 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
 
 void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d, int64_t thr,
              int64_t max_rounds) {
+  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.csc();
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
@@ -155,7 +157,10 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
     L.go("init", k_pr_init, grid_n(nv), 256, s, csr_off, nv, omd, inv, labels_d, aux0);
     fill<double>(L, hacc, nv, 0.0, s);
     fill<unsigned long long>(L, gmax, 1, 0ull, s);
-    if (vne) L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax);
+    if (vne) {
+      L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, voff, vcol, nv, inv, gmax);
+      L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax);
+    }
     L.go("init", k_static_bins, grid_n(nv), 256, s, voff, (uint32_t)nv, thr, largeq, hugeq, ctl,
          cuts);
     if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
@@ -166,7 +171,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   const int64_t ne = v.ne;
   const double tol = p.tol;
   P.round = [=, &rb](RoundCtx &c) {
-    pull_round(c, a, op, blocked, hacc);
+    pull_round(c, a, op, blocked, hacc, classic);
     PrStop stop{gmax, d, tol, ne, std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds, c.cond,
                 c.use_cond, parts_nonempty};
     c.L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, c.s, a, op, hacc, stop);
@@ -176,6 +181,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
 
 void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d,
                 int64_t thr, int64_t max_rounds) {
+  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.sym();  // count rows: CSC(sym) and CSR(sym) rows hold the same multiset
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
@@ -203,7 +209,7 @@ void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *l
   const OpMark mop{alive, mark};
   const bool blocked = p.blocked != 0;
   P.round = [=, &rb](RoundCtx &c) {
-    pull_round(c, a, op, blocked, hcnt);
+    pull_round(c, a, op, blocked, hcnt, classic);
     if (thr != kNoHuge)
       c.L.go("kcore_huge", k_pull_finish<KcOp, false>, 1, 1024, c.s, a, op, hcnt, PrStop{});
     c.L.go("kcore_kill", k_kcore_kill, grid_n(nv), 256, c.s, a, alive);

@@ -11,9 +11,13 @@
 // Only huge rows are split across CTAs by the LB kernel; their partial sums
 // are pre-reduced per warp segment and combined with one atomicAdd per segment.
 #pragma once
-#include "sg_push.cuh"
+#include "sg_bm.cuh"
 
 namespace sg {
+
+#ifndef SG_PR_UNROLL
+#define SG_PR_UNROLL 4
+#endif
 
 struct PullArgs {
   const int64_t *off;
@@ -34,6 +38,8 @@ struct PullArgs {
 // pr: acc = sum aux[u]; new = (1-d) + d*acc (two roundings, as numpy); aux' = new*inv
 struct PrOp {
   using A = double;
+  static constexpr bool kWarpMedium = false;  // medium rows join the segmented warp gather
+  static constexpr int kUnroll = SG_PR_UNROLL;
   const double *aux0, *aux1;
   double *next0, *next1;
   double *rank;
@@ -64,6 +70,8 @@ struct PrOp {
 // kcore: count = sum alive[u] with multiplicity (integers: any order is exact)
 struct KcOp {
   using A = uint32_t;
+  static constexpr bool kWarpMedium = true;  // TWC warp bin: one medium row per warp step
+  static constexpr int kUnroll = 4;
   const uint8_t *alive;
   uint32_t k;
   double dmax = 0.0;            // unused
@@ -90,9 +98,22 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   const uint32_t *list = (round & 1) ? a.q[1] : a.q[0];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   unsigned long long my_edges = 0, my_large = 0;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsTB;
-  for (uint64_t c = (uint64_t)blockIdx.x * kWarpsTB + warp; c * 32 < n; c += nwarps) {
-    uint64_t i = c * 32 + lane;
+  // dynamic fetch: a warp grabs kChunkGrab chunks of 32 rows at a time (the
+  // dense pr rows are degree-skewed, a static split leaves a long tail)
+  const uint32_t nchunks = (n + 31) / 32;
+  uint32_t c = 0, c_end = 0;
+  (void)warp;
+  for (;;) {
+    if (c == c_end) {
+      uint32_t g = 0;
+      if (lane == 0) g = atomicAdd(&ctl->chunk_head, 1u);
+      g = __shfl_sync(kFull, g, 0);
+      c = g * kChunkGrab;
+      if (c >= nchunks) break;
+      c_end = min(c + kChunkGrab, nchunks);
+    }
+    const uint64_t i = (uint64_t)c * 32 + lane;
+    ++c;
     uint32_t v = 0;
     int64_t s = 0, deg = 0;
     const bool valid = i < n;
@@ -116,18 +137,23 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
         if (lane == 0 && lb) atomicOr(&ctl->part_lb_mask, lb);
       }
     }
+    // small rows (deg < 32): warp gather over the chunk's rows with a
+    // segmented reduction; medium rows (32 <= deg < kLarge): the whole warp
+    // takes one row at a time (TWC's warp bin, schedulers.py:157-159)
     const bool mine = valid && !huge && !large;
-    const uint32_t gd = mine ? (uint32_t)deg : 0u;
+    const bool small = mine && (deg < 32 || !Op::kWarpMedium);
+    const uint32_t gd = small ? (uint32_t)deg : 0u;
     const uint32_t incl = warp_incl_scan(gd);
     const uint32_t total = __shfl_sync(kFull, incl, 31);
     const uint32_t excl = incl - gd;
     typename Op::A acc = 0;
-    for (uint32_t base = 0; base < total; base += 32 * kU) {
-      int o[kU];
-      uint32_t src[kU];
-      typename Op::A x[kU];
+    constexpr int KP = Op::kUnroll;
+    for (uint32_t base = 0; base < total; base += 32 * KP) {
+      int o[KP];
+      uint32_t src[KP];
+      typename Op::A x[KP];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {  // kU adjacency loads in flight
+      for (int u = 0; u < KP; ++u) {  // KP adjacency loads in flight
         const uint32_t slot = base + u * 32 + lane;
         o[u] = warp_owner(incl, slot);
         const int64_t so = shfl64(s, o[u]);
@@ -135,10 +161,10 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
         src[u] = slot < total ? ld_stream(a.col + so + (slot - eo)) : 0xffffffffu;
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u)  // then kU value gathers in flight
+      for (int u = 0; u < KP; ++u)  // then KP value gathers in flight
         x[u] = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int u = 0; u < KP; ++u) {
         const uint32_t cb = base + u * 32;
         // segmented inclusive scan (owners are non-decreasing along the lanes)
 #pragma unroll
@@ -153,6 +179,26 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
         typename Op::A seg = __shfl_sync(kFull, x[u], (int)((hi - 1 - cb) & 31u));
         if (lo < hi) acc += seg;
       }
+    }
+    uint32_t mm = __ballot_sync(kFull, mine && !small);
+    while (mm) {
+      const int l = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int64_t ms = shfl64(s, l);
+      const uint32_t md = (uint32_t)__shfl_sync(kFull, (uint32_t)deg, l);
+      typename Op::A x = 0;
+      for (uint32_t b = 0; b < md; b += 32 * kV) {
+        uint32_t src[kV];
+#pragma unroll
+        for (int u = 0; u < kV; ++u) {
+          const uint32_t j = b + u * 32 + lane;
+          src[u] = j < md ? ld_stream(a.col + ms + j) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < kV; ++u) x += src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+      }
+      x = __shfl_sync(kFull, warp_sum(x), l);  // lane l's butterfly: a fixed order
+      if (lane == (uint32_t)l) acc = x;
     }
     bool die = false;
     if (mine) die = op.finish(v, acc);
@@ -179,10 +225,119 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   }
 }
 
-// TWC CTA bin: one CTA per row (dynamic fetch), deterministic tree reduction
+// TWC CTA bin: edge-balanced batches of kBatch rows (degree-mixed, dynamic
+// fetch).  Each warp takes 32*kV consecutive slots per step; rows own >= kLarge
+// >= 32*kV slots, so a step spans <= 2 rows.  A warp carries one running sum
+// for its current row and parks it in part[warp][row] when the row changes
+// (each warp meets a row in one contiguous stretch), and the batch's rows are
+// folded as part[0][r] + ... + part[7][r]: a fixed order, deterministic.
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
-  __shared__ typename Op::A red[32];
+  using A = typename Op::A;
+  __shared__ int64_t bstart[kBatch];
+  __shared__ long long bexcl[kBatch + 1];
+  __shared__ uint32_t brow[kBatch];
+  __shared__ A part[kWarpsTB][kBatch];
+  __shared__ uint32_t bhead;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t nb = (n + kBatch - 1) / kBatch;
+  for (;;) {
+    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    for (uint32_t i = threadIdx.x; i < kWarpsTB * kBatch; i += kTB) part[i / kBatch][i % kBatch] = A(0);
+    __syncthreads();
+    const uint32_t bidx = bhead;
+    if (bidx >= nb) break;
+    if (warp == 0) {
+      const uint32_t i = bidx + lane * nb;  // degree-mixed batch
+      long long d = 0;
+      uint32_t v = 0;
+      if (lane < kBatch && i < n) {
+        v = a.largeq[i];
+        const int64_t s0 = a.off[v];
+        d = a.off[v + 1] - s0;
+        bstart[lane] = s0;
+      }
+      if (lane < kBatch) brow[lane] = v;
+      const long long incl = warp_incl_scan(d);
+      if (lane < kBatch) bexcl[lane + 1] = incl;
+      if (lane == 0) bexcl[0] = 0;
+    }
+    __syncthreads();
+    const long long total = bexcl[kBatch];
+    int cur_o = -1;
+    A cur = 0;
+    for (long long b = 0; b < total; b += kTB * kV) {
+      const long long wbase = b + (long long)warp * (32 * kV);
+      if (wbase >= total) continue;
+      uint32_t lo = 0;  // last o with bexcl[o] <= wbase
+#pragma unroll
+      for (uint32_t step = kBatch / 2; step; step >>= 1)
+        lo = bexcl[lo + step] <= wbase ? lo + step : lo;
+      const long long x0 = bexcl[lo], x1 = bexcl[lo + 1];
+      const int64_t s0 = bstart[lo], s1 = lo + 1 < kBatch ? bstart[lo + 1] : 0;
+      uint32_t src[kV];
+      bool sec[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const long long slot = wbase + u * 32 + lane;
+        sec[u] = slot >= x1;
+        src[u] = slot < total ? ld_stream(a.col + (sec[u] ? s1 + (slot - x1) : s0 + (slot - x0)))
+                              : 0xffffffffu;
+      }
+      A xa = 0, xb = 0;
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const A y = src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
+        if (sec[u]) xb += y;
+        else xa += y;
+      }
+      xa = __shfl_sync(kFull, warp_sum(xa), 0);  // lane 0's butterfly: fixed order
+      xb = __shfl_sync(kFull, warp_sum(xb), 0);
+      if ((int)lo != cur_o) {
+        if (cur_o >= 0 && lane == 0) part[warp][cur_o] = cur;
+        cur_o = (int)lo;
+        cur = 0;
+      }
+      cur += xa;
+      if (x1 < wbase + 32 * kV && x1 < total) {  // the step crossed into row lo + 1
+        if (lane == 0) part[warp][cur_o] = cur;
+        cur_o = (int)lo + 1;
+        cur = xb;
+      }
+    }
+    if (cur_o >= 0 && lane == 0) part[warp][cur_o] = cur;
+    __syncthreads();
+    if (warp == 0) {
+      A acc = 0;
+#pragma unroll
+      for (int w = 0; w < kWarpsTB; ++w) acc += part[w][lane];
+      const bool row = lane < kBatch && bidx + lane * nb < n;
+      const bool die = row && op.finish(brow[lane], acc);
+      warp_append(die, brow[lane], a.dying, &ctl->ndying);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    if (sizeof(A) == 8) {
+      const double m = warp_max(op.dmax);
+      if (lane == 0 && m > 0) atomic_max_dbits(&ctl->delta_bits, m);
+    }
+    const unsigned long long bc = warp_sum(op.bcast);
+    if (lane == 0 && bc) atomicAdd(&ctl->comm_bcast, bc);
+  }
+}
+
+// Classic TWC CTA bin for the TWC-only ablation (SG_FLAG_TWC_CLASSIC): one
+// CTA per row (dynamic fetch), block tree reduction
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_pull_large_classic(PullArgs a, Op op) {
+  using A = typename Op::A;
+  __shared__ A red[32];
   __shared__ uint32_t item;
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
@@ -197,19 +352,18 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
     if (idx >= n) break;
     const uint32_t v = a.largeq[idx];
     const int64_t s = a.off[v], e = a.off[v + 1];
-    typename Op::A x = 0;
-    for (int64_t b = s + threadIdx.x; b < e; b += kTB * kU) {
-      uint32_t src[kU];
+    A x = 0;
+    for (int64_t b = s + threadIdx.x; b < e; b += kTB * kV) {
+      uint32_t src[kV];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) src[u] = b + u * kTB < e ? ld_stream(a.col + b + u * kTB) : 0xffffffffu;
+      for (int u = 0; u < kV; ++u) src[u] = b + u * kTB < e ? ld_stream(a.col + b + u * kTB) : 0xffffffffu;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) x += src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+      for (int u = 0; u < kV; ++u) x += src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
     }
     x = block_sum(x, red);
     if (threadIdx.x == 0 && op.finish(v, x)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
   }
-  if (sizeof(typename Op::A) == 8 && threadIdx.x == 0 && op.dmax > 0)
-    atomic_max_dbits(&ctl->delta_bits, op.dmax);
+  if (sizeof(A) == 8 && threadIdx.x == 0 && op.dmax > 0) atomic_max_dbits(&ctl->delta_bits, op.dmax);
   if (threadIdx.x == 0 && op.bcast) atomicAdd(&ctl->comm_bcast, op.bcast);
 }
 
@@ -264,6 +418,42 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
+  if (!BLOCKED && a.threshold >= 32 * kV) {
+    // warp-granular cyclic chunks of 32*kV edge ids, spanning <= 2 huge rows:
+    // one warp-uniform find_owner per chunk, two warp sums, <= 2 atomics
+    constexpr int64_t CH = 32 * kV;
+    const int64_t nwarps = T >> 5, nch = (E + CH - 1) / CH;
+    uint32_t olo = 0;
+    for (int64_t c = tid >> 5; c < nch; c += nwarps) {
+      const int64_t g0 = c * CH;
+      const uint32_t o = owner_search_from(a.hpre, olo, nh, g0);
+      olo = o;
+      const int64_t x0 = o ? a.hpre[o - 1] : 0, x1 = a.hpre[o];
+      const int64_t s0 = a.hstart[o], s1 = o + 1 < nh ? a.hstart[o + 1] : 0;
+      uint32_t src[kV];
+      bool sec[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int64_t g = g0 + u * 32 + lane;
+        sec[u] = g >= x1;
+        src[u] = g < E ? ld_stream(a.col + (sec[u] ? s1 + (g - x1) : s0 + (g - x0))) : 0xffffffffu;
+      }
+      typename Op::A xa = 0, xb = 0;
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const typename Op::A y = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+        if (sec[u]) xb += y;
+        else xa += y;
+      }
+      xa = warp_sum(xa);
+      xb = warp_sum(xb);
+      if (lane == 0) {
+        atomicAdd(hacc + o, xa);
+        if (x1 < g0 + CH && x1 < E) atomicAdd(hacc + o + 1, xb);
+      }
+    }
+    return;
+  }
   for (int64_t p0 = 0; p0 < passes; p0 += kU) {
     int o[kU];
     uint32_t src[kU];
@@ -354,6 +544,7 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
     ctl->comm_bcast = 0;
     ctl->delta_bits = 0;
     ctl->large_head = 0;
+    ctl->chunk_head = 0;
     ctl->round = round + 1;
     if (delta <= eps_stop) ctl->done = 1;  // apps.py:183-185
     else if ((int64_t)round + 1 >= stop.limit)

@@ -172,15 +172,41 @@ __global__ void k_pr_init(const int64_t *off, int64_t n, double omd, double *inv
   }
 }
 // gain[v] = sum_{u->v} inv[u] in CSC (== CSR edge) order, exactly as
-// np.bincount accumulates it (apps.py:166-168): a warp loads 32 terms, every
-// lane folds them sequentially through shuffles; max over v by atomicMax.
+// np.bincount accumulates it (apps.py:166-168); max over v by atomicMax.
+// Rows up to kGainThread edges: one thread folds its row left to right (loads
+// issued 8 ahead); longer rows: a warp loads 32 terms and every lane folds
+// them in order through shuffles.
+constexpr int64_t kGainThread = 64;
+__global__ void k_pr_gain_rows(const int64_t *off, const uint32_t *col, int64_t n,
+                               const double *inv, unsigned long long *maxbits) {
+  double best = 0.0;
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += st) {
+    const int64_t b = off[v], e = off[v + 1];
+    if (e - b > kGainThread) continue;
+    double acc = 0.0;
+    for (int64_t j = b; j < e; j += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = j + u < e ? inv[col[j + u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < e) acc = __dadd_rn(acc, x[u]);
+    }
+    best = acc > best ? acc : best;
+  }
+  best = warp_max(best);
+  if (lane_id() == 0 && best > 0)
+    atomicMax(maxbits, (unsigned long long)__double_as_longlong(best));
+}
 __global__ void k_pr_gain_max(const int64_t *off, const uint32_t *col, int64_t n,
                               const double *inv, unsigned long long *maxbits) {
   int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double best = 0.0;
   for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-    double acc = 0.0;
     const int64_t e = off[v + 1];
+    if (e - off[v] <= kGainThread) continue;
+    double acc = 0.0;
     for (int64_t b = off[v]; b < e; b += 32) {
       int64_t j = b + lane_id();
       double x = j < e ? inv[col[j]] : 0.0;
@@ -467,9 +493,13 @@ void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
 
 // single-device push round with the bitmap next-frontier (sg_bm.cuh)
 template <class Op>
-void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
+void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool classic = false) {
   c.L.go("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
-  c.L.go("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
+  if (classic)
+    c.L.go("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
+           c.s, a, op);
+  else
+    c.L.go("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
   if (a.threshold != kNoHuge) {
     c.L.go("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
     if (blocked)
@@ -482,9 +512,14 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
 }
 
 template <class Op>
-void pull_round(RoundCtx &c, const PullArgs &a, const Op &op, bool blocked, typename Op::A *hacc) {
+void pull_round(RoundCtx &c, const PullArgs &a, const Op &op, bool blocked, typename Op::A *hacc,
+                bool classic = false) {
   c.L.go("pull_twc", k_pull_twc<Op>, occupancy_grid(k_pull_twc<Op>, kTB), kTB, c.s, a, op);
-  c.L.go("pull_large", k_pull_large<Op>, occupancy_grid(k_pull_large<Op>, kTB), kTB, c.s, a, op);
+  if (classic)
+    c.L.go("pull_large", k_pull_large_classic<Op>, occupancy_grid(k_pull_large_classic<Op>, kTB),
+           kTB, c.s, a, op);
+  else
+    c.L.go("pull_large", k_pull_large<Op>, occupancy_grid(k_pull_large<Op>, kTB), kTB, c.s, a, op);
   if (a.threshold != kNoHuge) {
     if (a.dynamic_bins) c.L.go("huge_prefix", k_pull_prefix, 1, 1024, c.s, a);
     if (blocked)
