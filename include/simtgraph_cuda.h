@@ -133,11 +133,19 @@ int sg_run_profiled(sg_graph *g, const sg_params *p, double *labels_out, sg_roun
 /* --- multi-GPU edge cut (engine.py:64-113): one partition per rank over NCCL.
  * sg_nccl_unique_id on rank 0, broadcast the 128 bytes out of band (e.g.
  * torch.distributed), then every rank calls sg_dist_run on the same graph.
- * bfs / sssp / cc; labels_out receives the merged labels on every rank. */
+ * All apps: push apps exchange labels by all-reduce(min); pr broadcasts each
+ * rank's aux / rank rows; kcore all-reduces alive flags (min) and neighbour
+ * marks (max).  labels_out receives the merged labels on every rank. */
 int sg_nccl_unique_id(uint8_t id_out[128]);
 int sg_dist_run(sg_graph *g, const sg_params *p, const uint8_t nccl_id[128], int32_t rank,
                 int32_t world, double *labels_out, sg_round *rounds_out, int64_t rounds_cap,
                 int64_t *nrounds, double *ms_out);
+/* The same per-rank code path with `world` ranks as host threads sharing this
+ * GPU (collectives = device kernels over the ranks' buffers): the multi-rank
+ * protocol on one device.  Outputs are rank 0's. */
+int sg_dist_run_threads(sg_graph *g, const sg_params *p, int32_t world, double *labels_out,
+                        sg_round *rounds_out, int64_t rounds_cap, int64_t *nrounds,
+                        double *ms_out);
 
 /* --- kernel level: the reference plugin API (_kernels_py.py:88-201) ------ */
 int sg_lb_kernel(const int64_t *offsets, int64_t nv, const int32_t *targets, int64_t ne,

@@ -23,10 +23,9 @@
 //     libnccl is dlopen'ed (preferring the copy torch already loaded), so the
 //     single-GPU library has no NCCL dependency.
 // bfs runs as unit-weight relaxation (OpPair<1>): identical labels and rounds.
-#include <dlfcn.h>
-#include <nccl.h>
+#include <thread>
 
-#include "sg_runtime.cuh"
+#include "sg_comm.cuh"
 
 namespace sg {
 namespace {
@@ -191,37 +190,6 @@ __global__ void k_part_advance(PartCtl pc, int D, Ctl *g, PartAcc *acc, RoundSta
   }
 }
 
-// ------------------------------------------------------------- NCCL (dlopen)
-struct Nccl {
-  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
-  decltype(&ncclCommInitRank) commInitRank = nullptr;
-  decltype(&ncclAllReduce) allReduce = nullptr;
-  decltype(&ncclCommDestroy) commDestroy = nullptr;
-  decltype(&ncclGetErrorString) errorString = nullptr;
-};
-const Nccl &nccl() {
-  static Nccl n = [] {
-    Nccl x;
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // torch's copy if loaded
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return x;
-    x.getUniqueId = (decltype(x.getUniqueId))dlsym(h, "ncclGetUniqueId");
-    x.commInitRank = (decltype(x.commInitRank))dlsym(h, "ncclCommInitRank");
-    x.allReduce = (decltype(x.allReduce))dlsym(h, "ncclAllReduce");
-    x.commDestroy = (decltype(x.commDestroy))dlsym(h, "ncclCommDestroy");
-    x.errorString = (decltype(x.errorString))dlsym(h, "ncclGetErrorString");
-    return x;
-  }();
-  if (!n.allReduce) throw Error(SG_ECUDA, "libnccl.so.2 not loadable");
-  return n;
-}
-#define SG_NCCL(call)                                                                    \
-  do {                                                                                   \
-    ncclResult_t r_ = (call);                                                            \
-    if (r_ != ncclSuccess)                                                               \
-      throw ::sg::Error(SG_ECUDA, std::string("NCCL: ") + ::sg::nccl().errorString(r_));        \
-  } while (0)
-
 // -------------------------------------------------------------- the driver
 struct PartRunner {
   Graph &g;
@@ -301,7 +269,7 @@ void init_pairs(L *lab, int64_t nv, bool cc, int64_t src, cudaStream_t s) {
 
 template <class L, class Op>
 void run_partitioned(PartRunner &R, const std::vector<L *> &labs, const std::vector<Op> &ops,
-                     ncclComm_t comm, double *labels_out, sg_round *rounds_out, int64_t cap,
+                     Comm *comm, double *labels_out, sg_round *rounds_out, int64_t cap,
                      int64_t *nrounds, double *ms_out) {
   const bool blocked = R.p.blocked != 0;
   const int D = R.cuts.D;
@@ -372,18 +340,18 @@ void run_partitioned(PartRunner &R, const std::vector<L *> &labs, const std::vec
       SG_CUDA(cudaGraphLaunch(exec, s));
     } else {  // NCCL: host-driven rounds (one partition on this rank)
       const long long lo = R.cuts.c[R.first], hi = R.cuts.c[R.first + 1];
-      const ncclDataType_t dt = sizeof(L) == 4 ? ncclUint32 : ncclUint64;
+      const CType dt = sizeof(L) == 4 ? CType::U32 : CType::U64;
       Ctl h;
       for (int64_t r = 0; r < limit + 1; ++r) {
         RoundCtx c{lau, s, cudaGraphConditionalHandle{}, 0};
         partition_rounds(c);
         lau.go("count_sent", k_count_sent<L>, grid_n(nv), 256, s, (const L *)labs[0], nv, lo, hi,
              (const Ctl *)g, acc);
-        SG_NCCL(nccl().allReduce(labs[0], labs[0], 2 * nv, dt, ncclMin, comm, s));
+        comm->allreduce(labs[0], 2 * nv, dt, COp::Min, s);
         lau.go("diff", k_diff_owned<L>, grid_n(hi - lo), 256, s, (const L *)labs[0], lo, hi, pc, mc,
              (const Ctl *)g, acc);
         lau.go("acc_next", k_acc_next, 1, 32, s, pc, 1, (const Ctl *)g, acc);
-        SG_NCCL(nccl().allReduce(acc, acc, kAccN, ncclInt64, ncclSum, comm, s));
+        comm->allreduce(acc, kAccN, CType::I64, COp::Sum, s);
         lau.go("part_advance", k_part_advance, 1, 32, s, pc, 1, g, acc, R.stats.p,
              Loop{limit, R.max_rounds, cudaGraphConditionalHandle{}, 0});
         SG_CUDA(cudaMemcpyAsync(&h, g, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
@@ -431,7 +399,7 @@ void run_partitioned(PartRunner &R, const std::vector<L *> &labs, const std::vec
 }
 
 template <class L, class MakeOp>
-void run_push_partitioned(PartRunner &R, MakeOp make_op, ncclComm_t comm, double *labels_out,
+void run_push_partitioned(PartRunner &R, MakeOp make_op, Comm *comm, double *labels_out,
                           sg_round *rounds_out, int64_t cap, int64_t *nrounds, double *ms_out) {
   std::vector<L *> labs;
   std::vector<decltype(make_op((L *)nullptr))> ops;
@@ -444,7 +412,7 @@ void run_push_partitioned(PartRunner &R, MakeOp make_op, ncclComm_t comm, double
   run_partitioned<L>(R, labs, ops, comm, labels_out, rounds_out, cap, nrounds, ms_out);
 }
 
-void dispatch_push(PartRunner &R, ncclComm_t comm, double *labels_out, sg_round *rounds_out,
+void dispatch_push(PartRunner &R, Comm *comm, double *labels_out, sg_round *rounds_out,
                    int64_t cap, int64_t *nrounds, double *ms_out) {
   Graph &g = R.g;
   const sg_params &p = R.p;
@@ -468,6 +436,302 @@ void dispatch_push(PartRunner &R, ncclComm_t comm, double *labels_out, sg_round 
   return run_push_partitioned<unsigned long long>(
       R, [w](unsigned long long *l) { return OpPair<3>{l, nullptr, w}; }, comm, labels_out,
       rounds_out, cap, nrounds, ms_out);
+}
+
+
+// ------------------------------------------- pull apps, one partition per rank
+// Reference: the pull view's row blocks (engine.py:64-85); a pull round writes
+// only owned rows, so comm_sent is 0 and every changed value is broadcast to
+// its mirrors (comm_broadcast, engine.py:232-234).
+constexpr int kDistN = 12;  // counter block summed over ranks each round
+
+// pr: {twc launches, lb launches, nhuge, huge_edges, nlarge, large_edges}
+__global__ void k_dist_pr_collect(const Ctl *ctl, int has_rows, long long *acc) {
+  if (threadIdx.x || ctl->done) return;
+  acc[0] = has_rows;
+  acc[1] = ctl->nhuge > 0;
+  acc[2] = ctl->nhuge;
+  acc[3] = (long long)ctl->huge_edges;
+  acc[4] = ctl->nlarge;
+  acc[5] = (long long)ctl->large_edges;
+}
+
+// kcore, after the count phase and the kill: this rank's round counters
+__global__ void k_dist_kc_collect(PullArgs a, long long *acc) {
+  const Ctl *ctl = a.ctl;
+  if (threadIdx.x || ctl->done) return;
+  const long long fs = ctl->dense ? a.row_n : ctl->fsize;
+  acc[0] = fs;
+  acc[1] = (long long)ctl->edges;
+  acc[2] = ctl->nhuge;
+  acc[3] = (long long)ctl->huge_edges;
+  acc[4] = ctl->nlarge;
+  acc[5] = (long long)ctl->large_edges;
+  acc[6] = ctl->ndying;
+  acc[7] = (long long)ctl->comm_bcast;
+  acc[8] = fs > 0;            // run_round only for a non-empty local frontier (engine.py:216)
+  acc[9] = ctl->nhuge > 0;
+}
+
+// owned vertices marked this round (alive neighbours of any rank's dying
+// vertices, after the mark all-reduce) -> this rank's next local frontier
+__global__ void k_dist_kc_compact(const Ctl *ctl, const uint32_t *mark, uint32_t lo, uint32_t hi,
+                                  uint32_t *q0, uint32_t *q1, uint32_t *nsize) {
+  if (ctl->done) return;
+  const uint32_t round = ctl->round, stamp = round + 1;
+  uint32_t *q = (round & 1) ? q0 : q1;
+  const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < hi - lo; b += st) {
+    const uint64_t i = b + threadIdx.x;
+    const bool m = i < hi - lo && mark[lo + i] == stamp;
+    warp_append(m, lo + (uint32_t)i, q, nsize);
+  }
+}
+
+__global__ void k_dist_kc_next(const Ctl *ctl, long long *acc) {
+  if (threadIdx.x || ctl->done) return;
+  acc[10] = ctl->nsize;
+}
+
+// kcore round bookkeeping from the rank-summed counters (apps.py:220-232)
+__global__ void k_dist_kc_advance(PullArgs a, long long *acc, Loop lp) {
+  Ctl *ctl = a.ctl;
+  if (threadIdx.x || ctl->done) return;
+  const uint32_t round = ctl->round;
+  RoundStat &s = a.stats[round];
+  s.frontier_size = acc[0];
+  s.active_edges = acc[1];
+  s.huge_count = acc[2];
+  s.huge_edges = acc[3];
+  s.large_count = acc[4];
+  s.large_edges = acc[5];
+  s.updated = acc[6];
+  s.comm_sent = 0;
+  s.comm_broadcast = acc[7];
+  s.launches_twc = acc[8];
+  s.launches_lb = acc[9];
+  const bool stop = acc[6] == 0 || acc[10] == 0;
+  ctl->fsize = ctl->nsize;
+  ctl->nsize = 0;
+  ctl->ndying = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_bcast = 0;
+  ctl->dense = 0;
+  ctl->round = round + 1;
+  for (int i = 0; i < kDistN; ++i) acc[i] = 0;
+  loop_test(ctl, round, stop, lp);
+}
+
+struct DistLoop {  // host-driven rounds with a done-flag read back after each
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  DistLoop() {
+    SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SG_CUDA(cudaEventCreate(&e0));
+    SG_CUDA(cudaEventCreate(&e1));
+  }
+  ~DistLoop() {
+    cudaStreamSynchronize(s);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+  }
+  bool done(const Ctl *ctl) {
+    Ctl h;
+    SG_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    return h.done != 0;
+  }
+};
+
+void dist_results(RunBufs &rb, cudaStream_t s, double *labels_d, int64_t nv, sg_round *rounds_out,
+                  int64_t cap, int64_t *nrounds, double *labels_out, int64_t max_rounds) {
+  Ctl h;
+  SG_CUDA(cudaStreamSynchronize(s));
+  SG_CUDA(cudaMemcpy(&h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  const int64_t rounds = h.round;
+  std::vector<RoundStat> st((size_t)std::min<int64_t>(rounds, rb.stats_cap));
+  if (!st.empty())
+    SG_CUDA(cudaMemcpy(st.data(), rb.stats.p, sizeof(RoundStat) * st.size(),
+                       cudaMemcpyDeviceToHost));
+  if (rounds_out && !st.empty())
+    std::memcpy(rounds_out, st.data(),
+                sizeof(RoundStat) * (size_t)std::min<int64_t>(cap, (int64_t)st.size()));
+  *nrounds = rounds;
+  if (labels_out)
+    SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+  if (h.error == SG_ECONVERGE)
+    throw Error(SG_ECONVERGE, "did not converge within " + std::to_string(max_rounds) + " rounds");
+  if (h.error) throw Error(h.error, "round log capacity exhausted");
+}
+
+void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, Comm &cm,
+                 double *labels_out, sg_round *rounds_out, int64_t cap, int64_t *nrounds,
+                 double *ms_out) {
+  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
+  const View &v = g.csc();
+  const int64_t nv = v.nv;
+  const Cuts cuts = make_cuts(v, cm.world);
+  const uint32_t lo = (uint32_t)cuts.c[cm.rank], hi = (uint32_t)cuts.c[cm.rank + 1];
+  RunBufs rb;
+  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  PullArgs a = rb.pull_args(v, thr, 0);
+  a.row_lo = lo, a.row_n = hi - lo;
+  DBuf<uint32_t> mc;
+  if (cm.world > 1) {
+    mc.alloc(nv);
+    mirror_counts(v, cuts, mc.p);
+    a.mcount = mc.p;
+  }
+  DBuf<double> inv(nv), aux0(nv), aux1(nv), hacc(nv), rank(nv);
+  DBuf<unsigned long long> gmax(1);
+  DBuf<long long> acc(kDistN);
+  const double d = p.damping, omd = 1.0 - p.damping;
+  PrOp op{aux0.p, aux1.p, aux1.p, aux0.p, rank.p, inv.p, d, omd};
+  op.mcount = a.mcount;
+  Cuts one{};
+  one.D = 1, one.c[0] = 0, one.c[1] = nv;
+  DistLoop dl;
+  cudaStream_t s = dl.s;
+  Launcher L;
+  Ctl *ctl = rb.ctl.p;
+  const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
+  PrStop st1{gmax.p, d, p.tol, v.ne, limit, max_rounds, cudaGraphConditionalHandle{}, 0, 1, 1,
+             nullptr};
+  PrStop st2 = st1;
+  st2.mode = 2, st2.dist = acc.p;
+  SG_CUDA(cudaEventRecord(dl.e0, s));
+  L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
+  L.go("init", k_pr_init, grid_n(nv), 256, s, g.csr.off.p, nv, omd, inv.p, rank.p, aux0.p);
+  fill<double>(L, hacc.p, nv, 0.0, s);
+  fill<unsigned long long>(L, gmax.p, 1, 0ull, s);
+  fill<long long>(L, acc.p, kDistN, 0ll, s);
+  if (v.ne) {  // the gain over ALL rows: every rank holds the whole view
+    L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p);
+    L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p);
+  }
+  L.go("init", k_static_bins, grid_n(hi - lo), 256, s, v.off.p, lo, hi - lo, thr, rb.largeq.p,
+       rb.hugeq.p, ctl, one);
+  if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
+  for (int64_t r = 0; r <= limit; ++r) {
+    RoundCtx c{L, s, cudaGraphConditionalHandle{}, 0};
+    pull_round(c, a, op, p.blocked != 0, hacc.p, classic);
+    L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, s, a, op, hacc.p, st1);
+    L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
+    double *auxn = (r & 1) ? aux0.p : aux1.p;  // PrOp: round r writes next1 / next0
+    cm.group_begin();
+    for (int q = 0; q < cm.world; ++q)
+      cm.bcast(auxn + cuts.c[q], (size_t)(cuts.c[q + 1] - cuts.c[q]), CType::F64, q, s);
+    cm.group_end();
+    cm.allreduce(&ctl->delta_bits, 1, CType::U64, COp::Max, s);
+    cm.allreduce(&ctl->comm_bcast, 1, CType::U64, COp::Sum, s);
+    cm.allreduce(acc.p, 6, CType::I64, COp::Sum, s);
+    L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, s, a, op, hacc.p, st2);
+    if (dl.done(ctl)) break;
+  }
+  cm.group_begin();  // every rank's rows -> the full label vector
+  for (int q = 0; q < cm.world; ++q)
+    cm.bcast(rank.p + cuts.c[q], (size_t)(cuts.c[q + 1] - cuts.c[q]), CType::F64, q, s);
+  cm.group_end();
+  SG_CUDA(cudaEventRecord(dl.e1, s));
+  SG_CUDA(cudaEventSynchronize(dl.e1));
+  float ms = 0;
+  SG_CUDA(cudaEventElapsedTime(&ms, dl.e0, dl.e1));
+  if (ms_out) *ms_out = ms;
+  dist_results(rb, s, rank.p, nv, rounds_out, cap, nrounds, labels_out, max_rounds);
+}
+
+void run_kcore_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, Comm &cm,
+                    double *labels_out, sg_round *rounds_out, int64_t cap, int64_t *nrounds,
+                    double *ms_out) {
+  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
+  const View &v = g.sym();
+  const int64_t nv = v.nv;
+  const Cuts cuts = make_cuts(v, cm.world);
+  const uint32_t lo = (uint32_t)cuts.c[cm.rank], hi = (uint32_t)cuts.c[cm.rank + 1];
+  RunBufs rb;
+  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.dying.alloc(std::max<int64_t>(nv, 1));
+  PullArgs a = rb.pull_args(v, thr, 1);
+  a.row_lo = lo, a.row_n = hi - lo;
+  DBuf<uint32_t> mc;
+  if (cm.world > 1) {
+    mc.alloc(nv);
+    mirror_counts(v, cuts, mc.p);
+    a.mcount = mc.p;
+  }
+  PushArgs w = rb.push_args(v, kNoHuge);
+  w.src_mode = 1;
+  w.no_enqueue = 1;  // marks only; owners collect them after the exchange
+  DBuf<uint8_t> alive(std::max<int64_t>(nv, 1));
+  DBuf<uint32_t> mark(std::max<int64_t>(nv, 1)), hcnt(std::max<int64_t>(nv, 1));
+  DBuf<double> labels(std::max<int64_t>(nv, 1));
+  DBuf<long long> acc(kDistN);
+  const KcOp op{alive.p, (uint32_t)std::min<int64_t>(p.k, 0xffffffffLL)};
+  const OpMark mop{alive.p, mark.p};
+  DistLoop dl;
+  cudaStream_t s = dl.s;
+  Launcher L;
+  Ctl *ctl = rb.ctl.p;
+  const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
+  const Loop lp{limit, max_rounds, cudaGraphConditionalHandle{}, 0};
+  SG_CUDA(cudaEventRecord(dl.e0, s));
+  L.go("init", k_ctl_init, 1, 1, s, ctl, 1, hi - lo);
+  fill<uint8_t>(L, alive.p, nv, (uint8_t)1, s);
+  fill<uint32_t>(L, mark.p, nv, 0u, s);
+  fill<uint32_t>(L, hcnt.p, nv, 0u, s);
+  fill<long long>(L, acc.p, kDistN, 0ll, s);
+  for (int64_t r = 0; r <= limit; ++r) {
+    RoundCtx c{L, s, cudaGraphConditionalHandle{}, 0};
+    pull_round(c, a, op, p.blocked != 0, hcnt.p, classic);
+    if (thr != kNoHuge)
+      L.go("kcore_huge", k_pull_finish<KcOp, false>, 1, 1024, s, a, op, hcnt.p, PrStop{});
+    L.go("kcore_kill", k_kcore_kill, grid_n(nv), 256, s, a, alive.p);
+    L.go("dist", k_dist_kc_collect, 1, 32, s, a, acc.p);
+    L.go("kcore_stats", k_kcore_reset, 1, 1, s, a);
+    cm.allreduce(alive.p, nv, CType::U8, COp::Min, s);
+    L.go("mark_twc", k_push_twc<OpMark>, occupancy_grid(k_push_twc<OpMark>, kTB), kTB, s, w, mop);
+    L.go("mark_large", k_push_large<OpMark>, occupancy_grid(k_push_large<OpMark>, kTB), kTB, s,
+         w, mop);
+    cm.allreduce(mark.p, nv, CType::U32, COp::Max, s);
+    L.go("dist", k_dist_kc_compact, grid_n(hi - lo), 256, s, (const Ctl *)ctl,
+         (const uint32_t *)mark.p, lo, hi, rb.q0.p, rb.q1.p, &ctl->nsize);
+    L.go("dist", k_dist_kc_next, 1, 32, s, (const Ctl *)ctl, acc.p);
+    cm.allreduce(acc.p, kDistN, CType::I64, COp::Sum, s);
+    L.go("advance", k_dist_kc_advance, 1, 32, s, a, acc.p, lp);
+    if (dl.done(ctl)) break;
+  }
+  L.go("labels", k_labels_alive, grid_n(nv), 256, s, (const uint8_t *)alive.p, nv, labels.p);
+  SG_CUDA(cudaEventRecord(dl.e1, s));
+  SG_CUDA(cudaEventSynchronize(dl.e1));
+  float ms = 0;
+  SG_CUDA(cudaEventElapsedTime(&ms, dl.e0, dl.e1));
+  if (ms_out) *ms_out = ms;
+  dist_results(rb, s, labels.p, nv, rounds_out, cap, nrounds, labels_out, max_rounds);
+}
+
+// one rank of the edge-cut BSP over communicator `cm` (any app)
+void dist_run_rank(Graph &g, const sg_params &p, Comm &cm, double *labels_out,
+                   sg_round *rounds_out, int64_t cap, int64_t *nrounds, double *ms_out) {
+  if (p.app < SG_APP_BFS || p.app > SG_APP_KCORE) throw Error(SG_ECONFIG, "unknown app");
+  if ((p.app == SG_APP_BFS || p.app == SG_APP_SSSP) && (p.source < 0 || p.source >= g.nv))
+    throw Error(SG_ECONFIG, "source " + std::to_string(p.source) + " outside graph");
+  if (p.app == SG_APP_SSSP && g.weighted && g.wmin < 0)
+    throw Error(SG_ECONFIG, "sssp requires non-negative weights");
+  if (p.app == SG_APP_PR && !(p.damping > 0.0 && p.damping < 1.0))
+    throw Error(SG_ECONFIG, "damping must be in (0, 1)");
+  if (p.app == SG_APP_PR && !(p.tol > 0.0)) throw Error(SG_ECONFIG, "tolerance must be positive");
+  if (p.app == SG_APP_KCORE && p.k < 1) throw Error(SG_ECONFIG, "k must be >= 1");
+  const int64_t max_rounds =
+      p.max_rounds > 0 ? p.max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
+  const int64_t thr = p.sched == SG_SCHED_TWC ? kNoHuge : std::max<int64_t>(1, p.threshold);
+  *nrounds = 0;
+  if (ms_out) *ms_out = 0.0;
+  if (g.nv == 0) return;
+  if (p.app == SG_APP_PR) return run_pr_dist(g, p, thr, max_rounds, cm, labels_out, rounds_out, cap, nrounds, ms_out);
+  if (p.app == SG_APP_KCORE) return run_kcore_dist(g, p, thr, max_rounds, cm, labels_out, rounds_out, cap, nrounds, ms_out);
+  PartRunner R(g, p, thr, max_rounds, cm.world, cm.rank, 1);
+  dispatch_push(R, &cm, labels_out, rounds_out, cap, nrounds, ms_out);
 }
 
 }  // namespace
@@ -499,31 +763,55 @@ int sg_dist_run(sg_graph *gh, const sg_params *p, const uint8_t nccl_id[128], in
                 int32_t world, double *labels_out, sg_round *rounds_out, int64_t rounds_cap,
                 int64_t *nrounds, double *ms_out) {
   return sg::guard([&] {
-    sg::Graph &g = *gh->g;
     if (world < 1 || world > sg::kMaxParts || rank < 0 || rank >= world)
       throw Error(SG_ECONFIG, "bad rank / world size");
-    if (p->app != SG_APP_BFS && p->app != SG_APP_SSSP && p->app != SG_APP_CC)
-      throw Error(SG_ECONFIG, "multi-GPU edge-cut is implemented for bfs / sssp / cc");
-    if ((p->app == SG_APP_BFS || p->app == SG_APP_SSSP) && (p->source < 0 || p->source >= g.nv))
-      throw Error(SG_ECONFIG, "source outside graph");
-    if (p->app == SG_APP_SSSP && g.weighted && g.wmin < 0)
-      throw Error(SG_ECONFIG, "sssp requires non-negative weights");
-    const int64_t max_rounds =
-        p->max_rounds > 0 ? p->max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
-    const int64_t thr = p->sched == SG_SCHED_TWC ? std::numeric_limits<int64_t>::max()
-                                                 : std::max<int64_t>(1, p->threshold);
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, 128);
-    ncclComm_t comm = nullptr;
-    SG_NCCL(sg::nccl().commInitRank(&comm, world, id, rank));
-    try {
-      sg::PartRunner R(g, *p, thr, max_rounds, world, rank, 1);
-      sg::dispatch_push(R, comm, labels_out, rounds_out, rounds_cap, nrounds, ms_out);
-    } catch (...) {
-      sg::nccl().commDestroy(comm);
-      throw;
-    }
-    sg::nccl().commDestroy(comm);
+    sg::NcclComm comm(nccl_id, rank, world);
+    sg::dist_run_rank(*gh->g, *p, comm, labels_out, rounds_out, rounds_cap, nrounds, ms_out);
+  });
+}
+
+int sg_dist_run_threads(sg_graph *gh, const sg_params *p, int32_t world, double *labels_out,
+                        sg_round *rounds_out, int64_t rounds_cap, int64_t *nrounds,
+                        double *ms_out) {
+  return sg::guard([&] {
+    if (world < 1 || world > sg::kMaxParts) throw Error(SG_ECONFIG, "bad world size");
+    sg::Graph &g = *gh->g;
+    if (p->app == SG_APP_CC || p->app == SG_APP_KCORE) g.sym();  // lazy views: build once
+    if (p->app == SG_APP_PR) g.csc();
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    sg::ThreadHub hub(world);
+    std::vector<std::string> err(world);
+    std::vector<int> code(world, SG_OK);
+    std::vector<std::thread> th;
+    for (int r = 0; r < world; ++r)
+      th.emplace_back([&, r] {
+        try {
+          SG_CUDA(cudaSetDevice(dev));
+          sg::ThreadComm comm(hub, r);
+          std::vector<sg_round> rr(r == 0 ? (size_t)std::max<int64_t>(rounds_cap, 0) : 0);
+          std::vector<double> lab(r == 0 ? 0 : (size_t)g.nv);
+          int64_t nr = 0;
+          double ms = 0;
+          sg::dist_run_rank(g, *p, comm, r == 0 ? labels_out : lab.data(),
+                            r == 0 ? rounds_out : nullptr, r == 0 ? rounds_cap : 0, &nr, &ms);
+          if (r == 0) {
+            *nrounds = nr;
+            if (ms_out) *ms_out = ms;
+          }
+        } catch (const Error &e) {
+          err[r] = e.what(), code[r] = e.code;
+          hub.fail();
+        } catch (const std::exception &e) {
+          err[r] = e.what(), code[r] = SG_ECUDA;
+          hub.fail();
+        }
+      });
+    for (auto &t : th) t.join();
+    for (int r = 0; r < world; ++r)  // the first real failure (not "a peer rank failed")
+      if (code[r] != SG_OK && err[r] != "a peer rank failed") throw Error(code[r], err[r]);
+    for (int r = 0; r < world; ++r)
+      if (code[r] != SG_OK) throw Error(code[r], err[r]);
   });
 }
 

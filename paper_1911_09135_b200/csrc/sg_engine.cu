@@ -161,8 +161,8 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
       L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, voff, vcol, nv, inv, gmax);
       L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax);
     }
-    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, (uint32_t)nv, thr, largeq, hugeq, ctl,
-         cuts);
+    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, (uint32_t)nv, thr, largeq, hugeq,
+         ctl, cuts);
     if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
   };
   PrOp op{aux0, aux1, aux1, aux0, labels_d, inv, d, omd};

@@ -33,6 +33,7 @@ struct PullArgs {
   RoundStat *stats;
   Cuts cuts;                // devices > 1: partition accounting (engine.py:215-234)
   const uint32_t *mcount;   // mirror_count per vertex (devices > 1), else nullptr
+  uint32_t row_lo, row_n;   // a dense round covers rows [row_lo, row_lo + row_n)
 };
 
 // pr: acc = sum aux[u]; new = (1-d) + d*acc (two roundings, as numpy); aux' = new*inv
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   const uint32_t round = ctl->round;
   op.begin(round);
   const bool dense = !a.dynamic_bins || ctl->dense;
-  const uint32_t n = dense ? a.nv : ctl->fsize;
+  const uint32_t n = dense ? a.row_n : ctl->fsize;
   const uint32_t *list = (round & 1) ? a.q[1] : a.q[0];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   unsigned long long my_edges = 0, my_large = 0;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
     int64_t s = 0, deg = 0;
     const bool valid = i < n;
     if (valid) {
-      v = dense ? (uint32_t)i : list[i];
+      v = dense ? a.row_lo + (uint32_t)i : list[i];
       s = a.off[v];
       deg = a.off[v + 1] - s;
     }
@@ -496,6 +497,11 @@ struct PrStop {            // apps.py:163-171, 183-185 evaluated on the device
   cudaGraphConditionalHandle cond;
   int use_cond;
   int parts_nonempty;      // devices > 1: partitions with rows (each launches every round)
+  // 0: single process (fold + stop); 1: rank-local half (fold huge rows, local
+  // delta / comm_bcast into Ctl, no decision); 2: global half after the
+  // all-reduce (stats + stop from the reduced Ctl fields and `dist`)
+  int mode;
+  const long long *dist;   // mode 2: DistPr counters summed over ranks
 };
 
 template <class Op, bool PR>
@@ -507,15 +513,17 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
   const uint32_t round = ctl->round;
   op.begin(round);
   const uint32_t nh = ctl->nhuge;
-  for (uint32_t i = threadIdx.x; i < nh; i += 1024) {
-    typename Op::A acc = hacc[i];
-    hacc[i] = 0;
-    uint32_t v = a.hugeq[i];
-    if (op.finish(v, acc)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
+  if (stop.mode != 2) {
+    for (uint32_t i = threadIdx.x; i < nh; i += 1024) {
+      typename Op::A acc = hacc[i];
+      hacc[i] = 0;
+      uint32_t v = a.hugeq[i];
+      if (op.finish(v, acc)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
+    }
   }
   if (!PR) return;
   __shared__ unsigned long long redb[32];
-  if (a.mcount) {
+  if (a.mcount && stop.mode != 2) {
     unsigned long long b = block_sum(op.bcast, redb);
     if (threadIdx.x == 0 && b) atomicAdd(&ctl->comm_bcast, b);
   }
@@ -525,22 +533,27 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
   if (threadIdx.x == 0) {
     for (int w = 1; w < 32; ++w) m = redd[w] > m ? redd[w] : m;
     unsigned long long mb = (unsigned long long)__double_as_longlong(m);
-    unsigned long long old = atomicMax(&ctl->delta_bits, mb);
+    if (stop.mode == 1) {  // rank-local half: the all-reduce and mode 2 follow
+      atomicMax(&ctl->delta_bits, mb);
+      return;
+    }
+    unsigned long long old = stop.mode == 2 ? ctl->delta_bits : atomicMax(&ctl->delta_bits, mb);
     double delta = __longlong_as_double((long long)(old > mb ? old : mb));
     double worst = __dmul_rn(stop.damping, __longlong_as_double((long long)*stop.gain_max_bits));
     double eps_stop = stop.tol / (worst > 1.0 ? worst : 1.0);
     RoundStat &st = a.stats[round];
     st.frontier_size = a.nv;
     st.active_edges = stop.ne;
-    st.huge_count = nh;
-    st.huge_edges = (long long)ctl->huge_edges;
-    st.large_count = ctl->nlarge;
-    st.large_edges = (long long)ctl->large_edges;
+    const bool g2 = stop.mode == 2;  // dist = {twc, lb, nhuge, huge_edges, nlarge, large_edges}
+    st.huge_count = g2 ? stop.dist[2] : nh;
+    st.huge_edges = g2 ? stop.dist[3] : (long long)ctl->huge_edges;
+    st.large_count = g2 ? stop.dist[4] : ctl->nlarge;
+    st.large_edges = g2 ? stop.dist[5] : (long long)ctl->large_edges;
     st.updated = a.nv;
     st.comm_sent = 0;
     st.comm_broadcast = (long long)ctl->comm_bcast;
-    st.launches_twc = a.cuts.D > 1 ? stop.parts_nonempty : 1;
-    st.launches_lb = a.cuts.D > 1 ? __popc(ctl->part_lb_mask) : nh > 0;
+    st.launches_twc = stop.mode == 2 ? stop.dist[0] : a.cuts.D > 1 ? stop.parts_nonempty : 1;
+    st.launches_lb = stop.mode == 2 ? stop.dist[1] : a.cuts.D > 1 ? __popc(ctl->part_lb_mask) : nh > 0;
     ctl->comm_bcast = 0;
     ctl->delta_bits = 0;
     ctl->large_head = 0;

@@ -220,16 +220,17 @@ __global__ void k_pr_gain_max(const int64_t *off, const uint32_t *col, int64_t n
 }
 
 // static bins of a dense pull view (pr): CTA-bin rows and huge rows
-__global__ void k_static_bins(const int64_t *off, uint32_t n, int64_t thr, uint32_t *largeq,
-                              uint32_t *hugeq, Ctl *ctl, Cuts cuts) {
+__global__ void k_static_bins(const int64_t *off, uint32_t lo, uint32_t n, int64_t thr,
+                              uint32_t *largeq, uint32_t *hugeq, Ctl *ctl, Cuts cuts) {
   uint64_t st = (uint64_t)gridDim.x * blockDim.x;
   unsigned long long le = 0;
   uint32_t lbm = 0;
   for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < n; b += st) {
-    uint64_t v = b + threadIdx.x;
-    int64_t d = v < n ? off[v + 1] - off[v] : 0;
-    bool huge = v < n && d >= thr;
-    bool large = v < n && !huge && d >= (int64_t)kLarge;
+    const bool in = b + threadIdx.x < n;
+    uint64_t v = lo + b + threadIdx.x;
+    int64_t d = in ? off[v + 1] - off[v] : 0;
+    bool huge = in && d >= thr;
+    bool large = in && !huge && d >= (int64_t)kLarge;
     if (large) le += (unsigned long long)d;
     if (huge && cuts.D > 1) lbm |= 1u << owner_of(cuts, (uint32_t)v);
     warp_append(huge, (uint32_t)v, hugeq, &ctl->nhuge);
@@ -452,6 +453,8 @@ struct RunBufs {
     a.dynamic_bins = dyn;
     a.dying = dying.p;
     a.stats = stats.p;
+    a.row_lo = 0;
+    a.row_n = (uint32_t)v.nv;
     return a;
   }
 };

@@ -57,14 +57,27 @@ def max_over_ranks(dist, value: float) -> float:
 def run_app(graph, app_name: str, scheduler: Scheduler = Scheduler("alb"),
             config: KernelConfig = KernelConfig(), *, rank: int, world: int, nccl_id: bytes,
             max_rounds=None, **params) -> RunResult:
-    """engine.run_app with one edge-cut partition per rank (bfs / sssp / cc)."""
+    """engine.run_app with one edge-cut partition per rank (every app)."""
     app = make_app(app_name, **params)
-    if app.name not in ("bfs", "sssp", "cc"):
-        raise ConfigError("the NCCL edge cut covers bfs / sssp / cc")
     if max_rounds is None:
         max_rounds = 10 * max(graph.num_vertices, 1) + 256
     p = _device_params(app, scheduler, config, world, max_rounds)
     labels, log, ms = native.dist_run(graph.device(), p, nccl_id, rank, world)
+    return RunResult(labels=labels, records=_records_from_log(log, scheduler, config),
+                     app_name=app.name, scheduler=scheduler, config=config, devices=world,
+                     num_vertices=graph.num_vertices, num_edges=graph.num_edges,
+                     device_ms=ms, round_log=log)
+
+
+def run_app_threads(graph, app_name: str, scheduler: Scheduler = Scheduler("alb"),
+                    config: KernelConfig = KernelConfig(), *, world: int, max_rounds=None,
+                    **params) -> RunResult:
+    """The same per-rank protocol with `world` ranks as threads on this GPU."""
+    app = make_app(app_name, **params)
+    if max_rounds is None:
+        max_rounds = 10 * max(graph.num_vertices, 1) + 256
+    p = _device_params(app, scheduler, config, world, max_rounds)
+    labels, log, ms = native.dist_run_threads(graph.device(), p, world)
     return RunResult(labels=labels, records=_records_from_log(log, scheduler, config),
                      app_name=app.name, scheduler=scheduler, config=config, devices=world,
                      num_vertices=graph.num_vertices, num_edges=graph.num_edges,

@@ -27,7 +27,7 @@ EXPORTS = (
     "sg_last_error", "sg_device_count", "sg_graph_create", "sg_graph_create_rmat",
     "sg_graph_attach_random_weights", "sg_graph_with_weights", "sg_graph_info",
     "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_run_profiled",
-    "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run",
+    "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run", "sg_dist_run_threads",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
 )
 
@@ -92,6 +92,8 @@ def load(path: Path | None = None):
             "sg_nccl_unique_id": ([P], ctypes.c_int),
             "sg_dist_run": ([P, ctypes.POINTER(Params), P, i32, i32, P, P, i64, P, P],
                             ctypes.c_int),
+            "sg_dist_run_threads": ([P, ctypes.POINTER(Params), i32, P, P, i64, P, P],
+                                    ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -245,6 +247,20 @@ def dist_run(dev: DeviceGraph, params: Params, nccl_id: bytes, rank: int, world:
     idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
     check(load().sg_dist_run(dev.handle, ctypes.byref(params), idb, rank, world, ptr(labels),
                              ptr(rounds), rounds_cap, ctypes.byref(n), ctypes.byref(ms)))
+    return labels, rounds[: min(n.value, rounds_cap)].copy(), ms.value
+
+
+def dist_run_threads(dev: DeviceGraph, params: Params, world: int, rounds_cap=1 << 16):
+    """The per-rank edge-cut code path of sg_dist_run with `world` ranks as host
+    threads on this one GPU (collectives are device kernels): rank 0's labels
+    and the global round log."""
+    nv, _, _ = dev.info()
+    labels = np.empty(nv, dtype=np.float64)
+    rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
+    n = ctypes.c_int64(0)
+    ms = ctypes.c_double(0.0)
+    check(load().sg_dist_run_threads(dev.handle, ctypes.byref(params), world, ptr(labels),
+                                     ptr(rounds), rounds_cap, ctypes.byref(n), ctypes.byref(ms)))
     return labels, rounds[: min(n.value, rounds_cap)].copy(), ms.value
 
 

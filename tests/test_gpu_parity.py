@@ -231,7 +231,7 @@ def test_larger_scale_vs_c_oracle(sg, scale, thr, app):
         assert np.array_equal(res.labels, lab)
 
 
-@pytest.mark.parametrize("app", ["bfs", "sssp", "cc"])
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
 def test_nccl_edge_cut_single_rank(sg, golden, app):
     """The NCCL multi-GPU driver (sg_dist_run) with world size 1 on this GPU:
     partition restriction, NCCL all-reduce(min), diff pass and the NCCL
@@ -244,6 +244,29 @@ def test_nccl_edge_cut_single_rank(sg, golden, app):
     params = sg.engine._device_params(sg.apps.make_app(app), sg.Scheduler("alb"),
                                       sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
     labels, log, ms = native.dist_run(g.device(), params, native.nccl_unique_id(), 0, 1)
-    assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
+    if app == "pr":
+        ref = sg.run_app(g, "pr")
+        assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
+    else:
+        assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
     assert [[int(r["frontier_size"]), int(r["active_edges"])] for r in log] == \
         [x[:2] for x in info["per_round"]]
+
+
+@pytest.mark.parametrize("key", ["alb/d2", "alb/d4", "alb/d8", "alb-t256/d2", "alb-t256/d4"])
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
+def test_edge_cut_ranks_as_threads(sg, golden, app, key):
+    """The multi-rank protocol of sg_dist_run (the code NCCL runs per GPU) with
+    world = D ranks as threads on this GPU: labels, per-round log, comm_sent /
+    comm_broadcast and kernel launches against the reference's devices=D run."""
+    from paper_1911_09135_b200 import dist
+    info = golden["runs"]["rmat12"][f"{app}/{key}"]
+    g = _graph(sg, "rmat12")
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    world = int(key.split("/d")[1])
+    res = dist.run_app_threads(g, app, _sched(sg, "x/" + key.split("/")[0] + "/x"), world=world)
+    _check(sg, res, info, app)
+    if app == "pr":
+        ref = sg.run_app(g, "pr")
+        assert np.max(np.abs(res.labels - ref.labels)) <= PR_ATOL
