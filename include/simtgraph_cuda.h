@@ -93,6 +93,14 @@ typedef struct sg_round { /* one BSP round (engine.py:116-163) */
 const char *sg_last_error(void);
 int sg_device_count(int *count);
 
+/* Memory.  Device buffers come from a caching allocator (no cudaMalloc /
+ * cudaFree per graph or run after warm-up); sg_release_cached returns the
+ * cached blocks to the driver.  sg_host_alloc hands out cached pinned host
+ * blocks, e.g. for labels_out (full-speed D2H); release with sg_host_free. */
+int sg_host_alloc(int64_t bytes, void **out);
+void sg_host_free(void *p);
+void sg_release_cached(void);
+
 /* --- graph store (graph.py:29-177) ------------------------------------- */
 /* Upload a CSR (graph.py:33-37 dtypes): offsets int64[nv+1], targets int32[ne],
  * weights int64[ne] or NULL.  Validates like Graph._validate (graph.py:44-57). */

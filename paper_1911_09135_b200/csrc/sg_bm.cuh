@@ -54,6 +54,26 @@ struct BmBfs {
       if (!(w[u] & bit)) atomicOr(vis + (dst[u] >> 5), bit);  // RED.OR (result unused)
     }
   }
+  using W = uint32_t;
+  template <int N>
+  __device__ __forceinline__ void fetch(const PushArgs &a, const int64_t (&e)[N],
+                                        const bool (&ok)[N], uint32_t (&dst)[N],
+                                        W (&)[N]) const {
+#pragma unroll
+    for (int u = 0; u < N; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+  }
+  template <int N>
+  __device__ __forceinline__ void apply(const uint32_t (&dst)[N], const W (&)[N], const L (&)[N],
+                                        const bool (&ok)[N]) const {
+    uint32_t w[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) w[u] = ok[u] ? vis[dst[u] >> 5] : ~0u;
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      const uint32_t bit = 1u << (dst[u] & 31u);
+      if (!(w[u] & bit)) atomicOr(vis + (dst[u] >> 5), bit);
+    }
+  }
   // new bits of word wi (and advance prev)
   __device__ __forceinline__ uint32_t take(uint32_t wi) const {
     const uint32_t x = vis[wi], n = x & ~prev[wi];
@@ -97,6 +117,42 @@ struct BmMin {
       if (p[u] < cur[u]) {  // ok[u] implied: cur = 0 otherwise
         atomicMin(lab + dst[u], p[u]);                      // RED.MIN
         atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));  // RED.OR
+      }
+    }
+  }
+  // split relax for software-pipelined loops: fetch (adjacency + weight
+  // loads) of step k+1 is issued before apply (label gathers + reductions)
+  // of step k
+  using W = typename std::conditional<KIND == 3, int64_t, uint32_t>::type;
+  template <int N>
+  __device__ __forceinline__ void fetch(const PushArgs &a, const int64_t (&e)[N],
+                                        const bool (&ok)[N], uint32_t (&dst)[N],
+                                        W (&w)[N]) const {
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+      if (KIND == 2) w[u] = ok[u] ? ld_stream(w32 + e[u]) : 0u;
+      if (KIND == 3) w[u] = (ok[u] && w64) ? ld_stream(w64 + e[u]) : (W)1;
+    }
+  }
+  template <int N>
+  __device__ __forceinline__ void apply(const uint32_t (&dst)[N], const W (&w)[N],
+                                        const L (&sv)[N], const bool (&ok)[N]) const {
+    L p[N], cur[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      if (KIND == 0) p[u] = sv[u];
+      else if (KIND == 1) p[u] = sv[u] + 1u;
+      else if (KIND == 2) p[u] = sv[u] + (uint32_t)w[u];
+      else p[u] = (L)__double_as_longlong(
+               __dadd_rn(__longlong_as_double((long long)sv[u]), (double)w[u]));
+      cur[u] = ok[u] ? lab[dst[u]] : L(0);
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      if (ok[u] && p[u] < cur[u]) {
+        atomicMin(lab + dst[u], p[u]);
+        atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));
       }
     }
   }
@@ -239,6 +295,89 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
         svs[u] = second ? v1 : v0;
       }
       op.relax(a, e, ok, svs);
+    }
+    __syncthreads();
+  }
+}
+
+#ifndef SG_PIPE_V
+#define SG_PIPE_V 4
+#endif
+constexpr int kPV = SG_PIPE_V;  // edges per lane per step of the pipelined CTA-bin loop
+
+// CTA bin, software-pipelined: the adjacency (+ weight) loads of step k+1 are
+// in flight while step k's label gathers and reductions issue
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
+  using L = typename Op::L;
+  using W = typename Op::W;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  __shared__ int64_t bstart[kBatch];
+  __shared__ long long bexcl[kBatch + 1];
+  __shared__ L bsv[kBatch];
+  __shared__ uint32_t bhead;
+  const uint32_t nb = (n + kBatch - 1) / kBatch;
+  const long long wstep = 32 * kPV, step = (long long)kTB * kPV;
+  const long long woff = (long long)(threadIdx.x >> 5) * wstep;
+  const uint32_t lane = threadIdx.x & 31u;
+  for (;;) {
+    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    __syncthreads();
+    const uint32_t bidx = bhead;
+    if (bidx >= nb) break;
+    if (threadIdx.x < 32) {
+      const uint32_t i = bidx + threadIdx.x * nb;  // degree-mixed batch
+      long long d = 0;
+      if (threadIdx.x < kBatch && i < n) {
+        const uint32_t v = a.largeq[i];
+        const int64_t s = a.off[v];
+        d = a.off[v + 1] - s;
+        bstart[threadIdx.x] = s;
+        bsv[threadIdx.x] = (L)a.largesv[i];
+      }
+      const long long incl = warp_incl_scan(d);
+      if (threadIdx.x < kBatch) bexcl[threadIdx.x + 1] = incl;
+      if (threadIdx.x == 0) bexcl[0] = 0;
+    }
+    __syncthreads();
+    const long long total = bexcl[kBatch];
+    auto slots = [&](long long b, int64_t (&e)[kPV], bool (&ok)[kPV], L (&sv)[kPV]) {
+      const long long wbase = b + woff;
+      uint32_t lo = 0;
+#pragma unroll
+      for (uint32_t st = kBatch / 2; st; st >>= 1) lo = bexcl[lo + st] <= wbase ? lo + st : lo;
+      const long long x0 = bexcl[lo], x1 = bexcl[lo + 1];
+      const int64_t s0 = bstart[lo], s1 = lo + 1 < kBatch ? bstart[lo + 1] : 0;
+      const L v0 = bsv[lo], v1 = lo + 1 < kBatch ? bsv[lo + 1] : L(0);
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) {
+        const long long slot = wbase + u * 32 + lane;
+        ok[u] = slot < total;
+        const bool second = slot >= x1;
+        e[u] = second ? s1 + (slot - x1) : s0 + (slot - x0);
+        sv[u] = second ? v1 : v0;
+      }
+    };
+    int64_t e[kPV];
+    bool ok0[kPV], ok1[kPV];
+    L sv0[kPV], sv1[kPV];
+    uint32_t d0[kPV], d1[kPV];
+    W w0[kPV], w1[kPV];
+    slots(0, e, ok0, sv0);
+    op.fetch(a, e, ok0, d0, w0);
+    for (long long b = 0; b < total; b += step) {
+      const bool more = b + step < total;
+      if (more) {
+        slots(b + step, e, ok1, sv1);
+        op.fetch(a, e, ok1, d1, w1);
+      }
+      op.apply(d0, w0, sv0, ok0);
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) d0[u] = d1[u], w0[u] = w1[u], sv0[u] = sv1[u], ok0[u] = more && ok1[u];
     }
     __syncthreads();
   }

@@ -62,6 +62,18 @@ int guard(F &&f) {
 }
 
 // --------------------------------------------------------- device buffer --
+// Caching device allocator (sg_engine.cu): freed blocks are kept per size and
+// reused, so repeated graph uploads and runs do not pay cudaMalloc / cudaFree
+// (each a device-wide synchronisation).  Contract: a block is released only
+// after the stream work that uses it has completed (every driver synchronises
+// its stream before its buffers go out of scope).  On allocation failure the
+// cache is returned to the driver and the allocation retried.
+void *dev_alloc(size_t bytes);
+void dev_free(void *p);
+void dev_release_cached();
+void *host_alloc(size_t bytes);  // pinned, cached (result buffers)
+void host_free(void *p);
+
 template <class T>
 struct DBuf {
   T *p = nullptr;
@@ -79,10 +91,10 @@ struct DBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) SG_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    if (count) p = static_cast<T *>(dev_alloc(sizeof(T) * count));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }

@@ -18,6 +18,105 @@ std::atomic<int64_t> g_launches{0};
 static thread_local std::string t_last_error;
 void set_last_error(const std::string &m) { t_last_error = m; }
 
+namespace {
+struct DevPool {
+  std::mutex mu;
+  std::multimap<size_t, void *> free_blocks;
+  std::unordered_map<void *, size_t> block_size;
+};
+DevPool &dev_pool() {
+  static DevPool *p = new DevPool;  // intentionally leaked: usable during static destruction
+  return *p;
+}
+size_t pool_round(size_t b) {
+  const size_t g = b >= ((size_t)1 << 20) ? ((size_t)2 << 20) : 512;
+  return (b + g - 1) / g * g;
+}
+}  // namespace
+
+void *dev_alloc(size_t bytes) {
+  DevPool &P = dev_pool();
+  const size_t b = pool_round(bytes);
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.free_blocks.lower_bound(b);
+    if (it != P.free_blocks.end() && it->first <= b + b / 8) {  // <= 12.5 % slack
+      void *p = it->second;
+      P.free_blocks.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    dev_release_cached();
+    e = cudaMalloc(&p, b);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(SG_ENOMEM, "cudaMalloc(" + std::to_string(b) + " B): " + cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.block_size[p] = b;
+  return p;
+}
+
+void dev_free(void *p) {
+  DevPool &P = dev_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  auto it = P.block_size.find(p);
+  if (it == P.block_size.end()) return;
+  P.free_blocks.emplace(it->second, p);
+}
+
+// pinned host blocks for result buffers (cudaHostAlloc is slow: cache them)
+namespace {
+DevPool &host_pool() {
+  static DevPool *p = new DevPool;
+  return *p;
+}
+}  // namespace
+
+void *host_alloc(size_t bytes) {
+  DevPool &P = host_pool();
+  size_t b = (size_t)1 << 16;  // power-of-two classes: pinning is slow, reuse matters
+  while (b < bytes) b <<= 1;
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.free_blocks.find(b);
+    if (it != P.free_blocks.end()) {
+      void *p = it->second;
+      P.free_blocks.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  SG_CUDA(cudaHostAlloc(&p, b, cudaHostAllocDefault));
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.block_size[p] = b;
+  return p;
+}
+
+void host_free(void *p) {
+  DevPool &P = host_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  auto it = P.block_size.find(p);
+  if (it == P.block_size.end()) return;
+  P.free_blocks.emplace(it->second, p);
+}
+
+void dev_release_cached() {
+  DevPool &P = dev_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  cudaDeviceSynchronize();
+  for (auto &kv : P.free_blocks) {
+    cudaFree(kv.second);
+    P.block_size.erase(kv.second);
+  }
+  P.free_blocks.clear();
+}
+
 const SmInfo &sm_info() {
   static SmInfo info = [] {
     SmInfo s;
@@ -373,6 +472,19 @@ extern "C" {
 const char *sg_last_error(void) { return sg::t_last_error.c_str(); }
 
 int64_t sg_kernel_launches(void) { return sg::g_launches.load(); }
+
+int sg_host_alloc(int64_t bytes, void **out) {
+  return sg::guard([&] {
+    if (bytes < 0) throw Error(SG_ECONFIG, "negative size");
+    *out = sg::host_alloc((size_t)std::max<int64_t>(bytes, 1));
+  });
+}
+
+void sg_host_free(void *p) {
+  if (p) sg::host_free(p);
+}
+
+void sg_release_cached(void) { sg::dev_release_cached(); }
 
 int sg_device_count(int *count) {
   return sg::guard([&] { SG_CUDA(cudaGetDeviceCount(count)); });

@@ -494,6 +494,9 @@ void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
   }
 }
 
+#ifndef SG_LARGE_PIPE
+#define SG_LARGE_PIPE 1
+#endif
 // single-device push round with the bitmap next-frontier (sg_bm.cuh)
 template <class Op>
 void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool classic = false) {
@@ -501,6 +504,9 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
   if (classic)
     c.L.go("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
            c.s, a, op);
+  else if (SG_LARGE_PIPE)
+    c.L.go("push_large", k_bm_large_pipe<Op>, occupancy_grid(k_bm_large_pipe<Op>, kTB), kTB, c.s,
+           a, op);
   else
     c.L.go("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
   if (a.threshold != kNoHuge) {

@@ -29,6 +29,7 @@ EXPORTS = (
     "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_run_profiled",
     "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run", "sg_dist_run_threads",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
+    "sg_host_alloc", "sg_host_free", "sg_release_cached",
 )
 
 
@@ -94,6 +95,9 @@ def load(path: Path | None = None):
                             ctypes.c_int),
             "sg_dist_run_threads": ([P, ctypes.POINTER(Params), i32, P, P, i64, P, P],
                                     ctypes.c_int),
+            "sg_host_alloc": ([i64, pp], ctypes.c_int),
+            "sg_host_free": ([P], None),
+            "sg_release_cached": ([], None),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -101,6 +105,43 @@ def load(path: Path | None = None):
             fn.restype = res
         _lib = lib
         return lib
+
+
+class _PinnedBlock:
+    """A cached pinned host block (sg_host_alloc); returned to the library's
+    pool when the last numpy view of it is gone."""
+
+    __slots__ = ("ptr", "__weakref__")
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        check(load().sg_host_alloc(nbytes, ctypes.byref(p)))
+        self.ptr = p.value
+
+    def __del__(self):
+        if self.ptr and _lib is not None:
+            _lib.sg_host_free(self.ptr)
+            self.ptr = None
+
+
+PINNED_MIN_BYTES = 4 << 20  # below this a pageable copy costs less than pinning
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """numpy array in pinned host memory (device->host copies at full PCIe speed)."""
+    dtype = np.dtype(dtype)
+    nbytes = max(int(n) * dtype.itemsize, 1)
+    if nbytes < PINNED_MIN_BYTES:
+        return np.empty(int(n), dtype=dtype)
+    blk = _PinnedBlock(nbytes)
+    raw = (ctypes.c_char * nbytes).from_address(blk.ptr)
+    raw.owner = blk  # the array keeps the block alive
+    return np.frombuffer(raw, dtype=dtype, count=int(n))
+
+
+def release_cached():
+    """Return the library's cached device blocks to the CUDA driver."""
+    load().sg_release_cached()
 
 
 def check(code: int):
@@ -203,7 +244,7 @@ class DeviceGraph:
         """Run the BSP loop on the device.  Returns (labels, round log, ms) or,
         with ``profile``, (labels, round log, ms, {kernel: (launches, ms)})."""
         nv, _, _ = self.info()
-        labels = np.empty(nv, dtype=np.float64)
+        labels = pinned_empty(nv, np.float64)
         rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
         n = ctypes.c_int64(0)
         ms = ctypes.c_double(0.0)
@@ -240,7 +281,7 @@ def dist_run(dev: DeviceGraph, params: Params, nccl_id: bytes, rank: int, world:
     """One edge-cut partition per rank over NCCL (sg_dist_run); every rank gets
     the merged labels and the global round log."""
     nv, _, _ = dev.info()
-    labels = np.empty(nv, dtype=np.float64)
+    labels = pinned_empty(nv, np.float64)
     rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
     n = ctypes.c_int64(0)
     ms = ctypes.c_double(0.0)
@@ -255,7 +296,7 @@ def dist_run_threads(dev: DeviceGraph, params: Params, world: int, rounds_cap=1 
     threads on this one GPU (collectives are device kernels): rank 0's labels
     and the global round log."""
     nv, _, _ = dev.info()
-    labels = np.empty(nv, dtype=np.float64)
+    labels = pinned_empty(nv, np.float64)
     rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
     n = ctypes.c_int64(0)
     ms = ctypes.c_double(0.0)
