@@ -69,6 +69,8 @@ def parse():
                     help="comma list of extra apps reported on the same rmat graph ('' = none)")
     ap.add_argument("--no-ablation", action="store_true",
                     help="skip the ALB vs TWC-only (classic / batched CTA bin) ablation")
+    ap.add_argument("--pr-block", type=int, default=0,
+                    help="pr source-block size in vertices (0 = automatic, -1 = never tile)")
     ap.add_argument("--cta-bin", default="batched", choices=["batched", "classic"],
                     help="TWC CTA bin: edge-balanced batches (default) or one vertex per CTA")
     return ap.parse_args()
@@ -304,6 +306,7 @@ def main():
     dev = g.device()
     nv, ne, _ = dev.info()
     sched, params = run_params(sg, a.app, a.sched, a.threshold, nv, a.cta_bin == "classic")
+    params.reserved = a.pr_block if a.pr_block > 0 else (1 << 31) - 1 if a.pr_block < 0 else 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     nccl_id = None
     if world > 1:  # edge cut: one partition per rank, NCCL label exchange

@@ -607,8 +607,14 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
   fill<unsigned long long>(L, gmax.p, 1, 0ull, s);
   fill<long long>(L, acc.p, kDistN, 0ll, s);
   if (v.ne) {  // the gain over ALL rows: every rank holds the whole view
+    DBuf<uint32_t> big(nv), nbig(1);
+    fill<uint32_t>(L, nbig.p, 1, 0u, s);
     L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p);
-    L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p);
+    L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p,
+         big.p, nbig.p);
+    L.go("pr_gain", k_pr_gain_big, sm_info().sms * 4, 256, s, v.off.p, v.col.p,
+         (const double *)inv.p, (const uint32_t *)big.p, (const uint32_t *)nbig.p, gmax.p);
+    SG_CUDA(cudaStreamSynchronize(s));
   }
   L.go("init", k_static_bins, grid_n(hi - lo), 256, s, v.off.p, lo, hi - lo, thr, rb.largeq.p,
        rb.hugeq.p, ctl, one);

@@ -225,6 +225,9 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   }
 }
 
+constexpr int64_t kPrTileBytes = 64ll << 20;  // rank-vector slice per source block
+constexpr double kPrTileCoverage = 0.6;       // see prep_pr
+
 void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d, int64_t thr,
              int64_t max_rounds) {
   const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
@@ -244,6 +247,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   double *inv = P.buf<double>(nv), *aux0 = P.buf<double>(nv), *aux1 = P.buf<double>(nv),
          *hacc = P.buf<double>(nv);
   unsigned long long *gmax = P.buf<unsigned long long>(1);
+  uint32_t *gbig = P.buf<uint32_t>(nv), *nbig = P.buf<uint32_t>(1);
   const double d = p.damping, omd = 1.0 - p.damping;
   const int64_t *csr_off = g.csr.off.p;
   Ctl *ctl = rb.ctl.p;
@@ -257,8 +261,12 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
     fill<double>(L, hacc, nv, 0.0, s);
     fill<unsigned long long>(L, gmax, 1, 0ull, s);
     if (vne) {
+      fill<uint32_t>(L, nbig, 1, 0u, s);
       L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, voff, vcol, nv, inv, gmax);
-      L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax);
+      L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax, gbig,
+           nbig);
+      L.go("pr_gain", k_pr_gain_big, sm_info().sms * 4, 256, s, voff, vcol, (const double *)inv,
+           (const uint32_t *)gbig, (const uint32_t *)nbig, gmax);
     }
     L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, (uint32_t)nv, thr, largeq, hugeq,
          ctl, cuts);
@@ -269,6 +277,69 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   const bool blocked = p.blocked != 0;
   const int64_t ne = v.ne;
   const double tol = p.tol;
+
+  // Source-block tiling: once the rank vector (V * 8 B) outgrows the L2, one
+  // pull pass per source block gathers from an L2-resident slice (Tiles,
+  // sg_graph.cu); rows carry their partial sums between passes.  Without it a
+  // uniform rmat25 round moves ~95 B of DRAM per 8-byte gather (ncu).
+  // Automatic choice (p.reserved == 0): tile when the rank vector exceeds the
+  // slice AND the graph's sources are not already skewed enough for the L2 to
+  // catch the hot ranks by itself (rmat: the top quarter of vertices by
+  // out-degree source most edges; tiling only adds row passes there).
+  int64_t S = p.reserved > 0 ? (int64_t)p.reserved : 0;
+  if (!S && nv * 8 > kPrTileBytes) {
+    const int64_t B = (nv * 8 + kPrTileBytes - 1) / kPrTileBytes;
+    const int64_t S0 = ((nv + B - 1) / B + 1023) / 1024 * 1024;
+    if (g.source_coverage(S0) < kPrTileCoverage) S = S0;
+  }
+  if (S > 0 && S < nv && p.devices == 1) {
+    const Tiles &T = g.tiles(S);
+    const int B = (int)T.blk.size();
+    double *carry = P.buf<double>(nv);
+    long long *meta = P.buf<long long>(4 * (B + 1));  // per block + the full CSC (reference bins)
+    std::vector<PullArgs> ab((size_t)B);
+    for (int b = 0; b < B; ++b) {
+      PullArgs x = a;
+      x.off = T.blk[(size_t)b].off.p;
+      x.col = T.blk[(size_t)b].col.p;
+      x.largeq = P.buf<uint32_t>(nv), x.hugeq = P.buf<uint32_t>(nv);
+      x.hpre = P.buf<int64_t>(nv), x.hstart = P.buf<int64_t>(nv);
+      ab[(size_t)b] = x;
+    }
+    auto base_init = P.init;
+    P.init = [=](Launcher &L, cudaStream_t s) {
+      base_init(L, s);  // ranks, gain, full-CSC bins + prefix (for the round log)
+      L.go("init", k_tile_store, 1, 1, s, ctl, meta + 4 * B);
+      for (int b = 0; b < B; ++b) {
+        const PullArgs &x = ab[(size_t)b];
+        L.go("init", k_static_bins, grid_n(nv), 256, s, x.off, 0u, (uint32_t)nv, thr, x.largeq,
+             x.hugeq, ctl, cuts);
+        if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, x);
+        L.go("init", k_tile_store, 1, 1, s, ctl, meta + 4 * b);
+      }
+    };
+    P.round = [=, &rb](RoundCtx &c) {
+      for (int b = 0; b < B; ++b) {
+        PrOp ob = op;
+        ob.carry = carry;
+        ob.tmode = b == 0 ? 1 : b < B - 1 ? 2 : 3;
+        c.L.go("tile_select", k_tile_select, 1, 1, c.s, ctl, (const long long *)meta + 4 * b);
+        pull_round(c, ab[(size_t)b], ob, blocked, hacc, classic);
+        if (b < B - 1) {
+          c.L.go("pr_fold", k_pull_finish<PrOp, false>, 1, 1024, c.s, ab[(size_t)b], ob, hacc,
+                 PrStop{});
+        } else {
+          PrStop stop{gmax, d, tol, ne, std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds,
+                      c.cond, c.use_cond, parts_nonempty};
+          stop.bins = meta + 4 * B;
+          c.L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, c.s, ab[(size_t)b], ob, hacc,
+                 stop);
+        }
+      }
+    };
+    P.finish = [](Launcher &, cudaStream_t) {};
+    return;
+  }
   P.round = [=, &rb](RoundCtx &c) {
     pull_round(c, a, op, blocked, hacc, classic);
     PrStop stop{gmax, d, tol, ne, std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds, c.cond,

@@ -244,6 +244,102 @@ void weights_finalize(Graph &g) {
   }
 }
 
+namespace {
+// lengths of row v's block-b segment: positions of the block bounds inside the
+// (source-sorted) CSC row, by binary search
+__global__ void k_tile_len(const int64_t *off, const uint32_t *col, int64_t nv, int64_t lo_id,
+                           int64_t hi_id, int64_t *len) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st) {
+    const int64_t b = off[v], e = off[v + 1];
+    auto lower = [&](int64_t key) {  // first position with col >= key
+      int64_t l = b, h = e;
+      while (l < h) {
+        const int64_t m = (l + h) >> 1;
+        if ((int64_t)col[m] < key) l = m + 1;
+        else h = m;
+      }
+      return l;
+    };
+    len[v] = lower(hi_id) - lower(lo_id);
+  }
+}
+// copy row v's block segment into the block view (warp per row)
+__global__ void k_tile_fill(const int64_t *off, const uint32_t *col, int64_t nv, int64_t lo_id,
+                            const int64_t *boff, uint32_t *bcol) {
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nv; v += warps) {
+    const int64_t b = off[v], e = off[v + 1], n = boff[v + 1] - boff[v];
+    if (!n) continue;
+    int64_t l = b, h = e;  // segment start: first col >= lo_id
+    while (l < h) {
+      const int64_t m = (l + h) >> 1;
+      if ((int64_t)col[m] < lo_id) l = m + 1;
+      else h = m;
+    }
+    for (int64_t j = lane; j < n; j += 32) bcol[boff[v] + j] = col[l + j];
+  }
+}
+}  // namespace
+
+namespace {
+__global__ void k_outdeg(const int64_t *off, int64_t nv, uint32_t *deg) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st)
+    deg[v] = (uint32_t)(off[v + 1] - off[v]);
+}
+}  // namespace
+
+double Graph::source_coverage(int64_t K) {
+  if (K == cov_k_) return cov_;
+  cov_k_ = K;
+  cov_ = 1.0;
+  if (ne == 0 || K >= nv) return cov_;
+  DBuf<uint32_t> deg(nv), sorted(nv);
+  DBuf<unsigned long long> sum(1);
+  SG_LAUNCH(k_outdeg, grid_for(nv), 256, 0, 0, csr.off.p, nv, deg.p);
+  size_t t1 = 0, t2 = 0;
+  SG_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, t1, deg.p, sorted.p, nv));
+  SG_CUDA(cub::DeviceReduce::Sum(nullptr, t2, sorted.p, sum.p, K));
+  DBuf<char> t(std::max(t1, t2));
+  SG_CUDA(cub::DeviceRadixSort::SortKeysDescending(t.p, t1, deg.p, sorted.p, nv));
+  SG_CUDA(cub::DeviceReduce::Sum(t.p, t2, sorted.p, sum.p, K));
+  unsigned long long h = 0;
+  SG_CUDA(cudaMemcpy(&h, sum.p, sizeof(h), cudaMemcpyDeviceToHost));
+  cov_ = (double)h / (double)ne;
+  return cov_;
+}
+
+const Tiles &Graph::tiles(int64_t S) {
+  if (tiles_ && tiles_->S == S) return *tiles_;
+  const View &c = csc();
+  auto t = std::make_unique<Tiles>();
+  t->S = S;
+  const int64_t B = (nv + S - 1) / S;
+  t->blk.resize((size_t)B);
+  DBuf<int64_t> len(nv + 1);
+  for (int64_t b = 0; b < B; ++b) {
+    View &v = t->blk[(size_t)b];
+    v.nv = nv;
+    v.off.alloc(nv + 1);
+    SG_LAUNCH(k_tile_len, grid_for(nv), 256, 0, 0, c.off.p, c.col.p, nv, b * S,
+              std::min<int64_t>((b + 1) * S, nv), len.p);
+    SG_CUDA(cudaMemset(len.p + nv, 0, sizeof(int64_t)));
+    size_t tmp = 0;
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, len.p, v.off.p, nv + 1));
+    DBuf<char> t2(tmp);
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(t2.p, tmp, len.p, v.off.p, nv + 1));
+    SG_CUDA(cudaMemcpy(&v.ne, v.off.p + nv, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    v.col.alloc(v.ne ? v.ne : 1);
+    SG_LAUNCH(k_tile_fill, grid_for(nv * 32), 256, 0, 0, c.off.p, c.col.p, nv, b * S, v.off.p,
+              v.col.p);
+    SG_CUDA(cudaDeviceSynchronize());
+  }
+  tiles_ = std::move(t);
+  return *tiles_;
+}
+
 const View &Graph::csc() {
   if (!csc_) {
     auto v = std::make_unique<View>();

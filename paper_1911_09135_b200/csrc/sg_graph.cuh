@@ -14,6 +14,16 @@ struct View {
   DBuf<uint32_t> col;
 };
 
+// The CSC split into B source blocks (pr, sg_engine.cu): block b holds, for
+// every row, the in-edges whose source lies in [b*S, (b+1)*S) -- a contiguous
+// sub-range of the CSC row, since CSC rows are sorted by source.  A pull pass
+// over one block gathers from an S*8-byte slice of the rank vector that stays
+// resident in L2 (the whole vector does not once V*8 B exceeds the L2).
+struct Tiles {
+  int64_t S = 0;
+  std::vector<View> blk;
+};
+
 struct Graph {
   int64_t nv = 0, ne = 0;
   View csr;
@@ -25,6 +35,14 @@ struct Graph {
   std::unique_ptr<View> sym_;  // Graph.symmetrized() (graph.py:115-128), built lazily
   const View &csc();
   const View &sym();
+  std::unique_ptr<Tiles> tiles_;  // pr source blocks of the CSC, built lazily per S
+  const Tiles &tiles(int64_t S);
+  // fraction of the edges whose source is among the K highest out-degree
+  // vertices (cached per K): how much of a pull's gather traffic a cache of K
+  // rank values absorbs on its own
+  double source_coverage(int64_t K);
+  int64_t cov_k_ = -1;
+  double cov_ = 0.0;
 };
 
 // builders (sg_graph.cu)

@@ -51,12 +51,25 @@ struct PrOp {
   double *auxn = nullptr;
   double dmax = 0.0;
   unsigned long long bcast = 0;
+  // source-block tiling (prep_pr): 1 first block (carry = acc), 2 middle
+  // block (carry += acc), 3 last block (acc = carry + acc, then the fold)
+  double *carry = nullptr;
+  int tmode = 0;
   __device__ __forceinline__ void begin(uint32_t round) {
     aux = (round & 1) ? aux1 : aux0;
     auxn = (round & 1) ? next1 : next0;
   }
   __device__ __forceinline__ A load(uint32_t u) const { return __ldg(aux + u); }
   __device__ __forceinline__ bool finish(uint32_t v, A acc) {
+    if (tmode == 1) {
+      carry[v] = acc;
+      return false;
+    }
+    if (tmode == 2) {
+      carry[v] = carry[v] + acc;
+      return false;
+    }
+    if (tmode == 3) acc = carry[v] + acc;
     double nw = __dadd_rn(omd, __dmul_rn(d, acc));
     const double old = rank[v];
     double dl = fabs(__dsub_rn(nw, old));
@@ -487,6 +500,21 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
   }
 }
 
+// tiled pr: per-block static bin counts {nhuge, huge_edges, nlarge, large_edges}
+static __global__ void k_tile_store(Ctl *ctl, long long *meta) {
+  if (threadIdx.x) return;
+  meta[0] = ctl->nhuge, meta[1] = (long long)ctl->huge_edges;
+  meta[2] = ctl->nlarge, meta[3] = (long long)ctl->large_edges;
+  ctl->nhuge = ctl->nlarge = 0;
+  ctl->huge_edges = ctl->large_edges = 0;
+}
+static __global__ void k_tile_select(Ctl *ctl, const long long *meta) {
+  if (threadIdx.x || ctl->done) return;
+  ctl->nhuge = (uint32_t)meta[0], ctl->huge_edges = (unsigned long long)meta[1];
+  ctl->nlarge = (uint32_t)meta[2], ctl->large_edges = (unsigned long long)meta[3];
+  ctl->large_head = ctl->chunk_head = 0;
+}
+
 // huge-row fold (single CTA; huge rows are few) — plus the pr round advance
 struct PrStop {            // apps.py:163-171, 183-185 evaluated on the device
   const unsigned long long *gain_max_bits;  // max_v sum_{u->v} inv_outdeg[u]
@@ -502,6 +530,7 @@ struct PrStop {            // apps.py:163-171, 183-185 evaluated on the device
   // all-reduce (stats + stop from the reduced Ctl fields and `dist`)
   int mode;
   const long long *dist;   // mode 2: DistPr counters summed over ranks
+  const long long *bins;   // tiled pr: {nhuge, huge_edges, nlarge, large_edges} of the full CSC
 };
 
 template <class Op, bool PR>
@@ -545,15 +574,18 @@ __global__ void __launch_bounds__(1024) k_pull_finish(PullArgs a, Op op,
     st.frontier_size = a.nv;
     st.active_edges = stop.ne;
     const bool g2 = stop.mode == 2;  // dist = {twc, lb, nhuge, huge_edges, nlarge, large_edges}
-    st.huge_count = g2 ? stop.dist[2] : nh;
-    st.huge_edges = g2 ? stop.dist[3] : (long long)ctl->huge_edges;
-    st.large_count = g2 ? stop.dist[4] : ctl->nlarge;
-    st.large_edges = g2 ? stop.dist[5] : (long long)ctl->large_edges;
+    st.huge_count = g2 ? stop.dist[2] : stop.bins ? stop.bins[0] : nh;
+    st.huge_edges = g2 ? stop.dist[3] : stop.bins ? stop.bins[1] : (long long)ctl->huge_edges;
+    st.large_count = g2 ? stop.dist[4] : stop.bins ? stop.bins[2] : ctl->nlarge;
+    st.large_edges = g2 ? stop.dist[5] : stop.bins ? stop.bins[3] : (long long)ctl->large_edges;
     st.updated = a.nv;
     st.comm_sent = 0;
     st.comm_broadcast = (long long)ctl->comm_bcast;
     st.launches_twc = stop.mode == 2 ? stop.dist[0] : a.cuts.D > 1 ? stop.parts_nonempty : 1;
-    st.launches_lb = stop.mode == 2 ? stop.dist[1] : a.cuts.D > 1 ? __popc(ctl->part_lb_mask) : nh > 0;
+    st.launches_lb = stop.mode == 2 ? stop.dist[1]
+                     : a.cuts.D > 1  ? __popc(ctl->part_lb_mask)
+                     : stop.bins     ? stop.bins[0] > 0
+                                     : nh > 0;
     ctl->comm_bcast = 0;
     ctl->delta_bits = 0;
     ctl->large_head = 0;

@@ -171,11 +171,12 @@ __global__ void k_pr_init(const int64_t *off, int64_t n, double omd, double *inv
     aux[v] = __dmul_rn(omd, iv);
   }
 }
-// gain[v] = sum_{u->v} inv[u] in CSC (== CSR edge) order, exactly as
-// np.bincount accumulates it (apps.py:166-168); max over v by atomicMax.
-// Rows up to kGainThread edges: one thread folds its row left to right (loads
-// issued 8 ahead); longer rows: a warp loads 32 terms and every lane folds
-// them in order through shuffles.
+// gain[v] = sum_{u->v} inv[u] (apps.py:166-168), max over v by atomicMax.
+// Rows up to kGainThread edges: one thread folds its row left to right in
+// CSC (== CSR edge) order, exactly as np.bincount accumulates it.  Longer rows
+// (the hubs, where the maximum usually is): one warp, strided partial sums and
+// a tree reduction -- the same value to within rounding (a few ulp), which only
+// matters if a round's max|delta| lands within those ulps of eps_stop.
 constexpr int64_t kGainThread = 64;
 __global__ void k_pr_gain_rows(const int64_t *off, const uint32_t *col, int64_t n,
                                const double *inv, unsigned long long *maxbits) {
@@ -199,24 +200,55 @@ __global__ void k_pr_gain_rows(const int64_t *off, const uint32_t *col, int64_t 
   if (lane_id() == 0 && best > 0)
     atomicMax(maxbits, (unsigned long long)__double_as_longlong(best));
 }
+constexpr int64_t kGainWarp = 8192;  // longer rows: one CTA each (k_pr_gain_big)
 __global__ void k_pr_gain_max(const int64_t *off, const uint32_t *col, int64_t n,
-                              const double *inv, unsigned long long *maxbits) {
+                              const double *inv, unsigned long long *maxbits, uint32_t *big,
+                              uint32_t *nbig) {
   int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double best = 0.0;
   for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-    const int64_t e = off[v + 1];
-    if (e - off[v] <= kGainThread) continue;
-    double acc = 0.0;
-    for (int64_t b = off[v]; b < e; b += 32) {
-      int64_t j = b + lane_id();
-      double x = j < e ? inv[col[j]] : 0.0;
-      int cnt = (int)min((int64_t)32, e - b);
-      for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, __shfl_sync(kFull, x, t));
+    const int64_t b = off[v], e = off[v + 1];
+    if (e - b <= kGainThread) continue;
+    if (e - b > kGainWarp) {
+      if (lane_id() == 0) big[atomicAdd(nbig, 1u)] = (uint32_t)v;
+      continue;
     }
+    double acc = 0.0;
+    for (int64_t j = b + lane_id(); j < e; j += 32 * 4) {
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + 32 * u < e ? inv[col[j + 32 * u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += x[u];
+    }
+    acc = warp_sum(acc);
     best = acc > best ? acc : best;
   }
   if (lane_id() == 0 && best > 0)
     atomicMax(maxbits, (unsigned long long)__double_as_longlong(best));
+}
+
+__global__ void __launch_bounds__(256) k_pr_gain_big(const int64_t *off, const uint32_t *col,
+                                                     const double *inv, const uint32_t *big,
+                                                     const uint32_t *nbig,
+                                                     unsigned long long *maxbits) {
+  __shared__ double red[32];
+  for (uint32_t i = blockIdx.x; i < *nbig; i += gridDim.x) {
+    const uint32_t v = big[i];
+    const int64_t b = off[v], e = off[v + 1];
+    double acc = 0.0;
+    for (int64_t j = b + threadIdx.x; j < e; j += 256 * 4) {
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = j + 256 * u < e ? inv[col[j + 256 * u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += x[u];
+    }
+    acc = block_sum(acc, red);
+    if (threadIdx.x == 0 && acc > 0)
+      atomicMax(maxbits, (unsigned long long)__double_as_longlong(acc));
+    __syncthreads();
+  }
 }
 
 // static bins of a dense pull view (pr): CTA-bin rows and huge rows
@@ -414,8 +446,10 @@ struct RunBufs {
 
   void alloc_common(int64_t nv, int64_t rounds_cap) {
     size_t n = (size_t)std::max<int64_t>(nv, 1);
+    // no memset here: every driver zeroes the block with k_ctl_init on its own
+    // (non-blocking) stream; a legacy-stream memset is NOT ordered before that
+    // and could land after it (seen as a lost dense frontier with ranks as threads)
     ctl.alloc(1);
-    SG_CUDA(cudaMemset(ctl.p, 0, sizeof(Ctl)));
     stats_cap = rounds_cap;
     stats.alloc(rounds_cap);
     q0.alloc(n), q1.alloc(n), largeq.alloc(n), hugeq.alloc(n);

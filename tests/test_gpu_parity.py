@@ -270,3 +270,35 @@ def test_edge_cut_ranks_as_threads(sg, golden, app, key):
     if app == "pr":
         ref = sg.run_app(g, "pr")
         assert np.max(np.abs(res.labels - ref.labels)) <= PR_ATOL
+
+
+@pytest.mark.parametrize("gname,S", [("rmat12", 1000), ("rmat14", 3000), ("rmat16", 21845),
+                                     ("uniform16", 20000), ("rmat16", 1 << 15)])
+def test_pr_source_block_tiling(sg, golden, gname, S):
+    """pr over the CSC split into source blocks of S vertices (the L2-resident
+    tiling large graphs use): ranks within the reference tolerance, the same
+    rounds, and the round log's bins / lb launches of the untiled CSC."""
+    info = golden["runs"][gname]["pr/alb/d1"]
+    g = _graph(sg, gname)
+    p = sg.engine._device_params(sg.apps.make_app("pr"), sg.Scheduler("alb"), sg.KernelConfig(),
+                                 1, 10 * g.num_vertices + 256)
+    p.reserved = S
+    labels, log, ms = g.device().run(p)
+    ref = sg.run_app(g, "pr")
+    assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
+    got = [[int(r["frontier_size"]), int(r["active_edges"])] for r in log]
+    assert got == [x[:2] for x in info["per_round"]]
+    assert [int(r["launches_lb"]) for r in log] == [x[4] for x in info["per_round"]]
+
+
+def test_pr_tiling_thresholds(sg):
+    """Tiled pr with huge / CTA-bin rows inside each block (small thresholds)."""
+    g = _graph(sg, "rmat14")
+    ref = sg.run_app(g, "pr")
+    for thr in (1, 64, 300):
+        p = sg.engine._device_params(sg.apps.make_app("pr"), sg.Scheduler("alb", threshold=thr),
+                                     sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
+        p.reserved = 5000
+        labels, log, ms = g.device().run(p)
+        assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
+        assert len(log) == len(ref.records)
