@@ -434,6 +434,14 @@ def main():
                                  "classic_cta_bin": {"alb_gteps": alb_c, "twc_gteps": tw_c,
                                                      "alb_over_twc": alb_c / tw_c}}
 
+    # every scheduler of the reference on the headline workload (paper Table 3)
+    schedulers = {}
+    if rank == 0 and world == 1 and not a.no_ablation:
+        for kind in ("vertex", "edge", "lb", "twc", "alb"):
+            schedulers[kind] = round(device_steps(
+                torch, dev, run_params(sg, a.app, kind, a.threshold, nv)[1],
+                max(2, min(a.steps, 3)), 1, flush)["gteps"], 2)
+
     if rank != 0:
         return
     line = {
@@ -464,6 +472,7 @@ def main():
         "apps": {k: {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                  for k, v in extra.items()},
         "ablation_alb_vs_twc": ablation,
+        "schedulers_gteps": schedulers,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

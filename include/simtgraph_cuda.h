@@ -50,12 +50,15 @@ extern "C" {
 /* scheduler kinds (schedulers.py:30) */
 #define SG_SCHED_ALB 0
 #define SG_SCHED_TWC 1
+#define SG_SCHED_LB 2     /* prefix over every active vertex + LB kernel (schedulers.py:280-283) */
+#define SG_SCHED_VERTEX 3 /* one thread per active vertex (_kernels_py.py:88-97) */
+#define SG_SCHED_EDGE 4   /* contiguous per-thread active-edge ranges (_kernels_py.py:100-117) */
 
 typedef struct sg_graph sg_graph; /* opaque: HBM-resident CSR (+ lazy CSC / sym) */
 
 typedef struct sg_params {
   int32_t app;        /* SG_APP_* */
-  int32_t sched;      /* SG_SCHED_ALB | SG_SCHED_TWC (twc = no huge bin) */
+  int32_t sched;      /* SG_SCHED_* (twc = no huge bin) */
   int32_t blocked;    /* huge-vertex distribution: 0 cyclic, 1 blocked (schedulers.py:191-200) */
   int32_t devices;    /* edge-cut partitions (engine.py:64-85); >1 = simulated on this GPU */
   int64_t source;     /* bfs / sssp (apps.py:83-95) */

@@ -502,6 +502,166 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
   }
 }
 
+// ------------------------------------------- the other schedulers (run level)
+// vertex (_kernels_py.py:88-97): frontier vertex i -> one thread, which walks
+// all of its edges (no balancing: the baseline the bins exist to beat)
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_vertex(PushArgs a, Op op) {
+  using L = typename Op::L;
+  __shared__ unsigned long long red[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  op.begin(ctl->round);
+  const Src src = resolve_src(a, ctl);
+  unsigned long long my_edges = 0;
+  const uint64_t st = (uint64_t)gridDim.x * kTB;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kTB; i0 < src.n; i0 += st) {
+    const uint64_t i = i0 + threadIdx.x;
+    int64_t s = 0, deg = 0;
+    L sv = 0;
+    if (i < src.n) {
+      const uint32_t v = src.at(i);
+      s = a.off[v];
+      deg = a.off[v + 1] - s;
+      sv = op.src_val(i, v);
+    }
+    my_edges += (unsigned long long)deg;
+    for (int64_t j = 0; j < deg; j += kV) {
+      int64_t e[kV];
+      bool ok[kV];
+      L svs[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) ok[u] = j + u < deg, e[u] = s + j + u, svs[u] = sv;
+      op.relax(a, e, ok, svs);
+    }
+  }
+  const unsigned long long bs = block_sum(my_edges, red);
+  if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+}
+
+// lb / edge: the whole frontier as one prefix-summed list (PrefixWork over
+// every active vertex, schedulers.py:280-283), built by a multi-CTA scan in
+// tiles of kFT entries: hugeq / hstart / hval / hpre as for ALB's huge bin
+constexpr int kFT = 1024;
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_front_tiles(PushArgs a, Op op, long long *tsum) {
+  __shared__ long long red[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  op.begin(ctl->round);
+  const Src src = resolve_src(a, ctl);
+  const uint32_t ntiles = (src.n + kFT - 1) / kFT;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < kFT / kTB; ++k) {
+      const uint64_t i = (uint64_t)t * kFT + k * kTB + threadIdx.x;
+      if (i < src.n) {
+        const uint32_t v = src.at(i);
+        const int64_t s = a.off[v], d = a.off[v + 1] - s;
+        a.hugeq[i] = v;
+        a.hstart[i] = s;
+        a.hval[i] = (unsigned long long)op.src_val(i, v);
+        a.hpre[i] = d;  // degrees; k_front_apply turns them into the inclusive prefix
+        sum += d;
+      }
+    }
+    sum = block_sum(sum, red);
+    if (threadIdx.x == 0) tsum[t] = sum;
+    __syncthreads();
+  }
+}
+// exclusive scan of the tile sums (one CTA); totals into Ctl
+static __global__ void __launch_bounds__(1024) k_front_scan(PushArgs a, long long *tsum) {
+  __shared__ long long red[32];
+  __shared__ long long carry;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const Src src = resolve_src(a, ctl);
+  const uint32_t ntiles = (src.n + kFT - 1) / kFT;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t b = 0; b < ntiles; b += 1024) {
+    const uint32_t i = b + threadIdx.x;
+    const long long d = i < ntiles ? tsum[i] : 0;
+    const long long x = warp_incl_scan(d);
+    if (lane_id() == 31) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) red[threadIdx.x] = warp_incl_scan(red[threadIdx.x]);
+    __syncthreads();
+    const long long incl = carry + ((threadIdx.x >> 5) ? red[(threadIdx.x >> 5) - 1] : 0) + x;
+    if (i < ntiles) tsum[i] = incl - d;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ctl->huge_edges = (unsigned long long)carry;
+    ctl->edges = (unsigned long long)carry;
+    ctl->nhuge = src.n;
+  }
+}
+static __global__ void __launch_bounds__(kTB) k_front_apply(PushArgs a, const long long *tsum) {
+  __shared__ long long red[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const Src src = resolve_src(a, ctl);
+  const uint32_t ntiles = (src.n + kFT - 1) / kFT;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    long long carry = tsum[t];
+#pragma unroll
+    for (int k = 0; k < kFT / kTB; ++k) {
+      const uint64_t i = (uint64_t)t * kFT + k * kTB + threadIdx.x;
+      const long long d = i < src.n ? a.hpre[i] : 0;
+      const long long x = warp_incl_scan(d);
+      if (lane_id() == 31) red[threadIdx.x >> 5] = x;
+      __syncthreads();
+      long long wpre = 0, tot = 0;
+      for (int w = 0; w < kWarpsTB; ++w) {
+        if (w < (int)(threadIdx.x >> 5)) wpre += red[w];
+        tot += red[w];
+      }
+      if (i < src.n) a.hpre[i] = carry + wpre + x;
+      carry += tot;
+      __syncthreads();
+    }
+  }
+}
+
+// edge (_kernels_py.py:100-117): thread t takes the contiguous active-edge
+// range [t*chunk, (t+1)*chunk); the owner is found once and then walked
+// forward (the O(1) endpoint step the reference gets from its COO array)
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_edge(PushArgs a, Op op) {
+  using L = typename Op::L;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t nh = ctl->nhuge;
+  const int64_t E = (int64_t)ctl->huge_edges;
+  if (!nh || !E) return;
+  op.begin(ctl->round);
+  const int64_t T = (int64_t)gridDim.x * kTB;
+  const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
+  const int64_t chunk = (E + T - 1) / T;
+  const int64_t g0 = tid * chunk, g1 = min(g0 + chunk, E);
+  if (g0 >= E) return;
+  uint32_t o = owner_search(a.hpre, nh, g0);
+  for (int64_t g = g0; g < g1; g += kV) {
+    int64_t e[kV];
+    bool ok[kV];
+    L sv[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t gg = g + u;
+      ok[u] = gg < g1;
+      while (ok[u] && gg >= a.hpre[o]) ++o;
+      e[u] = a.hstart[o] + (gg - (o ? a.hpre[o - 1] : 0));
+      sv[u] = (L)a.hval[o];
+    }
+    op.relax(a, e, ok, sv);
+  }
+}
+
 // next frontier from the round's bitmap: ids ascending within each warp's
 // 1024-vertex range, one atomic per warp range, coalesced id / snapshot writes
 template <class Op>

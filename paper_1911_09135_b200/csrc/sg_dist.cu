@@ -730,7 +730,10 @@ void dist_run_rank(Graph &g, const sg_params &p, Comm &cm, double *labels_out,
   if (p.app == SG_APP_KCORE && p.k < 1) throw Error(SG_ECONFIG, "k must be >= 1");
   const int64_t max_rounds =
       p.max_rounds > 0 ? p.max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
-  const int64_t thr = p.sched == SG_SCHED_TWC ? kNoHuge : std::max<int64_t>(1, p.threshold);
+  if (p.sched < SG_SCHED_ALB || p.sched > SG_SCHED_EDGE) throw Error(SG_ECONFIG, "unknown scheduler");
+  const int64_t thr = p.sched == SG_SCHED_TWC ? kNoHuge
+                      : p.sched == SG_SCHED_ALB ? std::max<int64_t>(1, p.threshold)
+                                                : 1;  // lb / vertex / edge: the LB path
   *nrounds = 0;
   if (ms_out) *ms_out = 0.0;
   if (g.nv == 0) return;

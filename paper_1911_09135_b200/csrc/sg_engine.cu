@@ -146,6 +146,8 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   PushArgs a = rb.push_args(v, thr);
   a.q[1] = a.q[0];  // one frontier array: k_bm_compact rewrites it after the round
+  a.sched = p.sched == SG_SCHED_LB ? 1 : p.sched == SG_SCHED_VERTEX ? 2 : p.sched == SG_SCHED_EDGE ? 3 : 0;
+  long long *tsum = a.sched == 1 || a.sched == 3 ? P.buf<long long>((nv + kFT - 1) / kFT + 1) : nullptr;
   const bool blocked = p.blocked != 0;
   const int64_t src = p.source;
   Ctl *ctl = rb.ctl.p;
@@ -157,7 +159,7 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   };
   auto set_round = [&](auto op) {
     P.round = [=, &rb](RoundCtx &c) {
-      bm_round(c, a, op, blocked, classic);
+      bm_round(c, a, op, blocked, classic, tsum);
       c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
     };
   };
@@ -235,6 +237,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   PullArgs a = rb.pull_args(v, thr, 0);
+  a.vertex = p.sched == SG_SCHED_VERTEX;
   // devices > 1: CSC-row edge cut; pulls write only owned rows, so comm_sent
   // is 0 and every changed rank is broadcast to its mirrors (engine.py:88-113)
   const Cuts cuts = make_cuts(v, p.devices);
@@ -292,7 +295,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
     const int64_t S0 = ((nv + B - 1) / B + 1023) / 1024 * 1024;
     if (g.source_coverage(S0) < kPrTileCoverage) S = S0;
   }
-  if (S > 0 && S < nv && p.devices == 1) {
+  if (S > 0 && S < nv && p.devices == 1 && !a.vertex) {
     const Tiles &T = g.tiles(S);
     const int B = (int)T.blk.size();
     double *carry = P.buf<double>(nv);
@@ -357,6 +360,7 @@ void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *l
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   rb.dying.alloc(std::max<int64_t>(nv, 1));
   PullArgs a = rb.pull_args(v, thr, 1);
+  a.vertex = p.sched == SG_SCHED_VERTEX;
   const Cuts cuts = make_cuts(v, p.devices);  // sym CSC rows == sym CSR rows
   if (p.devices > 1) {
     uint32_t *mc = P.buf<uint32_t>(nv);
@@ -414,7 +418,15 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
     throw Error(SG_ECONFIG, "sssp requires non-negative weights");
   const int64_t max_rounds =
       p.max_rounds > 0 ? p.max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
-  const int64_t thr = p.sched == SG_SCHED_TWC ? kNoHuge : std::max<int64_t>(1, p.threshold);
+  if (p.sched < SG_SCHED_ALB || p.sched > SG_SCHED_EDGE) throw Error(SG_ECONFIG, "unknown scheduler");
+  // alb: the resolved threshold; twc / vertex: no huge bin; lb / edge: every
+  // active vertex goes through the prefix (the push engine runs dedicated
+  // frontier-prefix / vertex / edge kernels, the pull and partitioned paths
+  // the LB kernel with threshold 1 or a one-thread-per-row kernel)
+  const int64_t thr = p.sched == SG_SCHED_TWC || p.sched == SG_SCHED_VERTEX ? kNoHuge
+                      : p.sched == SG_SCHED_LB || p.sched == SG_SCHED_EDGE
+                          ? 1
+                          : std::max<int64_t>(1, p.threshold);
   *nrounds = 0;
   if (ms_out) *ms_out = 0.0;
   if (g.nv == 0) return;

@@ -34,6 +34,7 @@ struct PullArgs {
   Cuts cuts;                // devices > 1: partition accounting (engine.py:215-234)
   const uint32_t *mcount;   // mirror_count per vertex (devices > 1), else nullptr
   uint32_t row_lo, row_n;   // a dense round covers rows [row_lo, row_lo + row_n)
+  int vertex;               // vertex scheduler: k_pull_vertex instead of the bins
 };
 
 // pr: acc = sum aux[u]; new = (1-d) + d*acc (two roundings, as numpy); aux' = new*inv
@@ -235,6 +236,59 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
     if (a.mcount) {
       unsigned long long b = warp_sum(op.bcast);
       if (lane == 0 && b) atomicAdd(&ctl->comm_bcast, b);
+    }
+  }
+}
+
+// vertex scheduler (_kernels_py.py:88-97): one thread folds one row
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_pull_vertex(PullArgs a, Op op) {
+  __shared__ unsigned long long red[32];
+  __shared__ double redd[32];
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  const uint32_t round = ctl->round;
+  op.begin(round);
+  const bool dense = !a.dynamic_bins || ctl->dense;
+  const uint32_t n = dense ? a.row_n : ctl->fsize;
+  const uint32_t *list = (round & 1) ? a.q[1] : a.q[0];
+  unsigned long long my_edges = 0;
+  const uint64_t st = (uint64_t)gridDim.x * kTB;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kTB; i0 < n; i0 += st) {
+    const uint64_t i = i0 + threadIdx.x;
+    bool die = false;
+    uint32_t v = 0;
+    if (i < n) {
+      v = dense ? a.row_lo + (uint32_t)i : list[i];
+      const int64_t s = a.off[v], e = a.off[v + 1];
+      my_edges += (unsigned long long)(e - s);
+      typename Op::A acc = 0;
+      for (int64_t j = s; j < e; j += 4) {
+        typename Op::A x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = j + u < e ? op.load(a.col[j + u]) : typename Op::A(0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += x[u];
+      }
+      die = op.finish(v, acc);
+    }
+    warp_append(die, v, a.dying, &ctl->ndying);
+  }
+  if (a.dynamic_bins) {
+    const unsigned long long bs = block_sum(my_edges, red);
+    if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+  }
+  if (sizeof(typename Op::A) == 8) {
+    double m = warp_max(op.dmax);
+    if (lane_id() == 0) redd[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kWarpsTB; ++w) m = redd[w] > m ? redd[w] : m;
+      if (m > 0) atomic_max_dbits(&ctl->delta_bits, m);
+    }
+    if (a.mcount) {
+      unsigned long long b = warp_sum(op.bcast);
+      if (lane_id() == 0 && b) atomicAdd(&ctl->comm_bcast, b);
     }
   }
 }

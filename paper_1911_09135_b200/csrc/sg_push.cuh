@@ -57,6 +57,7 @@ struct PushArgs {
   int src_mode;           // 0 frontier, 1 kcore dying list
   RoundStat *stats;
   int no_enqueue;         // partitioned runs: frontiers come from the label exchange
+  int sched;              // 0 alb / twc, 1 lb, 2 vertex, 3 edge (round-log launch accounting)
   uint32_t dense_lo, dense_n;  // a dense frontier is [dense_lo, dense_lo + dense_n)
 };
 

@@ -368,8 +368,12 @@ __global__ void k_push_advance(PushArgs a, Loop lp) {
   s.updated = nn;
   s.comm_sent = (long long)ctl->comm_sent;
   s.comm_broadcast = (long long)ctl->comm_bcast;
-  s.launches_twc = s.frontier_size > 0;
-  s.launches_lb = ctl->nhuge > 0;
+  // alb / twc: inspect + twc per non-empty round, lb when huge vertices exist;
+  // lb: one lb launch when the prefix has edges (schedulers.py:280-283);
+  // vertex / edge: one launch per non-empty round (reported as launches_twc)
+  s.launches_twc = a.sched == 1 ? 0 : s.frontier_size > 0;
+  s.launches_lb = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
+  if (a.sched >= 2) s.huge_count = s.large_count = s.large_edges = 0, s.huge_edges = 0;
   ctl->fsize = nn;
   ctl->nsize = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
@@ -533,7 +537,28 @@ void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
 #endif
 // single-device push round with the bitmap next-frontier (sg_bm.cuh)
 template <class Op>
-void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool classic = false) {
+void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool classic = false,
+              long long *tsum = nullptr) {
+  if (a.sched == 2) {  // vertex
+    c.L.go("push_vertex", k_bm_vertex<Op>, occupancy_grid(k_bm_vertex<Op>, kTB), kTB, c.s, a, op);
+    c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
+    return;
+  }
+  if (a.sched == 1 || a.sched == 3) {  // lb / edge: prefix over the whole frontier
+    const int g = occupancy_grid(k_front_tiles<Op>, kTB);
+    c.L.go("front_prefix", k_front_tiles<Op>, g, kTB, c.s, a, op, tsum);
+    c.L.go("front_prefix", k_front_scan, 1, 1024, c.s, a, tsum);
+    c.L.go("front_prefix", k_front_apply, g, kTB, c.s, a, (const long long *)tsum);
+    if (a.sched == 3)
+      c.L.go("push_edge", k_bm_edge<Op>, occupancy_grid(k_bm_edge<Op>, kTB), kTB, c.s, a, op);
+    else if (blocked)
+      c.L.go("push_lb", k_bm_lb<Op, true>, occupancy_grid(k_bm_lb<Op, true>, kTB), kTB, c.s, a, op);
+    else
+      c.L.go("push_lb", k_bm_lb<Op, false>, occupancy_grid(k_bm_lb<Op, false>, kTB), kTB, c.s, a,
+             op);
+    c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
+    return;
+  }
   c.L.go("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
   if (classic)
     c.L.go("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
@@ -557,6 +582,11 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
 template <class Op>
 void pull_round(RoundCtx &c, const PullArgs &a, const Op &op, bool blocked, typename Op::A *hacc,
                 bool classic = false) {
+  if (a.vertex) {  // vertex scheduler: one thread per row
+    c.L.go("pull_vertex", k_pull_vertex<Op>, occupancy_grid(k_pull_vertex<Op>, kTB), kTB, c.s, a,
+           op);
+    return;
+  }
   c.L.go("pull_twc", k_pull_twc<Op>, occupancy_grid(k_pull_twc<Op>, kTB), kTB, c.s, a, op);
   if (classic)
     c.L.go("pull_large", k_pull_large_classic<Op>, occupancy_grid(k_pull_large_classic<Op>, kTB),

@@ -21,7 +21,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsimtgraph_cuda.so"
 
 SG_OK, SG_ECONFIG, SG_ERANGE, SG_ECONVERGE, SG_ECUDA, SG_ENOMEM = 0, -1, -2, -3, -4, -5
 APP_IDS = {"bfs": 0, "sssp": 1, "cc": 2, "pr": 3, "kcore": 4}
-SCHED_IDS = {"alb": 0, "twc": 1}
+SCHED_IDS = {"alb": 0, "twc": 1, "lb": 2, "vertex": 3, "edge": 4}
 
 EXPORTS = (
     "sg_last_error", "sg_device_count", "sg_graph_create", "sg_graph_create_rmat",

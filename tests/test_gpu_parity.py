@@ -81,9 +81,6 @@ def _runs(golden):
         for key in runs:
             if key == "graph":
                 continue
-            app, sched, d = key.split("/")
-            if sched.startswith("lb"):
-                continue  # lb kind is covered separately (labels/rounds only)
             out.append((gname, key))
     return out
 
@@ -97,8 +94,7 @@ def test_run_level_parity(sg, golden, gname, key):
     g = _graph(sg, gname)
     if app == "sssp":
         g = sg.attach_random_weights(g, 2)
-    mode = "kernel" if key.split("/")[1] in ("vertex", "edge") else "device"
-    res = sg.run_app(g, app, _sched(sg, key), devices=devices, mode=mode)
+    res = sg.run_app(g, app, _sched(sg, key), devices=devices)  # every scheduler on the device
     _check(sg, res, info, app)
     if app == "pr":
         from oracle import oracle_c as C
