@@ -37,6 +37,9 @@ struct Comm {
   virtual void bcast(void *buf, size_t n, CType t, int root, cudaStream_t s) = 0;
   virtual void group_begin() {}
   virtual void group_end() {}
+  // personalised exchange: element counts / displacements per peer (host arrays)
+  virtual void alltoallv(const void *send, const size_t *scount, const size_t *sdispl, void *recv,
+                         const size_t *rcount, const size_t *rdispl, CType t, cudaStream_t s) = 0;
 };
 
 // ----------------------------------------------------------------- NCCL --
@@ -45,6 +48,8 @@ struct NcclApi {
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
@@ -60,6 +65,8 @@ inline const NcclApi &nccl() {
     x.commInitRank = (decltype(x.commInitRank))dlsym(h, "ncclCommInitRank");
     x.allReduce = (decltype(x.allReduce))dlsym(h, "ncclAllReduce");
     x.broadcast = (decltype(x.broadcast))dlsym(h, "ncclBroadcast");
+    x.send = (decltype(x.send))dlsym(h, "ncclSend");
+    x.recv = (decltype(x.recv))dlsym(h, "ncclRecv");
     x.groupStart = (decltype(x.groupStart))dlsym(h, "ncclGroupStart");
     x.groupEnd = (decltype(x.groupEnd))dlsym(h, "ncclGroupEnd");
     x.commDestroy = (decltype(x.commDestroy))dlsym(h, "ncclCommDestroy");
@@ -105,6 +112,18 @@ struct NcclComm : Comm {
   }
   void group_begin() override { SG_NCCL(nccl().groupStart()); }
   void group_end() override { SG_NCCL(nccl().groupEnd()); }
+  void alltoallv(const void *send, const size_t *scount, const size_t *sdispl, void *recv,
+                 const size_t *rcount, const size_t *rdispl, CType t, cudaStream_t s) override {
+    const size_t es = ctype_size(t);
+    SG_NCCL(nccl().groupStart());
+    for (int q = 0; q < world; ++q) {
+      if (scount[q])
+        SG_NCCL(nccl().send((const char *)send + sdispl[q] * es, scount[q], dt(t), q, comm, s));
+      if (rcount[q])
+        SG_NCCL(nccl().recv((char *)recv + rdispl[q] * es, rcount[q], dt(t), q, comm, s));
+    }
+    SG_NCCL(nccl().groupEnd());
+  }
 };
 
 // ---------------------------------------------------- threads on one GPU --
@@ -133,6 +152,7 @@ struct ThreadHub {
   int arrived = 0;
   int64_t gen = 0;
   RankPtrs ptrs{};
+  const size_t *scount[kMaxRanks], *sdispl[kMaxRanks];
   bool failed = false;
   explicit ThreadHub(int w) : world(w) {}
   void barrier() {
@@ -177,6 +197,24 @@ struct ThreadComm : Comm {
     }
     hub.barrier();
   }
+  void alltoallv(const void *send, const size_t *scount, const size_t *sdispl, void *recv,
+                 const size_t *rcount, const size_t *rdispl, CType t, cudaStream_t s) override {
+    SG_CUDA(cudaStreamSynchronize(s));
+    hub.ptrs.p[rank] = const_cast<void *>(send);
+    hub.scount[rank] = scount, hub.sdispl[rank] = sdispl;
+    hub.barrier();
+    const size_t es = ctype_size(t);
+    for (int q = 0; q < world; ++q) {  // pull what every peer addressed to this rank
+      const size_t n = hub.scount[q][rank];
+      if (n != rcount[q]) throw Error(SG_ECUDA, "alltoallv: count mismatch");
+      if (n)
+        SG_CUDA(cudaMemcpyAsync((char *)recv + rdispl[q] * es,
+                                (const char *)hub.ptrs.p[q] + hub.sdispl[q][rank] * es, n * es,
+                                cudaMemcpyDeviceToDevice, s));
+    }
+    SG_CUDA(cudaStreamSynchronize(s));
+    hub.barrier();
+  }
   void bcast(void *buf, size_t n, CType t, int root, cudaStream_t s) override {
     SG_CUDA(cudaStreamSynchronize(s));
     hub.ptrs.p[rank] = buf;
@@ -189,5 +227,55 @@ struct ThreadComm : Comm {
     hub.barrier();
   }
 };
+
+// ------------------------------------------------ host-driven dist loops --
+struct DistLoop {  // host-driven rounds with a done-flag read back after each
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  DistLoop() {
+    SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SG_CUDA(cudaEventCreate(&e0));
+    SG_CUDA(cudaEventCreate(&e1));
+  }
+  ~DistLoop() {
+    cudaStreamSynchronize(s);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+  }
+  bool done(const Ctl *ctl) {
+    Ctl h;
+    SG_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    return h.done != 0;
+  }
+};
+
+inline void dist_results(RunBufs &rb, cudaStream_t s, double *labels_d, int64_t nv, sg_round *rounds_out,
+                  int64_t cap, int64_t *nrounds, double *labels_out, int64_t max_rounds) {
+  Ctl h;
+  SG_CUDA(cudaStreamSynchronize(s));
+  SG_CUDA(cudaMemcpy(&h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  const int64_t rounds = h.round;
+  std::vector<RoundStat> st((size_t)std::min<int64_t>(rounds, rb.stats_cap));
+  if (!st.empty())
+    SG_CUDA(cudaMemcpy(st.data(), rb.stats.p, sizeof(RoundStat) * st.size(),
+                       cudaMemcpyDeviceToHost));
+  if (rounds_out && !st.empty())
+    std::memcpy(rounds_out, st.data(),
+                sizeof(RoundStat) * (size_t)std::min<int64_t>(cap, (int64_t)st.size()));
+  *nrounds = rounds;
+  if (labels_out)
+    SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+  if (h.error == SG_ECONVERGE)
+    throw Error(SG_ECONVERGE, "did not converge within " + std::to_string(max_rounds) + " rounds");
+  if (h.error) throw Error(h.error, "round log capacity exhausted");
+}
+
+
+// one rank of the bitmap-frontier push apps (sg_dist_push.cu)
+void run_push_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, Comm &cm,
+                   double *labels_out, sg_round *rounds_out, int64_t cap, int64_t *nrounds,
+                   double *ms_out);
 
 }  // namespace sg

@@ -522,49 +522,6 @@ __global__ void k_dist_kc_advance(PullArgs a, long long *acc, Loop lp) {
   loop_test(ctl, round, stop, lp);
 }
 
-struct DistLoop {  // host-driven rounds with a done-flag read back after each
-  cudaStream_t s = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  DistLoop() {
-    SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    SG_CUDA(cudaEventCreate(&e0));
-    SG_CUDA(cudaEventCreate(&e1));
-  }
-  ~DistLoop() {
-    cudaStreamSynchronize(s);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaStreamDestroy(s);
-  }
-  bool done(const Ctl *ctl) {
-    Ctl h;
-    SG_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    SG_CUDA(cudaStreamSynchronize(s));
-    return h.done != 0;
-  }
-};
-
-void dist_results(RunBufs &rb, cudaStream_t s, double *labels_d, int64_t nv, sg_round *rounds_out,
-                  int64_t cap, int64_t *nrounds, double *labels_out, int64_t max_rounds) {
-  Ctl h;
-  SG_CUDA(cudaStreamSynchronize(s));
-  SG_CUDA(cudaMemcpy(&h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
-  const int64_t rounds = h.round;
-  std::vector<RoundStat> st((size_t)std::min<int64_t>(rounds, rb.stats_cap));
-  if (!st.empty())
-    SG_CUDA(cudaMemcpy(st.data(), rb.stats.p, sizeof(RoundStat) * st.size(),
-                       cudaMemcpyDeviceToHost));
-  if (rounds_out && !st.empty())
-    std::memcpy(rounds_out, st.data(),
-                sizeof(RoundStat) * (size_t)std::min<int64_t>(cap, (int64_t)st.size()));
-  *nrounds = rounds;
-  if (labels_out)
-    SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * nv, cudaMemcpyDeviceToHost));
-  if (h.error == SG_ECONVERGE)
-    throw Error(SG_ECONVERGE, "did not converge within " + std::to_string(max_rounds) + " rounds");
-  if (h.error) throw Error(h.error, "round log capacity exhausted");
-}
-
 void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, Comm &cm,
                  double *labels_out, sg_round *rounds_out, int64_t cap, int64_t *nrounds,
                  double *ms_out) {
@@ -739,8 +696,7 @@ void dist_run_rank(Graph &g, const sg_params &p, Comm &cm, double *labels_out,
   if (g.nv == 0) return;
   if (p.app == SG_APP_PR) return run_pr_dist(g, p, thr, max_rounds, cm, labels_out, rounds_out, cap, nrounds, ms_out);
   if (p.app == SG_APP_KCORE) return run_kcore_dist(g, p, thr, max_rounds, cm, labels_out, rounds_out, cap, nrounds, ms_out);
-  PartRunner R(g, p, thr, max_rounds, cm.world, cm.rank, 1);
-  dispatch_push(R, &cm, labels_out, rounds_out, cap, nrounds, ms_out);
+  run_push_dist(g, p, thr, max_rounds, cm, labels_out, rounds_out, cap, nrounds, ms_out);
 }
 
 }  // namespace

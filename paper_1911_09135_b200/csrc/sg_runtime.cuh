@@ -538,10 +538,11 @@ void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
 // single-device push round with the bitmap next-frontier (sg_bm.cuh)
 template <class Op>
 void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool classic = false,
-              long long *tsum = nullptr) {
+              long long *tsum = nullptr, bool compact = true) {
   if (a.sched == 2) {  // vertex
     c.L.go("push_vertex", k_bm_vertex<Op>, occupancy_grid(k_bm_vertex<Op>, kTB), kTB, c.s, a, op);
-    c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
+    if (compact)
+      c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
     return;
   }
   if (a.sched == 1 || a.sched == 3) {  // lb / edge: prefix over the whole frontier
@@ -556,7 +557,8 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
     else
       c.L.go("push_lb", k_bm_lb<Op, false>, occupancy_grid(k_bm_lb<Op, false>, kTB), kTB, c.s, a,
              op);
-    c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
+    if (compact)
+      c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
     return;
   }
   c.L.go("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
@@ -576,7 +578,8 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
       c.L.go("push_lb", k_bm_lb<Op, false>, occupancy_grid(k_bm_lb<Op, false>, kTB), kTB, c.s, a,
              op);
   }
-  c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
+  if (compact)
+    c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
 }
 
 template <class Op>

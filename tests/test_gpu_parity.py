@@ -249,6 +249,31 @@ def test_nccl_edge_cut_single_rank(sg, golden, app):
         [x[:2] for x in info["per_round"]]
 
 
+@pytest.mark.parametrize("xmode", [0, 1, 2])
+@pytest.mark.parametrize("key", ["lb/d2", "alb/d4", "twc/d2"])
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc"])
+def test_edge_cut_exchange_modes(sg, golden, app, key, xmode):
+    """Push apps over ranks-as-threads with the label exchange forced sparse
+    (owners receive (id, label) of touched mirrors and broadcast changed rows)
+    or dense (all-reduce(min)); labels, rounds and comm counters unchanged."""
+    from paper_1911_09135_b200 import native
+    gname = "rmat12" if key.startswith("alb") else "rmat10"
+    info = golden["runs"][gname][f"{app}/{key}"]
+    g = _graph(sg, gname)
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    world = int(key.split("/d")[1])
+    sched = _sched(sg, "x/" + key.split("/")[0] + "/x")
+    p = sg.engine._device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), world,
+                                 10 * g.num_vertices + 256)
+    p.reserved = xmode
+    labels, log, ms = native.dist_run_threads(g.device(), p, world)
+    assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
+    got = [[int(r["frontier_size"]), int(r["active_edges"]), int(r["comm_sent"]),
+            int(r["comm_broadcast"])] for r in log]
+    assert got == [x[:4] for x in info["per_round"]]
+
+
 @pytest.mark.parametrize("key", ["alb/d2", "alb/d4", "alb/d8", "alb-t256/d2", "alb-t256/d4"])
 @pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
 def test_edge_cut_ranks_as_threads(sg, golden, app, key):
