@@ -131,6 +131,14 @@ void sg_graph_destroy(sg_graph *g);
 int sg_run(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
            int64_t rounds_cap, int64_t *nrounds, double *ms_out);
 
+/* sg_run with hardware load counters: cta_out[r * cta_g + c] = edges processed
+ * by CTA slot c (blockIdx.x of the traversal kernels) in round r, for the first
+ * min(rounds, cta_rounds_cap, 4096) rounds -- the device analogue of the
+ * reference's modeled per_cta_edges (simt.py RoundMetrics).  devices == 1. */
+int sg_run_cta_counts(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
+                      int64_t rounds_cap, int64_t *nrounds, double *ms_out, uint64_t *cta_out,
+                      int64_t cta_rounds_cap, int32_t *cta_g);
+
 typedef struct sg_kernel_time { /* per-kernel totals of a profiled run */
   char name[32];
   int64_t launches;

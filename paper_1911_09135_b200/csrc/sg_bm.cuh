@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
   if (ctl->done) return;
   const uint32_t round = ctl->round;
   op.begin(round);
+  unsigned long long my_proc = 0;
   const Src src = resolve_src(a, ctl);
   const uint32_t lane = lane_id();
   unsigned long long my_edges = 0, my_large = 0;
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
         ok[u] = slot < total;
         e[u] = so + (int64_t)(slot - eo);
       }
+      if (a.cta_edges) my_proc += count_ok(ok);
       op.relax(a, e, ok, svo);
     }
   }
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
   if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
   bs = block_sum(my_large, red);
   if (threadIdx.x == 0 && bs) atomicAdd(&ctl->large_edges, bs);
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // TWC CTA bin: block-level gather over batches of kBatch queued vertices
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   __shared__ int64_t bstart[kBatch];
   __shared__ long long bexcl[kBatch + 1];
   __shared__ L bsv[kBatch];
@@ -294,10 +298,12 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
         e[u] = second ? s1 + (slot - x1) : s0 + (slot - x0);
         svs[u] = second ? v1 : v0;
       }
+      if (a.cta_edges) my_proc += count_ok(ok);
       op.relax(a, e, ok, svs);
     }
     __syncthreads();
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 #ifndef SG_PIPE_V
@@ -316,6 +322,7 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   __shared__ int64_t bstart[kBatch];
   __shared__ long long bexcl[kBatch + 1];
   __shared__ L bsv[kBatch];
@@ -375,12 +382,14 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
         slots(b + step, e, ok1, sv1);
         op.fetch(a, e, ok1, d1, w1);
       }
+      if (a.cta_edges) my_proc += count_ok(ok0);
       op.apply(d0, w0, sv0, ok0);
 #pragma unroll
       for (int u = 0; u < kPV; ++u) d0[u] = d1[u], w0[u] = w1[u], sv0[u] = sv1[u], ok0[u] = more && ok1[u];
     }
     __syncthreads();
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // Classic TWC CTA bin (Merrill; the reference's twc_kernel maps each large
@@ -396,6 +405,7 @@ __global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   for (;;) {
     if (threadIdx.x == 0) item = atomicAdd(&ctl->large_head, 1u);
     __syncthreads();
@@ -416,9 +426,11 @@ __global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
         e[u] = s + slot;
         svs[u] = sv;
       }
+      if (a.cta_edges) my_proc += count_ok(ok);
       op.relax(a, e, ok, svs);
     }
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // ALB huge-vertex kernel (Algorithm 2): every thread of every CTA walks the
@@ -434,6 +446,7 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
   if (!nh) return;
   const int64_t E = (int64_t)ctl->huge_edges;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
@@ -468,8 +481,10 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
         e[u] = second ? s1 + (g - x1) : s0 + (g - x0);
         sv[u] = second ? v1 : v0;
       }
+      if (a.cta_edges) my_proc += count_ok(ok);
       op.relax(a, e, ok, sv);
     }
+    cta_flush(a, my_proc, ctl->round);
     return;
   }
   const bool staged = nh <= kHugeSmem;
@@ -498,8 +513,10 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
         sv[u] = (L)a.hval[o];
       }
     }
+    if (a.cta_edges) my_proc += count_ok(ok);
     op.relax(a, e, ok, sv);
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // ------------------------------------------- the other schedulers (run level)
@@ -512,6 +529,7 @@ __global__ void __launch_bounds__(kTB) k_bm_vertex(PushArgs a, Op op) {
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   const Src src = resolve_src(a, ctl);
   unsigned long long my_edges = 0;
   const uint64_t st = (uint64_t)gridDim.x * kTB;
@@ -532,11 +550,13 @@ __global__ void __launch_bounds__(kTB) k_bm_vertex(PushArgs a, Op op) {
       L svs[kV];
 #pragma unroll
       for (int u = 0; u < kV; ++u) ok[u] = j + u < deg, e[u] = s + j + u, svs[u] = sv;
+      if (a.cta_edges) my_proc += count_ok(ok);
       op.relax(a, e, ok, svs);
     }
   }
   const unsigned long long bs = block_sum(my_edges, red);
   if (threadIdx.x == 0 && bs) atomicAdd(&ctl->edges, bs);
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // lb / edge: the whole frontier as one prefix-summed list (PrefixWork over
@@ -640,6 +660,7 @@ __global__ void __launch_bounds__(kTB) k_bm_edge(PushArgs a, Op op) {
   const int64_t E = (int64_t)ctl->huge_edges;
   if (!nh || !E) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t chunk = (E + T - 1) / T;
@@ -658,8 +679,10 @@ __global__ void __launch_bounds__(kTB) k_bm_edge(PushArgs a, Op op) {
       e[u] = a.hstart[o] + (gg - (o ? a.hpre[o - 1] : 0));
       sv[u] = (L)a.hval[o];
     }
+    if (a.cta_edges) my_proc += count_ok(ok);
     op.relax(a, e, ok, sv);
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // next frontier from the round's bitmap: ids ascending within each warp's

@@ -403,8 +403,14 @@ struct RunResultC {
   double ms = 0;
 };
 
+struct CtaOut {  // SG_FLAG_CTA_COUNTS results
+  uint64_t *host = nullptr;
+  int64_t rounds_cap = 0;
+  int32_t *g = nullptr;
+};
+
 void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out, int64_t cap,
-             int64_t *nrounds, double *ms_out, Launcher *prof) {
+             int64_t *nrounds, double *ms_out, Launcher *prof, const CtaOut *cta = nullptr) {
   if (p.app < SG_APP_BFS || p.app > SG_APP_KCORE) throw Error(SG_ECONFIG, "unknown app");
   if (p.devices < 1) throw Error(SG_ECONFIG, "device count must be >= 1");
   if (g.nv > 0x7fffffffLL) throw Error(SG_ERANGE, "vertex ids must fit int32");
@@ -442,6 +448,7 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
   if (p.app == SG_APP_PR) g.csc();
 
   RunBufs rb;
+  rb.want_cta = cta != nullptr;
   Program P;
   double *labels_d = P.buf<double>(g.nv);
   switch (p.app) {
@@ -492,6 +499,8 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
     }
     Launcher &L = prof ? *prof : plain;
     SG_CUDA(cudaEventRecord(e0, s));
+    if (rb.cta.p)
+      SG_CUDA(cudaMemsetAsync(rb.cta.p, 0, rb.cta.bytes(), s));
     P.init(L, s);
     int64_t rounds = 0;
     if (!prof) {
@@ -531,6 +540,13 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
                   sizeof(RoundStat) * (size_t)std::min<int64_t>(cap, (int64_t)st.size()));
     *nrounds = rounds;
     SG_CUDA(cudaStreamSynchronize(s));
+    if (cta && rb.cta.p) {
+      *cta->g = (int32_t)rb.cta_g;
+      const int64_t r = std::min<int64_t>({rounds, cta->rounds_cap, (int64_t)rb.cta_rounds});
+      if (r > 0)
+        SG_CUDA(cudaMemcpy(cta->host, rb.cta.p, sizeof(uint64_t) * rb.cta_g * r,
+                           cudaMemcpyDeviceToHost));
+    }
     if (labels_out)
       SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * g.nv, cudaMemcpyDeviceToHost));
     if (h.error == SG_ECONVERGE)
@@ -698,6 +714,16 @@ int sg_run(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds
            int64_t rounds_cap, int64_t *nrounds, double *ms_out) {
   return sg::guard([&] {
     sg::run_app(*g->g, *p, labels_out, rounds_out, rounds_cap, nrounds, ms_out, nullptr);
+  });
+}
+
+int sg_run_cta_counts(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,
+                      int64_t rounds_cap, int64_t *nrounds, double *ms_out, uint64_t *cta_out,
+                      int64_t cta_rounds_cap, int32_t *cta_g) {
+  return sg::guard([&] {
+    if (p->devices != 1) throw Error(SG_ECONFIG, "per-CTA counters need devices == 1");
+    sg::CtaOut co{cta_out, cta_rounds_cap, cta_g};
+    sg::run_app(*g->g, *p, labels_out, rounds_out, rounds_cap, nrounds, ms_out, nullptr, &co);
   });
 }
 

@@ -35,6 +35,8 @@ struct PullArgs {
   const uint32_t *mcount;   // mirror_count per vertex (devices > 1), else nullptr
   uint32_t row_lo, row_n;   // a dense round covers rows [row_lo, row_lo + row_n)
   int vertex;               // vertex scheduler: k_pull_vertex instead of the bins
+  unsigned long long *cta_edges;  // SG_FLAG_CTA_COUNTS (see PushArgs)
+  uint32_t cta_g, cta_rounds;
 };
 
 // pr: acc = sum aux[u]; new = (1-d) + d*acc (two roundings, as numpy); aux' = new*inv
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
   if (ctl->done) return;
   const uint32_t round = ctl->round;
   op.begin(round);
+  unsigned long long my_proc = 0;
   const bool dense = !a.dynamic_bins || ctl->dense;
   const uint32_t n = dense ? a.row_n : ctl->fsize;
   const uint32_t *list = (round & 1) ? a.q[1] : a.q[0];
@@ -176,8 +179,10 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
         src[u] = slot < total ? ld_stream(a.col + so + (slot - eo)) : 0xffffffffu;
       }
 #pragma unroll
-      for (int u = 0; u < KP; ++u)  // then KP value gathers in flight
+      for (int u = 0; u < KP; ++u) {  // then KP value gathers in flight
         x[u] = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+        my_proc += src[u] != 0xffffffffu;
+      }
 #pragma unroll
       for (int u = 0; u < KP; ++u) {
         const uint32_t cb = base + u * 32;
@@ -210,7 +215,10 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
           src[u] = j < md ? ld_stream(a.col + ms + j) : 0xffffffffu;
         }
 #pragma unroll
-        for (int u = 0; u < kV; ++u) x += src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+        for (int u = 0; u < kV; ++u) {
+          x += src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
+          my_proc += src[u] != 0xffffffffu;
+        }
       }
       x = __shfl_sync(kFull, warp_sum(x), l);  // lane l's butterfly: a fixed order
       if (lane == (uint32_t)l) acc = x;
@@ -238,6 +246,7 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
       if (lane == 0 && b) atomicAdd(&ctl->comm_bcast, b);
     }
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // vertex scheduler (_kernels_py.py:88-97): one thread folds one row
@@ -249,6 +258,7 @@ __global__ void __launch_bounds__(kTB) k_pull_vertex(PullArgs a, Op op) {
   if (ctl->done) return;
   const uint32_t round = ctl->round;
   op.begin(round);
+  unsigned long long my_proc = 0;
   const bool dense = !a.dynamic_bins || ctl->dense;
   const uint32_t n = dense ? a.row_n : ctl->fsize;
   const uint32_t *list = (round & 1) ? a.q[1] : a.q[0];
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(kTB) k_pull_vertex(PullArgs a, Op op) {
       v = dense ? a.row_lo + (uint32_t)i : list[i];
       const int64_t s = a.off[v], e = a.off[v + 1];
       my_edges += (unsigned long long)(e - s);
+      my_proc += (unsigned long long)(e - s);
       typename Op::A acc = 0;
       for (int64_t j = s; j < e; j += 4) {
         typename Op::A x[4];
@@ -291,6 +302,7 @@ __global__ void __launch_bounds__(kTB) k_pull_vertex(PullArgs a, Op op) {
       if (lane_id() == 0 && b) atomicAdd(&ctl->comm_bcast, b);
     }
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // TWC CTA bin: edge-balanced batches of kBatch rows (degree-mixed, dynamic
@@ -312,6 +324,7 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t nb = (n + kBatch - 1) / kBatch;
   for (;;) {
@@ -361,6 +374,7 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
 #pragma unroll
       for (int u = 0; u < kV; ++u) {
         const A y = src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
+        my_proc += src[u] != 0xffffffffu;
         if (sec[u]) xb += y;
         else xa += y;
       }
@@ -398,6 +412,7 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
     const unsigned long long bc = warp_sum(op.bcast);
     if (lane == 0 && bc) atomicAdd(&ctl->comm_bcast, bc);
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // Classic TWC CTA bin for the TWC-only ablation (SG_FLAG_TWC_CLASSIC): one
@@ -412,6 +427,7 @@ __global__ void __launch_bounds__(kTB) k_pull_large_classic(PullArgs a, Op op) {
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   for (;;) {
     if (threadIdx.x == 0) item = atomicAdd(&ctl->large_head, 1u);
     __syncthreads();
@@ -426,13 +442,17 @@ __global__ void __launch_bounds__(kTB) k_pull_large_classic(PullArgs a, Op op) {
 #pragma unroll
       for (int u = 0; u < kV; ++u) src[u] = b + u * kTB < e ? ld_stream(a.col + b + u * kTB) : 0xffffffffu;
 #pragma unroll
-      for (int u = 0; u < kV; ++u) x += src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
+      for (int u = 0; u < kV; ++u) {
+        x += src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
+        my_proc += src[u] != 0xffffffffu;
+      }
     }
     x = block_sum(x, red);
     if (threadIdx.x == 0 && op.finish(v, x)) a.dying[atomicAdd(&ctl->ndying, 1u)] = v;
   }
   if (sizeof(A) == 8 && threadIdx.x == 0 && op.dmax > 0) atomic_max_dbits(&ctl->delta_bits, op.dmax);
   if (threadIdx.x == 0 && op.bcast) atomicAdd(&ctl->comm_bcast, op.bcast);
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // PrefixWork of the huge rows (no labels needed for pull)
@@ -475,6 +495,7 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
   const uint32_t nh = ctl->nhuge;
   if (!nh) return;
   op.begin(ctl->round);
+  unsigned long long my_proc = 0;
   const int64_t E = (int64_t)ctl->huge_edges;
   const int64_t *pre = a.hpre;
   if (nh <= kHugeSmem) {
@@ -509,6 +530,7 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
       typename Op::A xa = 0, xb = 0;
 #pragma unroll
       for (int u = 0; u < kV; ++u) {
+        my_proc += src[u] != 0xffffffffu;
         const typename Op::A y = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
         if (sec[u]) xb += y;
         else xa += y;
@@ -520,6 +542,7 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
         if (x1 < g0 + CH && x1 < E) atomicAdd(hacc + o + 1, xb);
       }
     }
+    cta_flush(a, my_proc, ctl->round);
     return;
   }
   for (int64_t p0 = 0; p0 < passes; p0 += kU) {
@@ -538,7 +561,10 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) x[u] = o[u] >= 0 ? op.load(src[u]) : typename Op::A(0);
+    for (int u = 0; u < kU; ++u) {
+      x[u] = o[u] >= 0 ? op.load(src[u]) : typename Op::A(0);
+      my_proc += o[u] >= 0;
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
 #pragma unroll
@@ -552,6 +578,7 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
       if (o[u] >= 0 && last) atomicAdd(hacc + o[u], x[u]);
     }
   }
+  cta_flush(a, my_proc, ctl->round);
 }
 
 // tiled pr: per-block static bin counts {nhuge, huge_edges, nlarge, large_edges}

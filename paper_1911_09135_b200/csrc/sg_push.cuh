@@ -59,7 +59,24 @@ struct PushArgs {
   int no_enqueue;         // partitioned runs: frontiers come from the label exchange
   int sched;              // 0 alb / twc, 1 lb, 2 vertex, 3 edge (round-log launch accounting)
   uint32_t dense_lo, dense_n;  // a dense frontier is [dense_lo, dense_lo + dense_n)
+  // SG_FLAG_CTA_COUNTS: edges processed per CTA per round ([round][cta_g]), the
+  // hardware analogue of the reference's modeled per-CTA counters
+  unsigned long long *cta_edges;
+  uint32_t cta_g, cta_rounds;
 };
+
+template <class Args>
+__device__ __forceinline__ void cta_flush(const Args &a, unsigned long long n, uint32_t round) {
+  if (a.cta_edges && n && round < a.cta_rounds)
+    atomicAdd(a.cta_edges + (size_t)round * a.cta_g + blockIdx.x, n);
+}
+template <int N>
+__device__ __forceinline__ unsigned count_ok(const bool (&ok)[N]) {
+  unsigned c = 0;
+#pragma unroll
+  for (int u = 0; u < N; ++u) c += ok[u];
+  return c;
+}
 
 __device__ __forceinline__ uint32_t *next_queue(const PushArgs &a, uint32_t round) {
   return a.no_enqueue ? nullptr : ((round & 1) ? a.q[0] : a.q[1]);

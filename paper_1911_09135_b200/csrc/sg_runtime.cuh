@@ -447,9 +447,18 @@ struct RunBufs {
   DBuf<uint32_t> q0, q1, largeq, hugeq, dying;
   DBuf<int64_t> hpre, hstart;
   DBuf<unsigned long long> hval, largesv;
+  // SG_FLAG_CTA_COUNTS: per-CTA processed edges of the first cta_rounds rounds
+  bool want_cta = false;
+  DBuf<unsigned long long> cta;
+  uint32_t cta_g = 0, cta_rounds = 0;
 
   void alloc_common(int64_t nv, int64_t rounds_cap) {
     size_t n = (size_t)std::max<int64_t>(nv, 1);
+    if (want_cta) {
+      cta_g = (uint32_t)persistent_grid(8);  // >= every traversal kernel's grid
+      cta_rounds = (uint32_t)std::min<int64_t>(rounds_cap, 4096);
+      cta.alloc((size_t)cta_g * cta_rounds);
+    }
     // no memset here: every driver zeroes the block with k_ctl_init on its own
     // (non-blocking) stream; a legacy-stream memset is NOT ordered before that
     // and could land after it (seen as a lost dense frontier with ranks as threads)
@@ -476,6 +485,7 @@ struct RunBufs {
     a.no_enqueue = 0;
     a.dense_lo = 0;
     a.dense_n = (uint32_t)v.nv;
+    a.cta_edges = cta.p, a.cta_g = cta_g, a.cta_rounds = cta_rounds;
     return a;
   }
   PullArgs pull_args(const View &v, int64_t thr, int dyn) {
@@ -493,6 +503,7 @@ struct RunBufs {
     a.stats = stats.p;
     a.row_lo = 0;
     a.row_n = (uint32_t)v.nv;
+    a.cta_edges = cta.p, a.cta_g = cta_g, a.cta_rounds = cta_rounds;
     return a;
   }
 };

@@ -29,7 +29,7 @@ EXPORTS = (
     "sg_graph_download", "sg_graph_view_size", "sg_graph_destroy", "sg_run", "sg_run_profiled",
     "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run", "sg_dist_run_threads",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
-    "sg_host_alloc", "sg_host_free", "sg_release_cached",
+    "sg_host_alloc", "sg_host_free", "sg_release_cached", "sg_run_cta_counts",
 )
 
 
@@ -95,6 +95,8 @@ def load(path: Path | None = None):
                             ctypes.c_int),
             "sg_dist_run_threads": ([P, ctypes.POINTER(Params), i32, P, P, i64, P, P],
                                     ctypes.c_int),
+            "sg_run_cta_counts": ([P, ctypes.POINTER(Params), P, P, i64, P, P, P, i64, P],
+                                  ctypes.c_int),
             "sg_host_alloc": ([i64, pp], ctypes.c_int),
             "sg_host_free": ([P], None),
             "sg_release_cached": ([], None),
@@ -268,6 +270,23 @@ class DeviceGraph:
                        for i in range(nkt.value)}
             return labels, log, ms.value, kernels
         return labels, log, ms.value
+
+    def run_cta_counts(self, params: Params, rounds_cap=1 << 16, cta_rounds=512):
+        """sg_run with hardware load counters: (labels, log, ms, cta) where
+        cta[r, c] = edges processed by CTA slot c in round r (first cta_rounds)."""
+        nv, _, _ = self.info()
+        labels = pinned_empty(nv, np.float64)
+        rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
+        n = ctypes.c_int64(0)
+        ms = ctypes.c_double(0.0)
+        g = ctypes.c_int32(0)
+        cta = np.zeros(cta_rounds * 4096, dtype=np.uint64)  # room for <= 512 SMs x 8 CTAs
+        check(load().sg_run_cta_counts(self.handle, ctypes.byref(params), ptr(labels),
+                                       ptr(rounds), rounds_cap, ctypes.byref(n),
+                                       ctypes.byref(ms), ptr(cta), cta_rounds, ctypes.byref(g)))
+        log = rounds[: min(n.value, rounds_cap)].copy()
+        r = min(len(log), cta_rounds)
+        return labels, log, ms.value, cta[: r * g.value].reshape(r, g.value).astype(np.int64)
 
 
 def nccl_unique_id() -> bytes:

@@ -323,3 +323,26 @@ def test_pr_tiling_thresholds(sg):
         labels, log, ms = g.device().run(p)
         assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
         assert len(log) == len(ref.records)
+
+
+@pytest.mark.parametrize("sched", ["alb", "twc", "lb", "vertex", "edge"])
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
+def test_hardware_cta_counters(sg, app, sched):
+    """sg_run_cta_counts: every round's per-CTA processed edges add up to the
+    reference's active_edges (each operator application counted exactly once
+    on the hardware), labels unchanged."""
+    g = _graph(sg, "rmat14")
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    s = sg.Scheduler(sched, threshold=256 if sched == "alb" else None)
+    res = sg.run_app(g, app, s, hardware_counters=True)
+    ref = sg.run_app(g, app, s)
+    for rec in res.records:
+        assert len(rec.metrics[0].per_cta_edges) >= 148
+        assert int(rec.metrics[0].per_cta_edges.sum()) == rec.active_edges()
+    if app == "pr":
+        assert np.max(np.abs(res.labels - ref.labels)) <= PR_ATOL
+    else:
+        assert sg.engine.labels_sha256(res.labels) == sg.engine.labels_sha256(ref.labels)
+    rep = sg.report(res)
+    assert rep["load"]["worst_cta_max_mean"] >= 1.0
