@@ -434,8 +434,8 @@ def main():
                                  "classic_cta_bin": {"alb_gteps": alb_c, "twc_gteps": tw_c,
                                                      "alb_over_twc": alb_c / tw_c}}
 
-    # hardware CTA load balance (paper Fig. 1 / 7 analogue): per-round edges per
-    # CTA slot from sg_run_cta_counts, worst round's max/mean and CV
+    # hardware load balance (paper Fig. 1 / 7 analogue): per-round edges per SM
+    # from sg_run_cta_counts, worst round's max/mean and CV
     if rank == 0 and world == 1 and not a.no_ablation:
         def cta_load(kind, classic):
             _, lg, _, cta = dev.run_cta_counts(run_params(sg, a.app, kind, a.threshold, nv,
@@ -449,7 +449,7 @@ def main():
                 if mm > worst_mm:
                     worst_mm, worst_cv, heavy = mm, cv, r
             return {"worst_round": heavy, "max_over_mean": round(worst_mm, 3),
-                    "cv": round(worst_cv, 3), "ctas": int(cta.shape[1]) if len(cta) else 0}
+                    "cv": round(worst_cv, 3), "sms": int(cta.shape[1]) if len(cta) else 0}
         ablation.setdefault(a.app, {})["cta_load"] = {
             "alb": cta_load("alb", False), "twc": cta_load("twc", False),
             "alb_classic_cta_bin": cta_load("alb", True), "twc_classic": cta_load("twc", True)}

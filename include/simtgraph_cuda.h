@@ -132,7 +132,7 @@ int sg_run(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds
            int64_t rounds_cap, int64_t *nrounds, double *ms_out);
 
 /* sg_run with hardware load counters: cta_out[r * cta_g + c] = edges processed
- * by CTA slot c (blockIdx.x of the traversal kernels) in round r, for the first
+ * by the CTAs that ran on SM c (cta_g = SM count) in round r, for the first
  * min(rounds, cta_rounds_cap, 4096) rounds -- the device analogue of the
  * reference's modeled per_cta_edges (simt.py RoundMetrics).  devices == 1. */
 int sg_run_cta_counts(sg_graph *g, const sg_params *p, double *labels_out, sg_round *rounds_out,

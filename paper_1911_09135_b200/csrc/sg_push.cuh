@@ -65,10 +65,17 @@ struct PushArgs {
   uint32_t cta_g, cta_rounds;
 };
 
+// counters are kept per SM (the slot a CTA ran on): the persistent grids of
+// the round's kernels differ in size, SMs are the fixed resource they share
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 template <class Args>
 __device__ __forceinline__ void cta_flush(const Args &a, unsigned long long n, uint32_t round) {
   if (a.cta_edges && n && round < a.cta_rounds)
-    atomicAdd(a.cta_edges + (size_t)round * a.cta_g + blockIdx.x, n);
+    atomicAdd(a.cta_edges + (size_t)round * a.cta_g + (sm_id() % a.cta_g), n);
 }
 template <int N>
 __device__ __forceinline__ unsigned count_ok(const bool (&ok)[N]) {

@@ -455,7 +455,7 @@ struct RunBufs {
   void alloc_common(int64_t nv, int64_t rounds_cap) {
     size_t n = (size_t)std::max<int64_t>(nv, 1);
     if (want_cta) {
-      cta_g = (uint32_t)persistent_grid(8);  // >= every traversal kernel's grid
+      cta_g = (uint32_t)sm_info().sms;  // one slot per SM
       cta_rounds = (uint32_t)std::min<int64_t>(rounds_cap, 4096);
       cta.alloc((size_t)cta_g * cta_rounds);
     }
