@@ -78,6 +78,12 @@ typedef struct sg_params {
 #define SG_FLAG_TWC_CLASSIC 4 /* TWC CTA bin = one vertex per CTA (the reference's
                                  twc_kernel mapping, _kernels_py.py:140-146) instead of
                                  edge-balanced batches; for the TWC-only ablation */
+#define SG_FLAG_RELABEL 8     /* run on the hot-vertex relabeled store (sg_graph.cuh
+                                 Relabel): the highest-degree vertices take the low ids
+                                 so their labels share L1 lines; labels are mapped back */
+#define SG_FLAG_NO_RELABEL 16 /* never relabel.  Neither flag: relabel when devices == 1,
+                                 the graph has >= 2^20 vertices and it has been run
+                                 before (the build is amortised over repeated runs) */
 
 typedef struct sg_round { /* one BSP round (engine.py:116-163) */
   int64_t frontier_size;  /* RoundRecord.frontier_size */

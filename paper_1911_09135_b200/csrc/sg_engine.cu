@@ -9,6 +9,7 @@
 // times for the roofline report).  Results: float64 labels + one RoundStat
 // per round (frontier size, active edges, ... == RoundRecord).
 
+#include <cstdlib>
 #include "sg_runtime.cuh"
 
 
@@ -137,8 +138,28 @@ const SmInfo &sm_info() {
 namespace sg {
 namespace {
 
+// old id of every vertex of a relabeled store (nullptr: identity); cc's initial
+// labels are the vertex ids of the reference's numbering (apps.py:121-124)
+struct Layout {
+  const uint32_t *perm = nullptr;  // new -> old
+  const uint32_t *inv = nullptr;   // old -> new
+};
+
+__global__ void k_copy_u32(const uint32_t *__restrict__ a, int64_t n, uint32_t *__restrict__ b) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) b[i] = a[i];
+}
+
+// labels back to the reference's numbering: out[v] = lab[inv[v]]
+__global__ void k_unpermute(const double *__restrict__ lab, const uint32_t *__restrict__ inv,
+                            int64_t n, double *__restrict__ out) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = lab[inv[i]];
+}
+
 void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d,
-                   int64_t thr, int64_t max_rounds) {
+                   int64_t thr, int64_t max_rounds, const Layout &lay) {
   const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const bool cc = p.app == SG_APP_CC;
   const View &v = cc ? g.sym() : g.csr;
@@ -189,12 +210,16 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
     use32 = g.w32.p != nullptr && bound < 4294967295.0;
   }
   uint32_t *nb = P.buf<uint32_t>(nw);
+  const uint32_t *perm = lay.perm;
   if (use32) {
     uint32_t *lab = P.buf<uint32_t>(nv), *snap = P.buf<uint32_t>(nv);
     P.init = [=](Launcher &L, cudaStream_t s) {
       init_ctl(L, s);
       fill<uint32_t>(L, nb, nw, 0u, s);
-      if (cc) {
+      if (cc && perm) {
+        L.go("init", k_copy_u32, grid_n(nv), 256, s, perm, nv, lab);
+        L.go("init", k_copy_u32, grid_n(nv), 256, s, perm, nv, snap);
+      } else if (cc) {
         L.go("init", k_iota, grid_n(nv), 256, s, lab, nv);
         L.go("init", k_iota, grid_n(nv), 256, s, snap, nv);  // dense round 0: snap[i] = i
       } else {
@@ -409,8 +434,9 @@ struct CtaOut {  // SG_FLAG_CTA_COUNTS results
   int32_t *g = nullptr;
 };
 
-void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out, int64_t cap,
-             int64_t *nrounds, double *ms_out, Launcher *prof, const CtaOut *cta = nullptr) {
+void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out,
+                int64_t cap, int64_t *nrounds, double *ms_out, Launcher *prof, const CtaOut *cta,
+                const Layout &lay) {
   if (p.app < SG_APP_BFS || p.app > SG_APP_KCORE) throw Error(SG_ECONFIG, "unknown app");
   if (p.devices < 1) throw Error(SG_ECONFIG, "device count must be >= 1");
   if (g.nv > 0x7fffffffLL) throw Error(SG_ERANGE, "vertex ids must fit int32");
@@ -454,7 +480,7 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
   switch (p.app) {
     case SG_APP_BFS:
     case SG_APP_SSSP:
-    case SG_APP_CC: prep_push_min(P, g, p, rb, labels_d, thr, max_rounds); break;
+    case SG_APP_CC: prep_push_min(P, g, p, rb, labels_d, thr, max_rounds, lay); break;
     case SG_APP_PR: prep_pr(P, g, p, rb, labels_d, thr, max_rounds); break;
     case SG_APP_KCORE: prep_kcore(P, g, p, rb, labels_d, thr, max_rounds); break;
   }
@@ -547,8 +573,14 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
         SG_CUDA(cudaMemcpy(cta->host, rb.cta.p, sizeof(uint64_t) * rb.cta_g * r,
                            cudaMemcpyDeviceToHost));
     }
-    if (labels_out)
+    if (labels_out && lay.inv) {
+      double *tmp = P.buf<double>(g.nv);
+      SG_LAUNCH(k_unpermute, grid_n(g.nv), 256, 0, s, labels_d, lay.inv, g.nv, tmp);
+      SG_CUDA(cudaMemcpyAsync(labels_out, tmp, sizeof(double) * g.nv, cudaMemcpyDeviceToHost, s));
+      SG_CUDA(cudaStreamSynchronize(s));
+    } else if (labels_out) {
       SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * g.nv, cudaMemcpyDeviceToHost));
+    }
     if (h.error == SG_ECONVERGE)
       throw Error(SG_ECONVERGE, "did not converge within " + std::to_string(max_rounds) + " rounds");
     if (h.error)
@@ -558,6 +590,55 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
     throw;
   }
   cleanup();
+}
+
+// Hot-set size of the relabeled store (measured on rmat24, scripts/hotk_sweep.py):
+// push apps gather labels of u32: the top 2^16 vertices (256 KB, about one
+// SM's L1) first and the rest in id order is best (sssp +7 %, cc +7 %, bfs
+// +4 %; a full degree order loses part of it again); pull apps (pr, kcore)
+// gather over the whole vertex range every round and gain most from a full
+// degree order (pr +15 %, kcore +16 %).  SG_HOT_K overrides (tuning runs).
+int64_t hot_k(int64_t nv, int32_t app) {
+  static const int64_t env = [] {
+    const char *e = std::getenv("SG_HOT_K");
+    return e ? std::atoll(e) : (int64_t)-1;
+  }();
+  const bool pull = app == SG_APP_PR || app == SG_APP_KCORE;
+  const int64_t K = env >= 0 ? env : pull ? nv : (int64_t)1 << 16;
+  return K > nv ? nv : K;
+}
+
+constexpr int64_t kRelabelMinV = (int64_t)1 << 20;
+
+// Automatic choice: relabel graphs of >= 2^20 vertices on one device, from the
+// graph's second run on.  Building the relabeled store (degree sort + one
+// renaming pass over the CSR: ~15 ms at rmat24, sg_graph.cu) costs more than
+// one push run gains, so a graph that is created, run once and dropped (the
+// e2e path) keeps its original numbering; resident graphs that are run again
+// amortise it at once.
+bool use_relabel(Graph &g, const sg_params &p) {
+  if (p.devices != 1 || (p.flags & SG_FLAG_NO_RELABEL) || g.nv == 0) return false;
+  if (p.flags & SG_FLAG_RELABEL) return true;
+  return g.nv >= kRelabelMinV && g.runs++ >= 1;
+}
+
+void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out, int64_t cap,
+             int64_t *nrounds, double *ms_out, Launcher *prof, const CtaOut *cta = nullptr) {
+  if (!use_relabel(g, p)) {
+    run_app_on(g, p, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta, Layout{});
+    return;
+  }
+  // the relabeled store is built once per graph (cached like csc / sym) and
+  // is not timed; the source is renamed in, the labels renamed out
+  Relabel &R = g.hot(hot_k(g.nv, p.app));
+  sg_params q = p;
+  if ((p.app == SG_APP_BFS || p.app == SG_APP_SSSP) && p.source >= 0 && p.source < g.nv) {
+    uint32_t s = 0;
+    SG_CUDA(cudaMemcpy(&s, R.inv.p + p.source, sizeof(s), cudaMemcpyDeviceToHost));
+    q.source = s;
+  }
+  run_app_on(*R.g, q, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta,
+             Layout{R.perm.p, R.inv.p});
 }
 
 }  // namespace

@@ -7,6 +7,8 @@
 //                 concat(src,dst) by source yields exactly that order)
 //   generate_rmat / attach_random_weights: numpy PCG64 streams (graph.py:274-305)
 // The LSD radix sort (CUB) is stable, which is what makes these identical.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -138,6 +140,11 @@ __global__ void k_weights(int64_t ne, uint64_t s_hi, uint64_t s_lo, uint64_t i_h
   };
   w[2 * pair] = scale(lo);
   if (2 * pair + 1 < ne) w[2 * pair + 1] = scale(hi);
+}
+
+__global__ void k_fill_u32(uint32_t *__restrict__ p, int64_t n, uint32_t x) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = x;
 }
 
 __global__ void k_w32(const int64_t *__restrict__ w, int64_t ne, uint32_t *__restrict__ o) {
@@ -338,6 +345,131 @@ const Tiles &Graph::tiles(int64_t S) {
   }
   tiles_ = std::move(t);
   return *tiles_;
+}
+
+namespace {
+__global__ void k_indeg(const uint32_t *__restrict__ col, int64_t ne, uint32_t *__restrict__ cnt) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += st)
+    atomicAdd(cnt + col[i], 1u);
+}
+// key[v] = total degree (saturating), ids[v] = v
+__global__ void k_degkey(const int64_t *__restrict__ off, const uint32_t *indeg, int64_t nv,
+                         uint32_t *key, uint32_t *__restrict__ ids) {  // key may alias indeg
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st) {
+    const uint64_t d = (uint64_t)(off[v + 1] - off[v]) + indeg[v];
+    key[v] = (uint32_t)(d < 0xffffffffull ? d : 0xffffffffull);
+    ids[v] = (uint32_t)v;
+  }
+}
+// the top-K (sorted) ids take [0, K); flag them
+__global__ void k_hot_place(const uint32_t *__restrict__ sorted, int64_t K,
+                            uint32_t *__restrict__ perm, uint32_t *__restrict__ cold) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += st) {
+    perm[i] = sorted[i];
+    cold[sorted[i]] = 0u;
+  }
+}
+// every other vertex after them, in id order: new id = K + #cold vertices before v
+__global__ void k_cold_place(const uint32_t *__restrict__ cold, const uint32_t *__restrict__ rank,
+                             int64_t nv, int64_t K, uint32_t *__restrict__ perm) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st)
+    if (cold[v]) perm[K + rank[v]] = (uint32_t)v;
+}
+__global__ void k_invert(const uint32_t *__restrict__ perm, int64_t nv, uint32_t *__restrict__ inv) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += st)
+    inv[perm[i]] = (uint32_t)i;
+}
+__global__ void k_perm_len(const int64_t *__restrict__ off, const uint32_t *__restrict__ perm,
+                           int64_t nv, int64_t *__restrict__ len) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += st) {
+    const uint32_t v = perm[i];
+    len[i] = off[v + 1] - off[v];
+  }
+}
+// new row i = old row perm[i] with its targets renamed (row order kept); warp per row
+__global__ void k_perm_rows(const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
+                            const int64_t *__restrict__ w64, const uint32_t *__restrict__ w32,
+                            const uint32_t *__restrict__ perm, const uint32_t *__restrict__ inv,
+                            const int64_t *__restrict__ noff, int64_t nv,
+                            uint32_t *__restrict__ ncol, int64_t *__restrict__ nw64,
+                            uint32_t *__restrict__ nw32) {
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nv; i += warps) {
+    const uint32_t v = perm[i];
+    const int64_t s = off[v], n = off[v + 1] - s, o = noff[i];
+    for (int64_t j = lane_id(); j < n; j += 32) {
+      ncol[o + j] = inv[col[s + j]];
+      if (nw64) nw64[o + j] = w64[s + j];
+      if (nw32) nw32[o + j] = w32[s + j];
+    }
+  }
+}
+}  // namespace
+
+Relabel &Graph::hot(int64_t K) {
+  K = std::max<int64_t>(0, std::min(K, nv));
+  auto it = hot_.find(K);
+  if (it != hot_.end()) return *it->second;
+  auto R = std::make_unique<Relabel>();
+  R->K = K;
+  R->perm.alloc(nv ? nv : 1);
+  R->inv.alloc(nv ? nv : 1);
+  auto h = std::make_unique<Graph>();
+  h->nv = nv, h->ne = ne;
+  h->csr.nv = nv, h->csr.ne = ne;
+  h->csr.off.alloc(nv + 1);
+  h->csr.col.alloc(ne ? ne : 1);
+  if (nv) {
+    DBuf<uint32_t> a(nv), b(nv), c(nv), d(nv);  // indeg/key, ids, sorted keys, sorted ids
+    SG_CUDA(cudaMemset(a.p, 0, sizeof(uint32_t) * nv));
+    if (ne) SG_LAUNCH(k_indeg, grid_for(ne), 256, 0, 0, csr.col.p, ne, a.p);
+    SG_LAUNCH(k_degkey, grid_for(nv), 256, 0, 0, csr.off.p, a.p, nv, a.p, b.p);
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, a.p, c.p, b.p, d.p, nv));
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, a.p, b.p, nv));
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, (int64_t *)nullptr, (int64_t *)nullptr,
+                                          nv + 1));
+    DBuf<char> t(std::max({t1, t2, t3}));
+    // stable: equal degrees keep ascending ids
+    SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, t1, a.p, c.p, b.p, d.p, nv));
+    g_launches.fetch_add(1);
+    // a = cold flags, b = rank among cold vertices
+    SG_LAUNCH(k_fill_u32, grid_for(nv), 256, 0, 0, a.p, nv, 1u);
+    if (K) SG_LAUNCH(k_hot_place, grid_for(K), 256, 0, 0, d.p, K, R->perm.p, a.p);
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, t2, a.p, b.p, nv));
+    SG_LAUNCH(k_cold_place, grid_for(nv), 256, 0, 0, a.p, b.p, nv, K, R->perm.p);
+    SG_LAUNCH(k_invert, grid_for(nv), 256, 0, 0, R->perm.p, nv, R->inv.p);
+    DBuf<int64_t> len(nv + 1);
+    SG_LAUNCH(k_perm_len, grid_for(nv), 256, 0, 0, csr.off.p, R->perm.p, nv, len.p);
+    SG_CUDA(cudaMemset(len.p + nv, 0, sizeof(int64_t)));
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, t3, len.p, h->csr.off.p, nv + 1));
+    // weights: the u32 copy the kernels stream, plus int64 only where a run
+    // may need the float64-bit path (no u32 copy, or u32 path sums may overflow)
+    const bool want64 =
+        weighted && (!w32.p || (double)wmax * (double)std::max<int64_t>(nv - 1, 1) >= 4294967295.0);
+    if (weighted) {
+      h->weighted = true, h->wmin = wmin, h->wmax = wmax;
+      if (w32.p) h->w32.alloc(ne ? ne : 1);
+      h->w64.alloc(want64 && ne ? ne : 1);
+    }
+    SG_LAUNCH(k_perm_rows, grid_for(nv * 32), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
+              R->perm.p, R->inv.p, h->csr.off.p, nv, h->csr.col.p,
+              want64 ? h->w64.p : nullptr, weighted && w32.p ? h->w32.p : nullptr);
+    SG_CUDA(cudaDeviceSynchronize());
+  } else {
+    SG_CUDA(cudaMemset(h->csr.off.p, 0, sizeof(int64_t)));
+    if (weighted) h->weighted = true, h->w64.alloc(1);
+  }
+  R->g = std::move(h);
+  Relabel &out = *R;
+  hot_[K] = std::move(R);
+  return out;
 }
 
 const View &Graph::csc() {

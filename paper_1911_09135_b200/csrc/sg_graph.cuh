@@ -1,5 +1,6 @@
 // sg_graph.cuh — the HBM-resident graph store (reference graph.py:29-177).
 #pragma once
+#include <map>
 #include <memory>
 
 #include "sg_common.cuh"
@@ -24,6 +25,8 @@ struct Tiles {
   std::vector<View> blk;
 };
 
+struct Relabel;
+
 struct Graph {
   int64_t nv = 0, ne = 0;
   View csr;
@@ -43,6 +46,27 @@ struct Graph {
   double source_coverage(int64_t K);
   int64_t cov_k_ = -1;
   double cov_ = 0.0;
+  // hot-vertex relabelings of this graph (built lazily, cached per K; see Relabel)
+  std::map<int64_t, std::unique_ptr<Relabel>> hot_;
+  Relabel &hot(int64_t K);
+  int64_t runs = 0;  // single-device runs on this graph (the relabeling is built from the 2nd)
+};
+
+// Hot-vertex relabeling: the kernel-side layout of the store.  The K vertices
+// of highest total degree (out + in; ties by id) take ids [0, K) in
+// descending-degree order and every other vertex keeps its relative order
+// after them.  Their labels then share cache lines, so one SM's L1 holds the
+// labels most random accesses hit (a scattered 4-byte gather that misses L1 is
+// one L1->L2 request; the request path is what bounds the push kernels, ncu).
+// The same permutation serves every view: total degree is the row length of
+// the symmetrized graph, and the CSC / sym of the relabeled CSR are built from
+// it.  Labels are invariant under renaming (BSP rounds touch the same vertex
+// sets), so runs map the source in and the labels back out (sg_engine.cu).
+struct Relabel {
+  int64_t K = 0;
+  DBuf<uint32_t> perm;       // new id -> old id
+  DBuf<uint32_t> inv;        // old id -> new id
+  std::unique_ptr<Graph> g;  // the relabeled CSR (+ weights, w32)
 };
 
 // builders (sg_graph.cu)

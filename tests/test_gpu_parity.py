@@ -346,3 +346,86 @@ def test_hardware_cta_counters(sg, app, sched):
         assert sg.engine.labels_sha256(res.labels) == sg.engine.labels_sha256(ref.labels)
     rep = sg.report(res)
     assert rep["load"]["worst_cta_max_mean"] >= 1.0
+
+
+# ------------------------------------------------ hot-vertex relabeled store
+SG_FLAG_RELABEL, SG_FLAG_NO_RELABEL = 8, 16
+
+
+def _run_flags(sg, g, app, sched, flags, devices=1):
+    p = sg.engine._device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), devices,
+                                 10 * g.num_vertices + 256)
+    p.flags |= flags
+    labels, log, _ = g.device().run(p)
+    return labels, [[int(r["frontier_size"]), int(r["active_edges"])] for r in log]
+
+
+def _relabel_keys():
+    import json
+    from pathlib import Path
+    runs = json.loads((Path(__file__).parent / "golden" / "golden.json").read_text())["runs"]
+    return [(gname, key) for gname, r in runs.items() for key in r
+            if key.endswith("/d1") and gname != "rmat12"]
+
+
+@pytest.mark.parametrize("gname,key", _relabel_keys())
+def test_relabeled_store_parity(sg, golden, gname, key):
+    """Runs on the relabeled store (hot vertices first; at these sizes K >= V,
+    i.e. a full degree order) reproduce the reference's labels (sha) and
+    per-round log for every app x scheduler of the goldens; the source and
+    cc's initial ids are renamed in, the labels renamed out."""
+    info = golden["runs"][gname][key]
+    app = key.split("/")[0]
+    g = _graph(sg, gname)
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    labels, rounds = _run_flags(sg, g, app, _sched(sg, key), SG_FLAG_RELABEL)
+    assert rounds == [x[:2] for x in info["per_round"]]
+    if app == "pr":
+        ref, _ = _run_flags(sg, g, app, _sched(sg, key), SG_FLAG_NO_RELABEL)
+        assert np.max(np.abs(labels - ref)) <= PR_ATOL
+    else:
+        assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
+
+
+@pytest.mark.parametrize("scale,flags", [(18, SG_FLAG_RELABEL), (20, SG_FLAG_NO_RELABEL), (20, 0)])
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "kcore", "pr"])
+def test_relabel_partial_hot_set_vs_c_oracle(sg, scale, flags, app):
+    """rmat18 forced onto the relabeled store (K = 2^16 < V for push apps: a
+    hot prefix and the rest in id order), rmat20 forced off it, and rmat20 on
+    the automatic choice (first run original, second run relabeled): all
+    bit-identical to the C oracle (pr: tolerance, rounds +-1)."""
+    from oracle import oracle_c as C
+    g = sg.generate_rmat(scale, 16, 1)
+    gw = sg.attach_random_weights(g, 2) if app == "sssp" else g
+    w = gw.edge_weights if app == "sssp" else None
+    lab, log, st = C.run(app, *C.prepare(g.out_offsets, g.out_targets, w, app), threads=8)
+    assert st == 0
+    runs = [_run_flags(sg, gw, app, sg.Scheduler("alb"), flags) for _ in range(2 if not flags else 1)]
+    for labels, rounds in runs:
+        _check_vs_oracle(labels, rounds, lab, log, app)
+
+
+def _check_vs_oracle(labels, rounds, lab, log, app):
+    if app == "pr":
+        assert abs(len(rounds) - len(log)) <= 1
+        assert np.max(np.abs(labels - lab)) <= PR_ATOL
+        return
+    assert rounds == log.tolist()
+    assert np.array_equal(labels, lab)
+
+
+def test_relabel_cta_counters_and_thresholds(sg):
+    """Hardware CTA counters and threshold invariance hold on the relabeled store."""
+    g = sg.attach_random_weights(sg.generate_rmat(14, 16, 1), 2)
+    base, brounds = _run_flags(sg, g, "sssp", sg.Scheduler("alb"), SG_FLAG_NO_RELABEL)
+    for thr in (1, 31, 256, 100000):
+        labels, rounds = _run_flags(sg, g, "sssp", sg.Scheduler("alb", threshold=thr),
+                                    SG_FLAG_RELABEL)
+        assert rounds == brounds and np.array_equal(labels, base)
+    p = sg.engine._device_params(sg.apps.make_app("sssp"), sg.Scheduler("alb"),
+                                 sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
+    p.flags |= SG_FLAG_RELABEL
+    labels, log, _, cta = g.device().run_cta_counts(p)
+    assert np.array_equal(labels, base)
+    assert [int(x) for x in cta.sum(axis=1)[:len(log)]] == [int(r["active_edges"]) for r in log]
