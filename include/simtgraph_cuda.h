@@ -39,6 +39,8 @@ extern "C" {
 #define SG_ECONVERGE (-3)   /* ConvergenceError (errors.py:36-45) */
 #define SG_ECUDA (-4)       /* SimtGraphError: CUDA failure      */
 #define SG_ENOMEM (-5)      /* SimtGraphError: device allocation */
+#define SG_EPARSE (-6)      /* ParseError    (errors.py:8-13): malformed input file */
+#define SG_EIO (-7)         /* OSError: file cannot be opened / read */
 
 /* apps (apps.py:24; opcodes _kernels_py.py:26-29) */
 #define SG_APP_BFS 0
@@ -126,6 +128,12 @@ int sg_graph_attach_random_weights(sg_graph *g, const uint64_t pcg[4], int64_t l
                                    sg_graph **out);
 /* Upload host weights for an existing device graph (same topology). */
 int sg_graph_with_weights(sg_graph *g, const int64_t *weights, sg_graph **out);
+/* Graph.load_binary (graph.py:159-177) of an SGB1 file, streamed from disk
+ * into HBM through pinned staging blocks (multi-threaded reads overlapped
+ * with the H2D copies); Graph._validate (graph.py:44-57) on the device.
+ * Bad magic / version: SG_EPARSE; short sections: the reference's
+ * ConfigError / RangeError of the arrays numpy would have produced. */
+int sg_graph_load_sgb1(const char *path, sg_graph **out);
 int sg_graph_info(sg_graph *g, int64_t *nv, int64_t *ne, int32_t *weighted);
 /* Copy arrays back to host; any pointer may be NULL.  which: 0 CSR, 1 CSC, 2 symmetrized CSR */
 int sg_graph_download(sg_graph *g, int32_t which, int64_t *offsets, int32_t *targets,

@@ -15,11 +15,12 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import ConfigError, ConvergenceError, RangeError, SimtGraphError
+from .errors import ConfigError, ConvergenceError, ParseError, RangeError, SimtGraphError
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsimtgraph_cuda.so"
 
 SG_OK, SG_ECONFIG, SG_ERANGE, SG_ECONVERGE, SG_ECUDA, SG_ENOMEM = 0, -1, -2, -3, -4, -5
+SG_EPARSE, SG_EIO = -6, -7
 APP_IDS = {"bfs": 0, "sssp": 1, "cc": 2, "pr": 3, "kcore": 4}
 SCHED_IDS = {"alb": 0, "twc": 1, "lb": 2, "vertex": 3, "edge": 4}
 
@@ -30,6 +31,7 @@ EXPORTS = (
     "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run", "sg_dist_run_threads",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
     "sg_host_alloc", "sg_host_free", "sg_release_cached", "sg_run_cta_counts",
+    "sg_graph_load_sgb1",
 )
 
 
@@ -100,6 +102,7 @@ def load(path: Path | None = None):
             "sg_host_alloc": ([i64, pp], ctypes.c_int),
             "sg_host_free": ([P], None),
             "sg_release_cached": ([], None),
+            "sg_graph_load_sgb1": ([ctypes.c_char_p, pp], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -156,6 +159,10 @@ def check(code: int):
         raise RangeError(msg)
     if code == SG_ECONVERGE:
         raise ConvergenceError(msg)
+    if code == SG_EPARSE:
+        raise ParseError(msg)
+    if code == SG_EIO:
+        raise OSError(msg)
     raise SimtGraphError(f"CUDA backend error {code}: {msg}")
 
 
@@ -208,6 +215,13 @@ class DeviceGraph:
         h = ctypes.c_void_p()
         check(load().sg_graph_create(ptr(offsets), ptr(targets), ptr(weights), len(offsets) - 1,
                                      len(targets), ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_sgb1(cls, path):
+        """SGB1 file straight into HBM (sg_graph_load_sgb1)."""
+        h = ctypes.c_void_p()
+        check(load().sg_graph_load_sgb1(os.fsencode(path), ctypes.byref(h)))
         return cls(h)
 
     @classmethod
