@@ -34,7 +34,7 @@ def test_round_trip_device(sg, tmp_path, scale, weighted):
     g = sg.generate_rmat(scale, 16, 1)
     if weighted:
         g = sg.attach_random_weights(g, 2)
-    p = tmp_path / "g.sgb"
+    p = tmp_path / "g.bin"  # load_graph picks the format by extension
     g.save_binary(str(p))
     h = sg.Graph.load_binary(str(p))
     assert h.num_vertices == g.num_vertices and h.num_edges == g.num_edges
