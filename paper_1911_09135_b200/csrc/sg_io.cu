@@ -126,15 +126,17 @@ extern "C" int sg_graph_load_sgb1(const char *path, sg_graph **out) {
     // what numpy's frombuffer would have produced from a short file: the
     // sections as far as the file goes (graph.py:168-174), then Graph's checks
     const int64_t body = std::max<int64_t>(0, fsize - 28);
-    const int64_t nv = (int64_t)nv_u, ne_hdr = (int64_t)ne_u;
+    const int64_t nv_hdr = (int64_t)nv_u, ne_hdr = (int64_t)ne_u;
     if (nv_u > (1ull << 40) || ne_u > (1ull << 40))
       throw Error(SG_ECONFIG, "offsets must have num_vertices+1 entries starting at 0");
-    const int64_t n_off = std::min<int64_t>(nv + 1, body / 8);
+    const int64_t n_off = std::min<int64_t>(nv_hdr + 1, body / 8);
     const int64_t rest = body - n_off * 8;
     const int64_t ne = std::min<int64_t>(ne_hdr, std::max<int64_t>(0, rest) / 4);  // len(targets)
     const int64_t rest2 = rest - ne * 4;
     const int64_t n_w = weighted ? std::min<int64_t>(ne_hdr, std::max<int64_t>(0, rest2) / 8) : 0;
-    if (n_off != nv + 1) throw Error(SG_ECONFIG, "offsets must have num_vertices+1 entries starting at 0");
+    // Graph() takes num_vertices = len(offsets) - 1 (graph.py:38)
+    if (n_off < 1) throw Error(SG_ECONFIG, "offsets must have num_vertices+1 entries starting at 0");
+    const int64_t nv = n_off - 1;
     if (nv > 0x7fffffffLL) throw Error(SG_ERANGE, "vertex ids must fit int32");
 
     auto g = std::make_shared<sg::Graph>();
