@@ -610,16 +610,21 @@ int64_t hot_k(int64_t nv, int32_t app) {
 
 constexpr int64_t kRelabelMinV = (int64_t)1 << 20;
 
-// Automatic choice: relabel graphs of >= 2^20 vertices on one device, from the
-// graph's second run on.  Building the relabeled store (degree sort + one
-// renaming pass over the CSR: ~15 ms at rmat24, sg_graph.cu) costs more than
-// one push run gains, so a graph that is created, run once and dropped (the
-// e2e path) keeps its original numbering; resident graphs that are run again
-// amortise it at once.
+// Automatic choice: relabel skewed graphs of >= 2^20 vertices on one device,
+// from the graph's second run on.  Building the relabeled store (degree sort +
+// one renaming pass over the CSR: ~15 ms at rmat24, sg_graph.cu) costs more
+// than one push run gains, so a graph that is created, run once and dropped
+// (the e2e path) keeps its original numbering; resident graphs that are run
+// again amortise it at once.  Without degree skew there is no hot set to
+// cluster (uniform rmat25 pr: 120 -> 114 GTEPS relabeled), so graphs whose top
+// 1 % of vertices source < 10 % of the edges keep their numbering.
+constexpr double kRelabelMinSkew = 0.10;
+
 bool use_relabel(Graph &g, const sg_params &p) {
   if (p.devices != 1 || (p.flags & SG_FLAG_NO_RELABEL) || g.nv == 0) return false;
   if (p.flags & SG_FLAG_RELABEL) return true;
-  return g.nv >= kRelabelMinV && g.runs++ >= 1;
+  if (g.nv < kRelabelMinV || g.runs++ < 1) return false;
+  return g.top1_share() >= kRelabelMinSkew;
 }
 
 void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out, int64_t cap,

@@ -318,6 +318,16 @@ double Graph::source_coverage(int64_t K) {
   return cov_;
 }
 
+double Graph::top1_share() {
+  if (top1_ < 0.0) {
+    const int64_t k_old = cov_k_;
+    const double c_old = cov_;
+    top1_ = source_coverage(std::max<int64_t>(1, nv / 100));
+    cov_k_ = k_old, cov_ = c_old;  // keep the pr tiling's cached entry
+  }
+  return top1_;
+}
+
 const Tiles &Graph::tiles(int64_t S) {
   if (tiles_ && tiles_->S == S) return *tiles_;
   const View &c = csc();
@@ -458,7 +468,9 @@ Relabel &Graph::hot(int64_t K) {
       if (w32.p) h->w32.alloc(ne ? ne : 1);
       h->w64.alloc(want64 && ne ? ne : 1);
     }
-    SG_LAUNCH(k_perm_rows, grid_for(nv * 32), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
+    // one warp per row, no grid-stride cap: the per-row chain of dependent
+    // loads (perm -> off -> col -> inv) needs every warp slot in flight
+    SG_LAUNCH(k_perm_rows, (unsigned)((nv + 7) / 8), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
               R->perm.p, R->inv.p, h->csr.off.p, nv, h->csr.col.p,
               want64 ? h->w64.p : nullptr, weighted && w32.p ? h->w32.p : nullptr);
     SG_CUDA(cudaDeviceSynchronize());

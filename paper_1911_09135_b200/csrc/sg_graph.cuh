@@ -50,6 +50,10 @@ struct Graph {
   std::map<int64_t, std::unique_ptr<Relabel>> hot_;
   Relabel &hot(int64_t K);
   int64_t runs = 0;  // single-device runs on this graph (the relabeling is built from the 2nd)
+  // share of the edges leaving the top 1 % of vertices by out-degree (cached;
+  // rmat skewed: ~0.5, uniform: ~0.03) -- whether a degree relabeling pays
+  double top1_share();
+  double top1_ = -1.0;
 };
 
 // Hot-vertex relabeling: the kernel-side layout of the store.  The K vertices
