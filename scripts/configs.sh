@@ -10,7 +10,9 @@ run() {
     >> $out 2>> gpurun_out/${TAG:-cfg}_configs.err
   echo "rc=$? $*"
 }
-for c in ${CONFIGS:-"--app cc --scale 25" "--app pr --scale 25" "--app pr --scale 25 --uniform" "--app bfs --scale 27" "--app kcore --scale 27"}; do
+# CONFIGS: ';'-separated bench argument lists (default: C3-C5)
+IFS=';' read -ra LIST <<< "${CONFIGS:---app cc --scale 25;--app pr --scale 25;--app pr --scale 25 --uniform;--app bfs --scale 27;--app kcore --scale 27}"
+for c in "${LIST[@]}"; do
   run $c
 done
 python - "$out" <<'PY'
