@@ -26,7 +26,7 @@
 namespace sg {
 
 #ifndef SG_BKV
-#define SG_BKV 8
+#define SG_BKV 6
 #endif
 constexpr int kV = SG_BKV;  // edges per lane per step in the bitmap-frontier kernels
 static_assert(kV * 32 <= (int)kLarge, "k_bm_large: a warp step must span <= 2 CTA-bin vertices");
