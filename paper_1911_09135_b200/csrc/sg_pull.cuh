@@ -15,6 +15,15 @@
 
 namespace sg {
 
+#ifndef SG_PULL_V
+#define SG_PULL_V 8
+#endif
+// edges per lane per step in the pull kernels (pr gathers 8-byte aux values:
+// kcore / pr measured 7 % slower at the push kernels' kV = 6)
+constexpr int kPullV = SG_PULL_V;
+static_assert(kPullV * 32 <= (int)kLarge, "k_pull_large: a warp step must span <= 2 rows");
+
+
 #ifndef SG_PR_UNROLL
 #define SG_PR_UNROLL 4
 #endif
@@ -207,15 +216,15 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
       const int64_t ms = shfl64(s, l);
       const uint32_t md = (uint32_t)__shfl_sync(kFull, (uint32_t)deg, l);
       typename Op::A x = 0;
-      for (uint32_t b = 0; b < md; b += 32 * kV) {
-        uint32_t src[kV];
+      for (uint32_t b = 0; b < md; b += 32 * kPullV) {
+        uint32_t src[kPullV];
 #pragma unroll
-        for (int u = 0; u < kV; ++u) {
+        for (int u = 0; u < kPullV; ++u) {
           const uint32_t j = b + u * 32 + lane;
           src[u] = j < md ? ld_stream(a.col + ms + j) : 0xffffffffu;
         }
 #pragma unroll
-        for (int u = 0; u < kV; ++u) {
+        for (int u = 0; u < kPullV; ++u) {
           x += src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
           my_proc += src[u] != 0xffffffffu;
         }
@@ -306,8 +315,8 @@ __global__ void __launch_bounds__(kTB) k_pull_vertex(PullArgs a, Op op) {
 }
 
 // TWC CTA bin: edge-balanced batches of kBatch rows (degree-mixed, dynamic
-// fetch).  Each warp takes 32*kV consecutive slots per step; rows own >= kLarge
-// >= 32*kV slots, so a step spans <= 2 rows.  A warp carries one running sum
+// fetch).  Each warp takes 32*kPullV consecutive slots per step; rows own >= kLarge
+// >= 32*kPullV slots, so a step spans <= 2 rows.  A warp carries one running sum
 // for its current row and parks it in part[warp][row] when the row changes
 // (each warp meets a row in one contiguous stretch), and the batch's rows are
 // folded as part[0][r] + ... + part[7][r]: a fixed order, deterministic.
@@ -352,8 +361,8 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
     const long long total = bexcl[kBatch];
     int cur_o = -1;
     A cur = 0;
-    for (long long b = 0; b < total; b += kTB * kV) {
-      const long long wbase = b + (long long)warp * (32 * kV);
+    for (long long b = 0; b < total; b += kTB * kPullV) {
+      const long long wbase = b + (long long)warp * (32 * kPullV);
       if (wbase >= total) continue;
       uint32_t lo = 0;  // last o with bexcl[o] <= wbase
 #pragma unroll
@@ -361,10 +370,10 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
         lo = bexcl[lo + step] <= wbase ? lo + step : lo;
       const long long x0 = bexcl[lo], x1 = bexcl[lo + 1];
       const int64_t s0 = bstart[lo], s1 = lo + 1 < kBatch ? bstart[lo + 1] : 0;
-      uint32_t src[kV];
-      bool sec[kV];
+      uint32_t src[kPullV];
+      bool sec[kPullV];
 #pragma unroll
-      for (int u = 0; u < kV; ++u) {
+      for (int u = 0; u < kPullV; ++u) {
         const long long slot = wbase + u * 32 + lane;
         sec[u] = slot >= x1;
         src[u] = slot < total ? ld_stream(a.col + (sec[u] ? s1 + (slot - x1) : s0 + (slot - x0)))
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
       }
       A xa = 0, xb = 0;
 #pragma unroll
-      for (int u = 0; u < kV; ++u) {
+      for (int u = 0; u < kPullV; ++u) {
         const A y = src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
         my_proc += src[u] != 0xffffffffu;
         if (sec[u]) xb += y;
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(kTB) k_pull_large(PullArgs a, Op op) {
         cur = 0;
       }
       cur += xa;
-      if (x1 < wbase + 32 * kV && x1 < total) {  // the step crossed into row lo + 1
+      if (x1 < wbase + 32 * kPullV && x1 < total) {  // the step crossed into row lo + 1
         if (lane == 0) part[warp][cur_o] = cur;
         cur_o = (int)lo + 1;
         cur = xb;
@@ -437,12 +446,12 @@ __global__ void __launch_bounds__(kTB) k_pull_large_classic(PullArgs a, Op op) {
     const uint32_t v = a.largeq[idx];
     const int64_t s = a.off[v], e = a.off[v + 1];
     A x = 0;
-    for (int64_t b = s + threadIdx.x; b < e; b += kTB * kV) {
-      uint32_t src[kV];
+    for (int64_t b = s + threadIdx.x; b < e; b += kTB * kPullV) {
+      uint32_t src[kPullV];
 #pragma unroll
-      for (int u = 0; u < kV; ++u) src[u] = b + u * kTB < e ? ld_stream(a.col + b + u * kTB) : 0xffffffffu;
+      for (int u = 0; u < kPullV; ++u) src[u] = b + u * kTB < e ? ld_stream(a.col + b + u * kTB) : 0xffffffffu;
 #pragma unroll
-      for (int u = 0; u < kV; ++u) {
+      for (int u = 0; u < kPullV; ++u) {
         x += src[u] != 0xffffffffu ? op.load(src[u]) : A(0);
         my_proc += src[u] != 0xffffffffu;
       }
@@ -507,10 +516,10 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
-  if (!BLOCKED && a.threshold >= 32 * kV) {
-    // warp-granular cyclic chunks of 32*kV edge ids, spanning <= 2 huge rows:
+  if (!BLOCKED && a.threshold >= 32 * kPullV) {
+    // warp-granular cyclic chunks of 32*kPullV edge ids, spanning <= 2 huge rows:
     // one warp-uniform find_owner per chunk, two warp sums, <= 2 atomics
-    constexpr int64_t CH = 32 * kV;
+    constexpr int64_t CH = 32 * kPullV;
     const int64_t nwarps = T >> 5, nch = (E + CH - 1) / CH;
     uint32_t olo = 0;
     for (int64_t c = tid >> 5; c < nch; c += nwarps) {
@@ -519,17 +528,17 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
       olo = o;
       const int64_t x0 = o ? a.hpre[o - 1] : 0, x1 = a.hpre[o];
       const int64_t s0 = a.hstart[o], s1 = o + 1 < nh ? a.hstart[o + 1] : 0;
-      uint32_t src[kV];
-      bool sec[kV];
+      uint32_t src[kPullV];
+      bool sec[kPullV];
 #pragma unroll
-      for (int u = 0; u < kV; ++u) {
+      for (int u = 0; u < kPullV; ++u) {
         const int64_t g = g0 + u * 32 + lane;
         sec[u] = g >= x1;
         src[u] = g < E ? ld_stream(a.col + (sec[u] ? s1 + (g - x1) : s0 + (g - x0))) : 0xffffffffu;
       }
       typename Op::A xa = 0, xb = 0;
 #pragma unroll
-      for (int u = 0; u < kV; ++u) {
+      for (int u = 0; u < kPullV; ++u) {
         my_proc += src[u] != 0xffffffffu;
         const typename Op::A y = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
         if (sec[u]) xb += y;
