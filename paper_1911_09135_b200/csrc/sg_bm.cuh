@@ -80,7 +80,10 @@ struct BmBfs {
     if (n) prev[wi] = x;
     return n;
   }
-  __device__ __forceinline__ void emit(uint32_t, uint32_t v) const { lab[v] = r + 1; }
+  // compaction: per emitted vertex, a load (none here) and the stores
+  using E = uint32_t;
+  __device__ __forceinline__ E emit_load(uint32_t) const { return 0u; }
+  __device__ __forceinline__ void emit_store(uint32_t, uint32_t v, E) const { lab[v] = r + 1; }
 };
 
 // sssp / cc (KIND as OpPair: 0 cc, 1 unit weight, 2 u32 weights, 3 float64 bits)
@@ -116,7 +119,9 @@ struct BmMin {
     for (int u = 0; u < kV; ++u) {
       if (p[u] < cur[u]) {  // ok[u] implied: cur = 0 otherwise
         atomicMin(lab + dst[u], p[u]);                      // RED.MIN
+#ifndef SG_EXP_NO_OR
         atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));  // RED.OR
+#endif
       }
     }
   }
@@ -152,7 +157,9 @@ struct BmMin {
     for (int u = 0; u < N; ++u) {
       if (ok[u] && p[u] < cur[u]) {
         atomicMin(lab + dst[u], p[u]);
+#ifndef SG_EXP_NO_OR
         atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));
+#endif
       }
     }
   }
@@ -161,7 +168,9 @@ struct BmMin {
     if (x) nb[wi] = 0u;
     return x;
   }
-  __device__ __forceinline__ void emit(uint32_t slot, uint32_t v) const { snap[slot] = lab[v]; }
+  using E = L;
+  __device__ __forceinline__ E emit_load(uint32_t v) const { return lab[v]; }
+  __device__ __forceinline__ void emit_store(uint32_t slot, uint32_t, E x) const { snap[slot] = x; }
 };
 
 // ---------------------------------------------------------------- kernels --
@@ -706,16 +715,31 @@ __global__ void __launch_bounds__(kTB) k_bm_compact(PushArgs a, Op op) {
     if (lane == 0) pos0 = atomicAdd(&ctl->nsize, total);
     pos0 = __shfl_sync(kFull, pos0, 0);
     const uint32_t excl = incl - cnt;
-    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-      const uint32_t slot = k0 + lane;
-      const int o = warp_owner(incl, slot);
-      const uint32_t bo = __shfl_sync(kFull, bits, o);
-      const uint32_t eo = __shfl_sync(kFull, excl, o);
-      if (slot < total) {
-        const uint32_t b = __fns(bo, 0, (int)(slot - eo) + 1);
-        const uint32_t v = (w0 + (uint32_t)o) * 32 + b;
-        q[pos0 + slot] = v;
-        op.emit(pos0 + slot, v);
+    // 4 emits per lane in flight: a dense word block (up to 1024 vertices,
+    // clustered at low ids on the relabeled store) is 8 steps, not 32
+    // dependent load -> store chains
+    constexpr int kE = 4;
+    for (uint32_t k0 = 0; k0 < total; k0 += 32 * kE) {
+      uint32_t v[kE];
+      typename Op::E x[kE];
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        const uint32_t slot = k0 + u * 32 + lane;
+        const int o = warp_owner(incl, slot);
+        const uint32_t bo = __shfl_sync(kFull, bits, o);
+        const uint32_t eo = __shfl_sync(kFull, excl, o);
+        v[u] = slot < total ? (w0 + (uint32_t)o) * 32 + __fns(bo, 0, (int)(slot - eo) + 1) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kE; ++u)
+        if (k0 + u * 32 + lane < total) x[u] = op.emit_load(v[u]);
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        const uint32_t slot = k0 + u * 32 + lane;
+        if (slot < total) {
+          q[pos0 + slot] = v[u];
+          op.emit_store(pos0 + slot, v[u], x[u]);
+        }
       }
     }
   }
