@@ -276,10 +276,10 @@ def run_reference(a):
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": f"{a.app} rmat{a.scale} ef16 seed1" + (" uniform" if a.uniform else "")
-                   + (" weights[1,64] seed2" if a.app == "sssp" else ""),
+                   + (" weights[1,64] seed2" if a.app == "sssp" else "") + " source0",
                    "edges_processed": edges, "scheduler": "n/a (CPU restatement)"},
         "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": "port",
                          "sample": f"full {a.app} run on rmat{a.scale}, oracle/sg_oracle.c "
