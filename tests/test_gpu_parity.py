@@ -429,3 +429,28 @@ def test_relabel_cta_counters_and_thresholds(sg):
     labels, log, _, cta = g.device().run_cta_counts(p)
     assert np.array_equal(labels, base)
     assert [int(x) for x in cta.sum(axis=1)[:len(log)]] == [int(r["active_edges"]) for r in log]
+
+
+def test_relabel_edge_cases(sg, golden, O):
+    """The relabeled store on the SPEC corner graphs (self loops, duplicate
+    edges, isolated vertices, an edgeless graph) and on int64 weights beyond
+    the u32 path (the relabeled copy then carries the int64 weights)."""
+    G = sg.Graph
+    spec = golden["spec"]
+    messy = G.from_edges([0, 0, 0, 1, 3, 3, 5], [0, 1, 1, 2, 4, 3, 5], [3, 2, 1, 7, 1, 1, 9], 7)
+    empty = G(np.zeros(5, np.int64), np.zeros(0, np.int32), None, 4)
+    for app in ("bfs", "sssp", "cc", "pr", "kcore"):
+        for name, gr in (("messy", messy), ("empty4", empty)):
+            got, _ = _run_flags(sg, gr, app, sg.Scheduler("alb"), SG_FLAG_RELABEL)
+            want = np.array(spec[f"{name}_{app}"])
+            if app == "pr":
+                assert np.allclose(got, want, rtol=0, atol=PR_ATOL), (name, app)
+            else:
+                assert got.tolist() == want.tolist(), (name, app)
+    off, tgt = O.rmat_csr(11)
+    w = np.random.default_rng(7).integers(1 << 40, 1 << 52, size=len(tgt), dtype=np.int64)
+    g = sg.Graph(off, tgt, w)
+    labels, rounds = _run_flags(sg, g, "sssp", sg.Scheduler("alb"), SG_FLAG_RELABEL)
+    lab, log = O.run(off, tgt, w, "sssp")
+    assert O.labels_sha256(labels) == O.labels_sha256(lab)
+    assert rounds == [[r.frontier_size, r.active_edges] for r in log]
