@@ -21,6 +21,9 @@ namespace sg {
 // edges per lane per step in the pull kernels (pr gathers 8-byte aux values:
 // kcore / pr measured 7 % slower at the push kernels' kV = 6)
 constexpr int kPullV = SG_PULL_V;
+#ifndef SG_PULL_SEQ
+#define SG_PULL_SEQ 32  // longest per-window row segment summed sequentially (0: scan only)
+#endif
 static_assert(kPullV * 32 <= (int)kLarge, "k_pull_large: a warp step must span <= 2 rows");
 
 
@@ -175,6 +178,13 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
     const uint32_t excl = incl - gd;
     typename Op::A acc = 0;
     constexpr int KP = Op::kUnroll;
+#if SG_PULL_SEQ
+    // short-segment windows: park the gathered values in shared memory and
+    // let each owner lane sum its own segment in order -- a few shared-memory
+    // wavefronts instead of the segmented scan's ~25 shuffles per 32 slots
+    // (the data pipe is what bounds this kernel, ncu)
+    __shared__ typename Op::A sbuf[kWarpsTB][32 * KP];
+#endif
     for (uint32_t base = 0; base < total; base += 32 * KP) {
       int o[KP];
       uint32_t src[KP];
@@ -192,6 +202,25 @@ __global__ void __launch_bounds__(kTB) k_pull_twc(PullArgs a, Op op) {
         x[u] = src[u] != 0xffffffffu ? op.load(src[u]) : typename Op::A(0);
         my_proc += src[u] != 0xffffffffu;
       }
+#if SG_PULL_SEQ
+      {
+        const uint32_t wlo = excl > base ? excl : base;
+        const uint32_t whi = incl < base + 32 * KP ? incl : base + 32 * KP;
+        const uint32_t len = wlo < whi ? whi - wlo : 0u;
+        const uint32_t maxlen = __reduce_max_sync(kFull, len);
+        if (maxlen <= SG_PULL_SEQ) {
+#pragma unroll
+          for (int u = 0; u < KP; ++u) sbuf[warp][u * 32 + lane] = x[u];
+          __syncwarp();
+          typename Op::A sum = 0;
+          for (uint32_t j = 0; j < maxlen; ++j)
+            if (j < len) sum += sbuf[warp][wlo - base + j];
+          acc += sum;
+          __syncwarp();
+          continue;
+        }
+      }
+#endif
 #pragma unroll
       for (int u = 0; u < KP; ++u) {
         const uint32_t cb = base + u * 32;

@@ -9,7 +9,7 @@ for v in ${VARIANTS:-base}; do
   if [ "$v" = base ]; then lib=paper_1911_09135_b200/_lib/libsimtgraph_cuda.so; else lib=paper_1911_09135_b200/_lib/$v/libsimtgraph_cuda.so; fi
   for app in ${APPS:-sssp}; do
     for sched in ${SCHEDS:-alb}; do
-      line=$(SIMTGRAPH_CUDA_LIB=$lib timeout 600 python bench.py --app $app --sched $sched --scale ${SCALE:-24} --steps ${STEPS:-5} --warmup 3 --no-e2e --no-cpu-baseline ${EXTRA:-} 2>>gpurun_out/${TAG:-var}_variants.err)
+      line=$(SIMTGRAPH_CUDA_LIB=$lib timeout 600 python bench.py --app $app --sched $sched --scale ${SCALE:-24} --steps ${STEPS:-5} --warmup 3 --no-e2e --no-cpu-baseline --extra "" --no-ablation ${EXTRA:-} 2>>gpurun_out/${TAG:-var}_variants.err)
       python -c "
 import json,sys
 d=json.loads(sys.argv[1]); k=d.get('kernel_ms',{})
