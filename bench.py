@@ -186,7 +186,7 @@ def kernel_edges(log):
 
 
 # profiled-run kernel names -> the CUDA kernels ncu lists
-NCU_NAME = {"push_twc": "k_bm_twc", "push_large": "k_bm_large", "push_lb": "k_bm_lb",
+NCU_NAME = {"push_twc": "k_bm_twc", "push_large": "k_bm_large_pipe", "push_lb": "k_bm_lb",
             "compact": "k_bm_compact", "pull_twc": "k_pull_twc", "pull_large": "k_pull_large",
             "pull_lb": "k_pull_lb"}
 # random 4-byte gathers per second the chip sustains (scripts/micro/gather.cu on

@@ -14,7 +14,7 @@ if [ "${NCU:-1}" = 1 ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
      --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --extra "" --no-ablation \
      > gpurun_out/${TAG}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${KERNEL:-k_push_twc} -c ${NCOUNT:-12} \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${KERNEL:-k_bm_large_pipe} -c ${NCOUNT:-9} \
      -o gpurun_out/${TAG}_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --extra "" --no-ablation \
      > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
