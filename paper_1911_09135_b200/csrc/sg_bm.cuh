@@ -471,11 +471,10 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
     constexpr int64_t CH = 32 * kV;
     const int64_t nwarps = T >> 5, nch = (E + CH - 1) / CH;
     const uint32_t lane = lane_id();
-    uint32_t olo = 0;
+    const Coarse cx = coarse_build(spre, a.hpre, nh);  // spre: >= kCoarse entries
     for (int64_t c = tid >> 5; c < nch; c += nwarps) {
       const int64_t g0 = c * CH;
-      const uint32_t o = owner_search_from(a.hpre, olo, nh, g0);
-      olo = o;
+      const uint32_t o = cx.find(g0);
       const int64_t x0 = o ? a.hpre[o - 1] : 0, x1 = a.hpre[o];
       const int64_t s0 = a.hstart[o], s1 = o + 1 < nh ? a.hstart[o + 1] : 0;
       const L v0 = (L)a.hval[o], v1 = o + 1 < nh ? (L)a.hval[o + 1] : L(0);

@@ -150,4 +150,40 @@ __device__ __forceinline__ uint32_t owner_search_from(const int64_t *pre, uint32
   return lo;
 }
 
+// Two-level find_owner for the LB kernels' chunk bisection: a shared-memory
+// sample of the huge prefix (every stride-th block end, <= kCoarse entries)
+// narrows the search to one stride-long block before the global-memory steps
+// (cc rmat24 round 0: 2,325 hubs -> 8 shared + 4 global steps instead of 11
+// global ones); 2 KB of shared memory, so the L1 keeps its size.
+constexpr uint32_t kCoarse = 256;
+struct Coarse {
+  const int64_t *pre;  // the inclusive huge prefix (global)
+  const int64_t *c;    // c[j] = pre[min((j + 1) * stride, n) - 1] (shared)
+  uint32_t n, stride, m;
+  // upper_bound: first i with pre[i] > g (g < pre[n - 1])
+  __device__ __forceinline__ uint32_t find(int64_t g) const {
+    uint32_t lo = 0, hi = m - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (g < c[mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    uint32_t a = lo * stride, b = min(a + stride, n) - 1;
+    while (a < b) {
+      const uint32_t mid = (a + b) >> 1;
+      if (g < pre[mid]) b = mid;
+      else a = mid + 1;
+    }
+    return a;
+  }
+};
+// all threads of the CTA: fill the sample (c has kCoarse entries)
+__device__ __forceinline__ Coarse coarse_build(int64_t *c, const int64_t *pre, uint32_t n) {
+  Coarse x{pre, c, n, (n + kCoarse - 1) / kCoarse, 0};
+  x.m = (n + x.stride - 1) / x.stride;
+  for (uint32_t i = threadIdx.x; i < x.m; i += blockDim.x) c[i] = pre[min((i + 1) * x.stride, n) - 1];
+  __syncthreads();
+  return x;
+}
+
 }  // namespace sg

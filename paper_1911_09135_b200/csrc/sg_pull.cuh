@@ -550,11 +550,11 @@ __global__ void __launch_bounds__(kTB) k_pull_lb(PullArgs a, Op op, typename Op:
     // one warp-uniform find_owner per chunk, two warp sums, <= 2 atomics
     constexpr int64_t CH = 32 * kPullV;
     const int64_t nwarps = T >> 5, nch = (E + CH - 1) / CH;
-    uint32_t olo = 0;
+    __shared__ int64_t csample[kCoarse];
+    const Coarse cx = coarse_build(csample, a.hpre, nh);
     for (int64_t c = tid >> 5; c < nch; c += nwarps) {
       const int64_t g0 = c * CH;
-      const uint32_t o = owner_search_from(a.hpre, olo, nh, g0);
-      olo = o;
+      const uint32_t o = cx.find(g0);
       const int64_t x0 = o ? a.hpre[o - 1] : 0, x1 = a.hpre[o];
       const int64_t s0 = a.hstart[o], s1 = o + 1 < nh ? a.hstart[o + 1] : 0;
       uint32_t src[kPullV];

@@ -39,6 +39,7 @@ constexpr int kWarpsTB = kTB / 32;
 constexpr int kU = SG_KU;       // edges per lane per step (memory-level parallelism)
 constexpr uint32_t kLarge = 256;  // TWC CTA-bin cut (threads_per_cta, schedulers.py:159)
 constexpr uint32_t kHugeSmem = 1024;  // huge-vertex prefix/start/label staged in shared memory
+static_assert(kHugeSmem >= 256, "k_bm_lb reuses spre for the 256-entry Coarse sample");
 constexpr uint32_t kChunkGrab = 4;    // TWC chunks (32 items each) per dynamic fetch
 constexpr int kBatch = 32;            // CTA-bin vertices per block-level gather batch
 
