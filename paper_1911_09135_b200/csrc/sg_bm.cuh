@@ -178,6 +178,8 @@ struct BmMin {
 // queued with their snapshot label
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   using L = typename Op::L;
   __shared__ unsigned long long red[32];
   Ctl *ctl = a.ctl;
@@ -250,6 +252,8 @@ __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
 // TWC CTA bin: block-level gather over batches of kBatch queued vertices
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   using L = typename Op::L;
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
@@ -324,6 +328,8 @@ constexpr int kPV = SG_PIPE_V;  // edges per lane per step of the pipelined CTA-
 // in flight while step k's label gathers and reductions issue
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   using L = typename Op::L;
   using W = typename Op::W;
   Ctl *ctl = a.ctl;
@@ -407,6 +413,8 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
 // (SG_FLAG_TWC_CLASSIC); one huge vertex pins one CTA for its whole degree.
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   using L = typename Op::L;
   __shared__ uint32_t item;
   Ctl *ctl = a.ctl;
@@ -446,6 +454,8 @@ __global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
 // huge edges cyclically (g = p*T + tid) or blocked (g = tid*ceil(e/T) + p)
 template <class Op, bool BLOCKED>
 __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   using L = typename Op::L;
   __shared__ int64_t spre[kHugeSmem], sstart[kHugeSmem];
   __shared__ unsigned long long sval[kHugeSmem];
@@ -697,6 +707,8 @@ __global__ void __launch_bounds__(kTB) k_bm_edge(PushArgs a, Op op) {
 // 1024-vertex range, one atomic per warp range, coalesced id / snapshot writes
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_bm_compact(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
   op.begin(ctl->round);

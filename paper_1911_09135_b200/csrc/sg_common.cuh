@@ -113,6 +113,14 @@ inline int persistent_grid(int per_sm) { return sm_info().sms * per_sm; }
 
 // ------------------------------------------------------------ warp utils --
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+// Programmatic dependent launch (sm_90+): the per-round kernels of the push
+// loop are launched with programmatic stream serialization, so a kernel's CTAs
+// are scheduled while its predecessor drains; every such kernel waits for the
+// predecessor's completion (and memory) before its first access, and lets its
+// own successor launch right away.  Without a programmatic edge both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

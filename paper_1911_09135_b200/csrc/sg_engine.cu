@@ -181,7 +181,7 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   auto set_round = [&](auto op) {
     P.round = [=, &rb](RoundCtx &c) {
       bm_round(c, a, op, blocked, classic, tsum);
-      c.L.go("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
+      c.L.go_pdl("advance", k_push_advance, 1, 32, c.s, a, loop_of(rb, max_rounds, c));
     };
   };
 

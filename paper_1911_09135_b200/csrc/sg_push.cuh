@@ -384,6 +384,8 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
 // degrees in list order, plus each vertex's first edge and snapshot label.
 template <class Op>
 __global__ void __launch_bounds__(1024) k_huge_prefix(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ long long red[32];
   __shared__ long long carry;
   Ctl *ctl = a.ctl;

@@ -43,6 +43,9 @@ inline int grid_n(int64_t n, int block = 256) {
 }
 
 // Launches round kernels: plain (graph capture) or bracketed by CUDA events.
+#ifndef SG_PDL
+#define SG_PDL 1
+#endif
 struct Launcher {
   bool profile = false;
   std::vector<std::tuple<const char *, cudaEvent_t, cudaEvent_t>> pending;
@@ -74,6 +77,26 @@ struct Launcher {
       pending.emplace_back(name, e0, e1);
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
+  }
+  // launch with a programmatic edge to the previous kernel on the stream
+  // (the kernel must start with pdl_wait(); see sg_common.cuh)
+  template <class K, class... A>
+  void go_pdl(const char *name, K kernel, int grid, int block, cudaStream_t s, A... args) {
+    if (profile || !SG_PDL) {
+      go(name, kernel, grid, block, s, args...);
+      return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SG_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
   }
   void collect() {
     for (auto &t : pending) {
@@ -350,6 +373,8 @@ __device__ __forceinline__ void loop_test(Ctl *ctl, uint32_t round, bool empty, 
 
 // round bookkeeping (the parity-paired labels need no commit pass)
 __global__ void k_push_advance(PushArgs a, Loop lp) {
+  pdl_wait();
+  pdl_trigger();
   Ctl *ctl = a.ctl;
   if (threadIdx.x) return;
   if (ctl->done) {
@@ -572,25 +597,25 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
       c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
     return;
   }
-  c.L.go("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
+  c.L.go_pdl("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
   if (classic)
-    c.L.go("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
+    c.L.go_pdl("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
            c.s, a, op);
   else if (SG_LARGE_PIPE)
-    c.L.go("push_large", k_bm_large_pipe<Op>, occupancy_grid(k_bm_large_pipe<Op>, kTB), kTB, c.s,
+    c.L.go_pdl("push_large", k_bm_large_pipe<Op>, occupancy_grid(k_bm_large_pipe<Op>, kTB), kTB, c.s,
            a, op);
   else
-    c.L.go("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
+    c.L.go_pdl("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
   if (a.threshold != kNoHuge) {
-    c.L.go("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
+    c.L.go_pdl("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
     if (blocked)
-      c.L.go("push_lb", k_bm_lb<Op, true>, occupancy_grid(k_bm_lb<Op, true>, kTB), kTB, c.s, a, op);
+      c.L.go_pdl("push_lb", k_bm_lb<Op, true>, occupancy_grid(k_bm_lb<Op, true>, kTB), kTB, c.s, a, op);
     else
-      c.L.go("push_lb", k_bm_lb<Op, false>, occupancy_grid(k_bm_lb<Op, false>, kTB), kTB, c.s, a,
+      c.L.go_pdl("push_lb", k_bm_lb<Op, false>, occupancy_grid(k_bm_lb<Op, false>, kTB), kTB, c.s, a,
              op);
   }
   if (compact)
-    c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
+    c.L.go_pdl("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
 }
 
 template <class Op>
