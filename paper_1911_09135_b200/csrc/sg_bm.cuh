@@ -119,9 +119,7 @@ struct BmMin {
     for (int u = 0; u < kV; ++u) {
       if (p[u] < cur[u]) {  // ok[u] implied: cur = 0 otherwise
         atomicMin(lab + dst[u], p[u]);                      // RED.MIN
-#ifndef SG_EXP_NO_OR
         atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));  // RED.OR
-#endif
       }
     }
   }
@@ -157,9 +155,7 @@ struct BmMin {
     for (int u = 0; u < N; ++u) {
       if (ok[u] && p[u] < cur[u]) {
         atomicMin(lab + dst[u], p[u]);
-#ifndef SG_EXP_NO_OR
         atomicOr(nb + (dst[u] >> 5), 1u << (dst[u] & 31u));
-#endif
       }
     }
   }
