@@ -402,23 +402,33 @@ __global__ void k_perm_len(const int64_t *__restrict__ off, const uint32_t *__re
     len[i] = off[v + 1] - off[v];
   }
 }
-// new row i = old row perm[i] with its targets renamed (row order kept); warp per row
+// new row i = old row perm[i] with its targets renamed (row order kept).
+// Rows [0, nbig) -- the head of the hot prefix, i.e. the hubs -- are split
+// over gridDim.y CTAs each (a 370 K-edge hub on one warp serialised the whole
+// pass); the rest take one warp per row.
 __global__ void k_perm_rows(const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
                             const int64_t *__restrict__ w64, const uint32_t *__restrict__ w32,
                             const uint32_t *__restrict__ perm, const uint32_t *__restrict__ inv,
-                            const int64_t *__restrict__ noff, int64_t nv,
+                            const int64_t *__restrict__ noff, int64_t nv, int64_t nbig,
                             uint32_t *__restrict__ ncol, int64_t *__restrict__ nw64,
                             uint32_t *__restrict__ nw32) {
-  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nv; i += warps) {
+  auto copy = [&](int64_t i, int64_t j0, int64_t step) {
     const uint32_t v = perm[i];
     const int64_t s = off[v], n = off[v + 1] - s, o = noff[i];
-    for (int64_t j = lane_id(); j < n; j += 32) {
+    for (int64_t j = j0; j < n; j += step) {
       ncol[o + j] = inv[col[s + j]];
       if (nw64) nw64[o + j] = w64[s + j];
       if (nw32) nw32[o + j] = w32[s + j];
     }
+  };
+  if (gridDim.y > 1) {  // hub rows: CTA (x, y) takes row x, stride over y
+    if ((int64_t)blockIdx.x < nbig)
+      copy(blockIdx.x, (int64_t)blockIdx.y * blockDim.x + threadIdx.x, (int64_t)gridDim.y * blockDim.x);
+    return;
   }
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = nbig + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < nv; i += warps)
+    copy(i, lane_id(), 32);
 }
 }  // namespace
 
@@ -468,11 +478,14 @@ Relabel &Graph::hot(int64_t K) {
       if (w32.p) h->w32.alloc(ne ? ne : 1);
       h->w64.alloc(want64 && ne ? ne : 1);
     }
-    // one warp per row, no grid-stride cap: the per-row chain of dependent
-    // loads (perm -> off -> col -> inv) needs every warp slot in flight
-    SG_LAUNCH(k_perm_rows, (unsigned)((nv + 7) / 8), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
-              R->perm.p, R->inv.p, h->csr.off.p, nv, h->csr.col.p,
-              want64 ? h->w64.p : nullptr, weighted && w32.p ? h->w32.p : nullptr);
+    const int64_t nbig = std::min<int64_t>(K, 4096);
+    uint32_t *nw32 = weighted && w32.p ? h->w32.p : nullptr;
+    int64_t *nw64 = want64 ? h->w64.p : nullptr;
+    if (nbig)
+      SG_LAUNCH(k_perm_rows, dim3((unsigned)nbig, 16), 256, 0, 0, csr.off.p, csr.col.p, w64.p,
+                w32.p, R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, h->csr.col.p, nw64, nw32);
+    SG_LAUNCH(k_perm_rows, grid_for(nv * 32), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
+              R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, h->csr.col.p, nw64, nw32);
     SG_CUDA(cudaDeviceSynchronize());
   } else {
     SG_CUDA(cudaMemset(h->csr.off.p, 0, sizeof(int64_t)));
