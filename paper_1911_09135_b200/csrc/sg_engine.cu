@@ -612,7 +612,7 @@ constexpr int64_t kRelabelMinV = (int64_t)1 << 20;
 
 // Automatic choice: relabel skewed graphs of >= 2^20 vertices on one device,
 // from the graph's second run on.  Building the relabeled store (degree sort +
-// one renaming pass over the CSR: ~15 ms at rmat24, sg_graph.cu) costs more
+// one renaming pass over the CSR: ~9 ms at rmat24, sg_graph.cu) costs more
 // than one push run gains, so a graph that is created, run once and dropped
 // (the e2e path) keeps its original numbering; resident graphs that are run
 // again amortise it at once.  Without degree skew there is no hot set to
