@@ -8,6 +8,7 @@
 //   generate_rmat / attach_random_weights: numpy PCG64 streams (graph.py:274-305)
 // The LSD radix sort (CUB) is stable, which is what makes these identical.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -373,13 +374,23 @@ __global__ void k_degkey(const int64_t *__restrict__ off, const uint32_t *indeg,
     ids[v] = (uint32_t)v;
   }
 }
+// new id of the hot vertex of degree rank r: r itself, or -- spread, K a
+// multiple of 32 -- line (r mod 32) x (K/32) + r / 32, so the 32 hottest
+// vertices sit in 32 different 128-byte label lines (their reductions land on
+// different L2 slices) while the hot set still packs 32 labels per line
+__host__ __device__ __forceinline__ int64_t hot_pos(int64_t r, int64_t K, bool spread) {
+  return spread ? (r & 31) * (K >> 5) + (r >> 5) : r;
+}
+__host__ __device__ __forceinline__ int64_t hot_rank(int64_t i, int64_t K, bool spread) {
+  return spread ? (i % (K >> 5)) * 32 + i / (K >> 5) : i;
+}
 // the top-K (sorted) ids take [0, K); flag them
-__global__ void k_hot_place(const uint32_t *__restrict__ sorted, int64_t K,
+__global__ void k_hot_place(const uint32_t *__restrict__ sorted, int64_t K, bool spread,
                             uint32_t *__restrict__ perm, uint32_t *__restrict__ cold) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += st) {
-    perm[i] = sorted[i];
-    cold[sorted[i]] = 0u;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < K; r += st) {
+    perm[hot_pos(r, K, spread)] = sorted[r];
+    cold[sorted[r]] = 0u;
   }
 }
 // every other vertex after them, in id order: new id = K + #cold vertices before v
@@ -410,8 +421,8 @@ __global__ void k_perm_rows(const int64_t *__restrict__ off, const uint32_t *__r
                             const int64_t *__restrict__ w64, const uint32_t *__restrict__ w32,
                             const uint32_t *__restrict__ perm, const uint32_t *__restrict__ inv,
                             const int64_t *__restrict__ noff, int64_t nv, int64_t nbig,
-                            uint32_t *__restrict__ ncol, int64_t *__restrict__ nw64,
-                            uint32_t *__restrict__ nw32) {
+                            int64_t K, bool spread, uint32_t *__restrict__ ncol,
+                            int64_t *__restrict__ nw64, uint32_t *__restrict__ nw32) {
   auto copy = [&](int64_t i, int64_t j0, int64_t step) {
     const uint32_t v = perm[i];
     const int64_t s = off[v], n = off[v + 1] - s, o = noff[i];
@@ -421,14 +432,15 @@ __global__ void k_perm_rows(const int64_t *__restrict__ off, const uint32_t *__r
       if (nw32) nw32[o + j] = w32[s + j];
     }
   };
-  if (gridDim.y > 1) {  // hub rows: CTA (x, y) takes row x, stride over y
+  if (gridDim.y > 1) {  // hub rows (degree ranks < nbig): CTA (x, y) takes rank x, stride over y
     if ((int64_t)blockIdx.x < nbig)
-      copy(blockIdx.x, (int64_t)blockIdx.y * blockDim.x + threadIdx.x, (int64_t)gridDim.y * blockDim.x);
+      copy(hot_pos(blockIdx.x, K, spread), (int64_t)blockIdx.y * blockDim.x + threadIdx.x,
+           (int64_t)gridDim.y * blockDim.x);
     return;
   }
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = nbig + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < nv; i += warps)
-    copy(i, lane_id(), 32);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nv; i += warps)
+    if (i >= K || hot_rank(i, K, spread) >= nbig) copy(i, lane_id(), 32);
 }
 }  // namespace
 
@@ -461,7 +473,12 @@ Relabel &Graph::hot(int64_t K) {
     g_launches.fetch_add(1);
     // a = cold flags, b = rank among cold vertices
     SG_LAUNCH(k_fill_u32, grid_for(nv), 256, 0, 0, a.p, nv, 1u);
-    if (K) SG_LAUNCH(k_hot_place, grid_for(K), 256, 0, 0, d.p, K, R->perm.p, a.p);
+    static const bool spread_env = [] {
+      const char *e = std::getenv("SG_HOT_SPREAD");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    const bool spread = spread_env && K < nv && K % 32 == 0 && K >= 1024;
+    if (K) SG_LAUNCH(k_hot_place, grid_for(K), 256, 0, 0, d.p, K, spread, R->perm.p, a.p);
     SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, t2, a.p, b.p, nv));
     SG_LAUNCH(k_cold_place, grid_for(nv), 256, 0, 0, a.p, b.p, nv, K, R->perm.p);
     SG_LAUNCH(k_invert, grid_for(nv), 256, 0, 0, R->perm.p, nv, R->inv.p);
@@ -483,9 +500,10 @@ Relabel &Graph::hot(int64_t K) {
     int64_t *nw64 = want64 ? h->w64.p : nullptr;
     if (nbig)
       SG_LAUNCH(k_perm_rows, dim3((unsigned)nbig, 16), 256, 0, 0, csr.off.p, csr.col.p, w64.p,
-                w32.p, R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, h->csr.col.p, nw64, nw32);
+                w32.p, R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, K, spread, h->csr.col.p, nw64,
+                nw32);
     SG_LAUNCH(k_perm_rows, grid_for(nv * 32), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
-              R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, h->csr.col.p, nw64, nw32);
+              R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, K, spread, h->csr.col.p, nw64, nw32);
     SG_CUDA(cudaDeviceSynchronize());
   } else {
     SG_CUDA(cudaMemset(h->csr.off.p, 0, sizeof(int64_t)));
