@@ -84,6 +84,7 @@ struct BmBfs {
   using E = uint32_t;
   __device__ __forceinline__ E emit_load(uint32_t) const { return 0u; }
   __device__ __forceinline__ void emit_store(uint32_t, uint32_t v, E) const { lab[v] = r + 1; }
+  __device__ __forceinline__ void emit_zero(uint32_t v) const { lab[v] = r + 1; }
 };
 
 // sssp / cc (KIND as OpPair: 0 cc, 1 unit weight, 2 u32 weights, 3 float64 bits)
@@ -167,6 +168,7 @@ struct BmMin {
   using E = L;
   __device__ __forceinline__ E emit_load(uint32_t v) const { return lab[v]; }
   __device__ __forceinline__ void emit_store(uint32_t slot, uint32_t, E x) const { snap[slot] = x; }
+  __device__ __forceinline__ void emit_zero(uint32_t) const {}
 };
 
 // ---------------------------------------------------------------- kernels --
@@ -713,7 +715,18 @@ __global__ void __launch_bounds__(kTB) k_bm_compact(PushArgs a, Op op) {
   uint32_t *q = a.q[0];
   for (uint32_t w0 = ((blockIdx.x * kTB + threadIdx.x) >> 5) * 32; w0 < nwords; w0 += warps * 32) {
     const uint32_t wi = w0 + lane;
-    const uint32_t bits = wi < nwords ? op.take(wi) : 0u;
+    uint32_t bits = wi < nwords ? op.take(wi) : 0u;
+    if (bits && wi * 32u + 31u >= a.zlo) {  // members without out-edges: count, do not queue
+      const uint32_t keep = wi * 32u >= a.zlo ? 0u : (1u << (a.zlo - wi * 32u)) - 1u;
+      uint32_t z = bits & ~keep;
+      bits &= keep;
+      if (z) atomicAdd(&ctl->nzero, (uint32_t)__popc(z));
+      while (z) {
+        const uint32_t b = __ffs(z) - 1;
+        z &= z - 1;
+        op.emit_zero(wi * 32u + b);
+      }
+    }
     const uint32_t cnt = __popc(bits);
     const uint32_t incl = warp_incl_scan(cnt);
     const uint32_t total = __shfl_sync(kFull, incl, 31);

@@ -28,6 +28,9 @@ struct Ctl {
   unsigned long long comm_sent;
   unsigned long long comm_bcast;
   unsigned long long large_edges;  // edges of CTA-bin vertices this round
+  // relabeled store: frontier members with no out-edges (ids >= PushArgs::zlo)
+  // are counted, not queued -- current frontier / next frontier
+  uint32_t fzero, nzero;
   uint32_t part_twc_mask;  // devices>1 accounting: partitions with a non-empty local frontier
   uint32_t part_lb_mask;   // ... whose local frontier holds a huge vertex
 };

@@ -143,6 +143,7 @@ namespace {
 struct Layout {
   const uint32_t *perm = nullptr;  // new -> old
   const uint32_t *inv = nullptr;   // old -> new
+  int64_t zout = -1, zsym = -1;    // first id without out-edges (CSR / symmetrized), -1: none known
 };
 
 __global__ void k_copy_u32(const uint32_t *__restrict__ a, int64_t n, uint32_t *__restrict__ b) {
@@ -167,6 +168,13 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   PushArgs a = rb.push_args(v, thr);
   a.q[1] = a.q[0];  // one frontier array: k_bm_compact rewrites it after the round
+  if (lay.perm && p.devices == 1) {  // relabeled store: edgeless vertices are numbered last
+    const int64_t z = cc ? lay.zsym : lay.zout;
+    if (z >= 0 && z <= nv) {
+      a.zlo = (uint32_t)z;
+      if (cc) a.dense_n = (uint32_t)z;  // round 0 (all of V) skips the isolated tail
+    }
+  }
   a.sched = p.sched == SG_SCHED_LB ? 1 : p.sched == SG_SCHED_VERTEX ? 2 : p.sched == SG_SCHED_EDGE ? 3 : 0;
   long long *tsum = a.sched == 1 || a.sched == 3 ? P.buf<long long>((nv + kFT - 1) / kFT + 1) : nullptr;
   const bool blocked = p.blocked != 0;
@@ -643,7 +651,7 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
     q.source = s;
   }
   run_app_on(*R.g, q, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta,
-             Layout{R.perm.p, R.inv.p});
+             Layout{R.perm.p, R.inv.p, R.zout, R.zsym});
 }
 
 }  // namespace

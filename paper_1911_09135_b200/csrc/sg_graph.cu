@@ -393,12 +393,33 @@ __global__ void k_hot_place(const uint32_t *__restrict__ sorted, int64_t K, bool
     cold[sorted[r]] = 0u;
   }
 }
-// every other vertex after them, in id order: new id = K + #cold vertices before v
-__global__ void k_cold_place(const uint32_t *__restrict__ cold, const uint32_t *__restrict__ rank,
-                             int64_t nv, int64_t K, uint32_t *__restrict__ perm) {
+// every other vertex after them, by class (1: out-degree > 0, 2: out 0 and
+// in > 0, 3: isolated), each class in id order: new id = base[class] + rank
+__global__ void k_cold_class(const int64_t *__restrict__ off, const uint32_t *__restrict__ indeg,
+                             int64_t nv, uint32_t *__restrict__ cls) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st)
-    if (cold[v]) perm[K + rank[v]] = (uint32_t)v;
+    if (cls[v]) cls[v] = off[v + 1] > off[v] ? 1u : indeg[v] ? 2u : 3u;
+}
+__global__ void k_count_nonzero(const uint32_t *__restrict__ x, int64_t n,
+                                unsigned long long *__restrict__ out) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) c += x[i] != 0u;
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31u) == 0 && c) atomicAdd(out, c);
+}
+__global__ void k_class_flag(const uint32_t *__restrict__ cls, int64_t nv, uint32_t c,
+                             uint32_t *__restrict__ flag) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st)
+    flag[v] = cls[v] == c;
+}
+__global__ void k_cold_place(const uint32_t *__restrict__ cls, const uint32_t *__restrict__ rank,
+                             int64_t nv, uint32_t c, int64_t base, uint32_t *__restrict__ perm) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st)
+    if (cls[v] == c) perm[base + rank[v]] = (uint32_t)v;
 }
 __global__ void k_invert(const uint32_t *__restrict__ perm, int64_t nv, uint32_t *__restrict__ inv) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
@@ -458,29 +479,53 @@ Relabel &Graph::hot(int64_t K) {
   h->csr.off.alloc(nv + 1);
   h->csr.col.alloc(ne ? ne : 1);
   if (nv) {
-    DBuf<uint32_t> a(nv), b(nv), c(nv), d(nv);  // indeg/key, ids, sorted keys, sorted ids
+    // a indeg, e key then class, b ids then class rank, c sorted keys then
+    // class flags, d sorted ids
+    DBuf<uint32_t> a(nv), b(nv), c(nv), d(nv), e(nv);
     SG_CUDA(cudaMemset(a.p, 0, sizeof(uint32_t) * nv));
     if (ne) SG_LAUNCH(k_indeg, grid_for(ne), 256, 0, 0, csr.col.p, ne, a.p);
-    SG_LAUNCH(k_degkey, grid_for(nv), 256, 0, 0, csr.off.p, a.p, nv, a.p, b.p);
+    SG_LAUNCH(k_degkey, grid_for(nv), 256, 0, 0, csr.off.p, a.p, nv, e.p, b.p);
     size_t t1 = 0, t2 = 0, t3 = 0;
-    SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, a.p, c.p, b.p, d.p, nv));
-    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, a.p, b.p, nv));
+    SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, e.p, c.p, b.p, d.p, nv));
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, c.p, b.p, nv));
     SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, (int64_t *)nullptr, (int64_t *)nullptr,
                                           nv + 1));
     DBuf<char> t(std::max({t1, t2, t3}));
     // stable: equal degrees keep ascending ids
-    SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, t1, a.p, c.p, b.p, d.p, nv));
+    SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, t1, e.p, c.p, b.p, d.p, nv));
     g_launches.fetch_add(1);
-    // a = cold flags, b = rank among cold vertices
-    SG_LAUNCH(k_fill_u32, grid_for(nv), 256, 0, 0, a.p, nv, 1u);
+    // vertices with any edge (keys sorted descending: the isolated ones are last)
+    unsigned long long nonzero = 0;
+    {
+      DBuf<unsigned long long> cnt(1);
+      SG_CUDA(cudaMemset(cnt.p, 0, sizeof(unsigned long long)));
+      SG_LAUNCH(k_count_nonzero, grid_for(nv), 256, 0, 0, c.p, nv, cnt.p);
+      SG_CUDA(cudaMemcpy(&nonzero, cnt.p, sizeof(nonzero), cudaMemcpyDeviceToHost));
+    }
+    SG_LAUNCH(k_fill_u32, grid_for(nv), 256, 0, 0, e.p, nv, 1u);
     static const bool spread_env = [] {
-      const char *e = std::getenv("SG_HOT_SPREAD");
-      return e ? std::atoi(e) != 0 : true;
+      const char *x = std::getenv("SG_HOT_SPREAD");
+      return x ? std::atoi(x) != 0 : true;
     }();
     const bool spread = spread_env && K < nv && K % 32 == 0 && K >= 1024;
-    if (K) SG_LAUNCH(k_hot_place, grid_for(K), 256, 0, 0, d.p, K, spread, R->perm.p, a.p);
-    SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, t2, a.p, b.p, nv));
-    SG_LAUNCH(k_cold_place, grid_for(nv), 256, 0, 0, a.p, b.p, nv, K, R->perm.p);
+    if (K) SG_LAUNCH(k_hot_place, grid_for(K), 256, 0, 0, d.p, K, spread, R->perm.p, e.p);
+    SG_LAUNCH(k_cold_class, grid_for(nv), 256, 0, 0, csr.off.p, a.p, nv, e.p);
+    int64_t base = K;
+    for (uint32_t cl = 1; cl <= 3; ++cl) {
+      SG_LAUNCH(k_class_flag, grid_for(nv), 256, 0, 0, e.p, nv, cl, c.p);
+      SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, t2, c.p, b.p, nv));
+      SG_LAUNCH(k_cold_place, grid_for(nv), 256, 0, 0, e.p, b.p, nv, cl, base, R->perm.p);
+      uint32_t last_rank = 0, last_flag = 0;
+      SG_CUDA(cudaMemcpy(&last_rank, b.p + nv - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      SG_CUDA(cudaMemcpy(&last_flag, c.p + nv - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      base += (int64_t)last_rank + last_flag;
+      if (cl == 1) R->zout = base;
+      if (cl == 2) R->zsym = base;
+    }
+    if (K == nv) {  // no cold region: a full degree order puts the isolated vertices last
+      R->zout = nv;
+      R->zsym = (int64_t)nonzero;
+    }
     SG_LAUNCH(k_invert, grid_for(nv), 256, 0, 0, R->perm.p, nv, R->inv.p);
     DBuf<int64_t> len(nv + 1);
     SG_LAUNCH(k_perm_len, grid_for(nv), 256, 0, 0, csr.off.p, R->perm.p, nv, len.p);

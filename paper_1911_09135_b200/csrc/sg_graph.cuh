@@ -68,6 +68,10 @@ struct Graph {
 // sets), so runs map the source in and the labels back out (sg_engine.cu).
 struct Relabel {
   int64_t K = 0;
+  // the cold vertices are numbered [out-degree > 0][out 0, in > 0][isolated],
+  // each in id order: ids >= zout have no out-edges (CSR), ids >= zsym none in
+  // the symmetrized graph either (their frontier members are only counted)
+  int64_t zout = 0, zsym = 0;
   DBuf<uint32_t> perm;       // new id -> old id
   DBuf<uint32_t> inv;        // old id -> new id
   std::unique_ptr<Graph> g;  // the relabeled CSR (+ weights, w32)

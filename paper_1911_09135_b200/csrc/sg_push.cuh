@@ -60,6 +60,9 @@ struct PushArgs {
   int no_enqueue;         // partitioned runs: frontiers come from the label exchange
   int sched;              // 0 alb / twc, 1 lb, 2 vertex, 3 edge (round-log launch accounting)
   uint32_t dense_lo, dense_n;  // a dense frontier is [dense_lo, dense_lo + dense_n)
+  // vertices >= zlo have no out-edges in this view (relabeled store: they are
+  // numbered last); the compaction counts them instead of queueing them
+  uint32_t zlo = 0xffffffffu;
   // SG_FLAG_CTA_COUNTS: edges processed per CTA per round ([round][cta_g]), the
   // hardware analogue of the reference's modeled per-CTA counters
   unsigned long long *cta_edges;

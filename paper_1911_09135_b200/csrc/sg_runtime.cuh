@@ -382,15 +382,15 @@ __global__ void k_push_advance(PushArgs a, Loop lp) {
     return;
   }
   const uint32_t round = ctl->round;
-  const uint32_t nn = ctl->nsize;
+  const uint32_t nn = ctl->nsize, nz = ctl->nzero;
   RoundStat &s = a.stats[round];
-  s.frontier_size = ctl->dense ? a.nv : ctl->fsize;
+  s.frontier_size = ctl->dense ? a.nv : ctl->fsize + ctl->fzero;
   s.active_edges = (long long)ctl->edges;
   s.huge_count = ctl->nhuge;
   s.huge_edges = (long long)ctl->huge_edges;
   s.large_count = ctl->nlarge;
   s.large_edges = (long long)ctl->large_edges;
-  s.updated = nn;
+  s.updated = (long long)nn + nz;
   s.comm_sent = (long long)ctl->comm_sent;
   s.comm_broadcast = (long long)ctl->comm_bcast;
   // alb / twc: inspect + twc per non-empty round, lb when huge vertices exist;
@@ -400,13 +400,15 @@ __global__ void k_push_advance(PushArgs a, Loop lp) {
   s.launches_lb = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
   if (a.sched >= 2) s.huge_count = s.large_count = s.large_edges = 0, s.huge_edges = 0;
   ctl->fsize = nn;
+  ctl->fzero = nz;
   ctl->nsize = 0;
+  ctl->nzero = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
   ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_sent = ctl->comm_bcast = 0;
   ctl->dense = 0;
   ctl->ticket = 0;
   ctl->round = round + 1;
-  loop_test(ctl, round, nn == 0, lp);
+  loop_test(ctl, round, nn == 0 && nz == 0, lp);
   __threadfence();
 }
 
