@@ -144,7 +144,13 @@ struct Layout {
   const uint32_t *perm = nullptr;  // new -> old
   const uint32_t *inv = nullptr;   // old -> new
   int64_t zout = -1, zsym = -1;    // first id without out-edges (CSR / symmetrized), -1: none known
+  int64_t zin = -1;                // first id without in-edges (pull layouts), -1: none known
 };
+
+__global__ void k_copy_f64(const double *__restrict__ a, int64_t n, double *__restrict__ b) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) b[i] = a[i];
+}
 
 __global__ void k_copy_u32(const uint32_t *__restrict__ a, int64_t n, uint32_t *__restrict__ b) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
@@ -264,13 +270,19 @@ constexpr int64_t kPrTileBytes = 64ll << 20;  // rank-vector slice per source bl
 constexpr double kPrTileCoverage = 0.6;       // see prep_pr
 
 void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d, int64_t thr,
-             int64_t max_rounds) {
+             int64_t max_rounds, const Layout &lay) {
   const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.csc();
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   PullArgs a = rb.pull_args(v, thr, 0);
   a.vertex = p.sched == SG_SCHED_VERTEX;
+  // relabeled store (in-edge-first order): rows >= zin have no in-edges, so
+  // their rank stays 1 - d from the start (apps.py:162, 180) -- every dense
+  // pass stops at zin; both aux buffers carry their constant aux
+  const uint32_t rows = lay.zin >= 0 && lay.zin <= nv && p.devices == 1 ? (uint32_t)lay.zin
+                                                                         : (uint32_t)nv;
+  a.row_n = rows;
   // devices > 1: CSC-row edge cut; pulls write only owned rows, so comm_sent
   // is 0 and every changed rank is broadcast to its mirrors (engine.py:88-113)
   const Cuts cuts = make_cuts(v, p.devices);
@@ -294,6 +306,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   P.init = [=](Launcher &L, cudaStream_t s) {
     L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
     L.go("init", k_pr_init, grid_n(nv), 256, s, csr_off, nv, omd, inv, labels_d, aux0);
+    if (rows < nv) L.go("init", k_copy_f64, grid_n(nv), 256, s, (const double *)aux0, nv, aux1);
     fill<double>(L, hacc, nv, 0.0, s);
     fill<unsigned long long>(L, gmax, 1, 0ull, s);
     if (vne) {
@@ -304,7 +317,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
       L.go("pr_gain", k_pr_gain_big, sm_info().sms * 4, 256, s, voff, vcol, (const double *)inv,
            (const uint32_t *)gbig, (const uint32_t *)nbig, gmax);
     }
-    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, (uint32_t)nv, thr, largeq, hugeq,
+    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, rows, thr, largeq, hugeq,
          ctl, cuts);
     if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
   };
@@ -348,7 +361,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
       L.go("init", k_tile_store, 1, 1, s, ctl, meta + 4 * B);
       for (int b = 0; b < B; ++b) {
         const PullArgs &x = ab[(size_t)b];
-        L.go("init", k_static_bins, grid_n(nv), 256, s, x.off, 0u, (uint32_t)nv, thr, x.largeq,
+        L.go("init", k_static_bins, grid_n(nv), 256, s, x.off, 0u, rows, thr, x.largeq,
              x.hugeq, ctl, cuts);
         if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, x);
         L.go("init", k_tile_store, 1, 1, s, ctl, meta + 4 * b);
@@ -489,7 +502,7 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
     case SG_APP_BFS:
     case SG_APP_SSSP:
     case SG_APP_CC: prep_push_min(P, g, p, rb, labels_d, thr, max_rounds, lay); break;
-    case SG_APP_PR: prep_pr(P, g, p, rb, labels_d, thr, max_rounds); break;
+    case SG_APP_PR: prep_pr(P, g, p, rb, labels_d, thr, max_rounds, lay); break;
     case SG_APP_KCORE: prep_kcore(P, g, p, rb, labels_d, thr, max_rounds); break;
   }
   cudaStream_t s;
@@ -643,7 +656,8 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
   }
   // the relabeled store is built once per graph (cached like csc / sym) and
   // is not timed; the source is renamed in, the labels renamed out
-  Relabel &R = g.hot(hot_k(g.nv, p.app));
+  const bool pull = p.app == SG_APP_PR || p.app == SG_APP_KCORE;
+  Relabel &R = g.hot(hot_k(g.nv, p.app), pull);
   sg_params q = p;
   if ((p.app == SG_APP_BFS || p.app == SG_APP_SSSP) && p.source >= 0 && p.source < g.nv) {
     uint32_t s = 0;
@@ -651,7 +665,7 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
     q.source = s;
   }
   run_app_on(*R.g, q, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta,
-             Layout{R.perm.p, R.inv.p, R.zout, R.zsym});
+             Layout{R.perm.p, R.inv.p, R.zout, R.zsym, R.zin});
 }
 
 }  // namespace

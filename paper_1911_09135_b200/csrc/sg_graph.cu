@@ -365,12 +365,13 @@ __global__ void k_indeg(const uint32_t *__restrict__ col, int64_t ne, uint32_t *
     atomicAdd(cnt + col[i], 1u);
 }
 // key[v] = total degree (saturating), ids[v] = v
+// key = total degree (saturating); in_first: 0 for vertices without in-edges
 __global__ void k_degkey(const int64_t *__restrict__ off, const uint32_t *indeg, int64_t nv,
-                         uint32_t *key, uint32_t *__restrict__ ids) {  // key may alias indeg
+                         bool in_first, uint32_t *key, uint32_t *__restrict__ ids) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st) {
     const uint64_t d = (uint64_t)(off[v + 1] - off[v]) + indeg[v];
-    key[v] = (uint32_t)(d < 0xffffffffull ? d : 0xffffffffull);
+    key[v] = in_first && !indeg[v] ? 0u : (uint32_t)(d < 0xffffffffull ? d : 0xffffffffull);
     ids[v] = (uint32_t)v;
   }
 }
@@ -465,12 +466,14 @@ __global__ void k_perm_rows(const int64_t *__restrict__ off, const uint32_t *__r
 }
 }  // namespace
 
-Relabel &Graph::hot(int64_t K) {
+Relabel &Graph::hot(int64_t K, bool in_first) {
   K = std::max<int64_t>(0, std::min(K, nv));
-  auto it = hot_.find(K);
+  const int64_t key = 2 * K + (in_first ? 1 : 0);
+  auto it = hot_.find(key);
   if (it != hot_.end()) return *it->second;
   auto R = std::make_unique<Relabel>();
   R->K = K;
+  R->in_first = in_first;
   R->perm.alloc(nv ? nv : 1);
   R->inv.alloc(nv ? nv : 1);
   auto h = std::make_unique<Graph>();
@@ -484,7 +487,7 @@ Relabel &Graph::hot(int64_t K) {
     DBuf<uint32_t> a(nv), b(nv), c(nv), d(nv), e(nv);
     SG_CUDA(cudaMemset(a.p, 0, sizeof(uint32_t) * nv));
     if (ne) SG_LAUNCH(k_indeg, grid_for(ne), 256, 0, 0, csr.col.p, ne, a.p);
-    SG_LAUNCH(k_degkey, grid_for(nv), 256, 0, 0, csr.off.p, a.p, nv, e.p, b.p);
+    SG_LAUNCH(k_degkey, grid_for(nv), 256, 0, 0, csr.off.p, a.p, nv, in_first, e.p, b.p);
     size_t t1 = 0, t2 = 0, t3 = 0;
     SG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, e.p, c.p, b.p, d.p, nv));
     SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, c.p, b.p, nv));
@@ -522,9 +525,10 @@ Relabel &Graph::hot(int64_t K) {
       if (cl == 1) R->zout = base;
       if (cl == 2) R->zsym = base;
     }
-    if (K == nv) {  // no cold region: a full degree order puts the isolated vertices last
+    if (K == nv) {  // no cold region: the zero keys are numbered last
       R->zout = nv;
-      R->zsym = (int64_t)nonzero;
+      R->zsym = in_first ? nv : (int64_t)nonzero;  // isolated vertices
+      R->zin = in_first ? (int64_t)nonzero : -1;   // vertices without in-edges
     }
     SG_LAUNCH(k_invert, grid_for(nv), 256, 0, 0, R->perm.p, nv, R->inv.p);
     DBuf<int64_t> len(nv + 1);
@@ -556,7 +560,7 @@ Relabel &Graph::hot(int64_t K) {
   }
   R->g = std::move(h);
   Relabel &out = *R;
-  hot_[K] = std::move(R);
+  hot_[key] = std::move(R);
   return out;
 }
 

@@ -48,7 +48,7 @@ struct Graph {
   double cov_ = 0.0;
   // hot-vertex relabelings of this graph (built lazily, cached per K; see Relabel)
   std::map<int64_t, std::unique_ptr<Relabel>> hot_;
-  Relabel &hot(int64_t K);
+  Relabel &hot(int64_t K, bool in_first = false);
   int64_t runs = 0;  // single-device runs on this graph (the relabeling is built from the 2nd)
   // share of the edges leaving the top 1 % of vertices by out-degree (cached;
   // rmat skewed: ~0.5, uniform: ~0.03) -- whether a degree relabeling pays
@@ -72,6 +72,10 @@ struct Relabel {
   // each in id order: ids >= zout have no out-edges (CSR), ids >= zsym none in
   // the symmetrized graph either (their frontier members are only counted)
   int64_t zout = 0, zsym = 0;
+  // in_first (the pull layouts): vertices without in-edges are numbered last,
+  // from zin on -- a pull row with no in-edges keeps its initial value
+  bool in_first = false;
+  int64_t zin = -1;
   DBuf<uint32_t> perm;       // new id -> old id
   DBuf<uint32_t> inv;        // old id -> new id
   std::unique_ptr<Graph> g;  // the relabeled CSR (+ weights, w32)
