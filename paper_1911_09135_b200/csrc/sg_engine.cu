@@ -656,8 +656,9 @@ void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_
   }
   // the relabeled store is built once per graph (cached like csc / sym) and
   // is not timed; the source is renamed in, the labels renamed out
-  const bool pull = p.app == SG_APP_PR || p.app == SG_APP_KCORE;
-  Relabel &R = g.hot(hot_k(g.nv, p.app), pull);
+  // pr: vertices without in-edges last (their rows are skipped); kcore keeps
+  // the plain degree order (in-edge-first measured 1.6 % slower there)
+  Relabel &R = g.hot(hot_k(g.nv, p.app), p.app == SG_APP_PR);
   sg_params q = p;
   if ((p.app == SG_APP_BFS || p.app == SG_APP_SSSP) && p.source >= 0 && p.source < g.nv) {
     uint32_t s = 0;
