@@ -399,7 +399,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
 }
 
 void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d,
-                int64_t thr, int64_t max_rounds) {
+                int64_t thr, int64_t max_rounds, const Layout &lay) {
   const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.sym();  // count rows: CSC(sym) and CSR(sym) rows hold the same multiset
   const int64_t nv = v.nv;
@@ -407,6 +407,13 @@ void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *l
   rb.dying.alloc(std::max<int64_t>(nv, 1));
   PullArgs a = rb.pull_args(v, thr, 1);
   a.vertex = p.sched == SG_SCHED_VERTEX;
+  // relabeled store: ids >= zsym are isolated; they die in round 0 (count 0 <
+  // k, apps.py:220-225) with no neighbour to tell, so they are killed at init
+  // and only counted in round 0's log (Ctl::fzero) -- the dense pass stops there
+  const uint32_t rows = lay.zsym >= 0 && lay.zsym <= nv && p.devices == 1 && !a.vertex
+                            ? (uint32_t)lay.zsym
+                            : (uint32_t)nv;
+  a.row_n = rows;
   const Cuts cuts = make_cuts(v, p.devices);  // sym CSC rows == sym CSR rows
   if (p.devices > 1) {
     uint32_t *mc = P.buf<uint32_t>(nv);
@@ -422,6 +429,10 @@ void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *l
   P.init = [=](Launcher &L, cudaStream_t s) {
     L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
     fill<uint8_t>(L, alive, nv, (uint8_t)1, s);
+    if (rows < nv) {
+      fill<uint8_t>(L, alive + rows, nv - rows, (uint8_t)0, s);
+      L.go("init", k_set1<uint32_t>, 1, 1, s, &ctl->fzero, (int64_t)0, (uint32_t)(nv - rows));
+    }
     fill<uint32_t>(L, mark, nv, 0u, s);
     fill<uint32_t>(L, hcnt, nv, 0u, s);
   };
@@ -503,7 +514,7 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
     case SG_APP_SSSP:
     case SG_APP_CC: prep_push_min(P, g, p, rb, labels_d, thr, max_rounds, lay); break;
     case SG_APP_PR: prep_pr(P, g, p, rb, labels_d, thr, max_rounds, lay); break;
-    case SG_APP_KCORE: prep_kcore(P, g, p, rb, labels_d, thr, max_rounds); break;
+    case SG_APP_KCORE: prep_kcore(P, g, p, rb, labels_d, thr, max_rounds, lay); break;
   }
   cudaStream_t s;
   SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

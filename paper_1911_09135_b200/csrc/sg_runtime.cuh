@@ -438,7 +438,7 @@ __global__ void k_kcore_reset(PullArgs a) {
   s.huge_edges = (long long)ctl->huge_edges;
   s.large_count = ctl->nlarge;
   s.large_edges = (long long)ctl->large_edges;
-  s.updated = ctl->ndying;
+  s.updated = (long long)ctl->ndying + ctl->fzero;
   s.comm_sent = 0;
   s.comm_broadcast = (long long)ctl->comm_bcast;
   s.launches_twc = a.cuts.D > 1 ? __popc(ctl->part_twc_mask) : s.frontier_size > 0;
@@ -455,8 +455,9 @@ __global__ void k_kcore_advance(Ctl *ctl, Loop lp) {
     return;
   }
   const uint32_t round = ctl->round;
-  const uint32_t nd = ctl->ndying, nn = ctl->nsize;
+  const uint32_t nd = ctl->ndying + ctl->fzero, nn = ctl->nsize;
   ctl->fsize = nn;
+  ctl->fzero = 0;
   ctl->nsize = 0;
   ctl->ndying = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
