@@ -28,7 +28,11 @@ namespace sg {
 #ifndef SG_BKV
 #define SG_BKV 6
 #endif
-constexpr int kV = SG_BKV;  // edges per lane per step in the bitmap-frontier kernels
+constexpr int kV = SG_BKV;
+#ifndef SG_LB_STEPS
+#define SG_LB_STEPS 4
+#endif
+constexpr int kLBSteps = SG_LB_STEPS;  // relax steps of 32 x kV edges per LB chunk (per bisection)  // edges per lane per step in the bitmap-frontier kernels
 static_assert(kV * 32 <= (int)kLarge, "k_bm_large: a warp step must span <= 2 CTA-bin vertices");
 
 // bfs: frontier vertices of round r carry label r.  vis = visited bitmap
@@ -467,16 +471,14 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
   const int64_t T = (int64_t)gridDim.x * kTB;
   const int64_t tid = (int64_t)blockIdx.x * kTB + threadIdx.x;
   const int64_t passes = (E + T - 1) / T;
-  if (!BLOCKED && a.threshold >= 32 * kV) {
-    // cyclic at warp granularity: warp w takes the 32*kV consecutive edge ids
-    // of chunks w, w + W, w + 2W, ... (consecutive lanes still read
-    // consecutive adjacency entries, the point of the paper's cyclic
-    // distribution).  Every huge vertex owns >= threshold >= 32*kV edges, so
-    // a chunk spans at most two of them: find_owner (worklist.py:96-119) is
-    // one warp-uniform bisection per chunk (broadcast loads), starting at the
-    // previous chunk's owner, and no shared-memory staging is needed for any
-    // number of huge vertices.
-    constexpr int64_t CH = 32 * kV;
+  if (!BLOCKED && a.threshold >= 32 * kV * kLBSteps) {
+    // cyclic at warp granularity: warp w takes the CH consecutive edge ids of
+    // chunks w, w + W, w + 2W, ... (consecutive lanes still read consecutive
+    // adjacency entries, the point of the paper's cyclic distribution).
+    // Every huge vertex owns >= threshold >= CH edges, so a chunk spans at
+    // most two of them: find_owner (worklist.py:96-119) is one warp-uniform
+    // two-level bisection per chunk, amortised over kLBSteps relax steps.
+    constexpr int64_t CH = 32 * kV * kLBSteps;
     const int64_t nwarps = T >> 5, nch = (E + CH - 1) / CH;
     const uint32_t lane = lane_id();
     const Coarse cx = coarse_build(spre, a.hpre, nh);  // spre: >= kCoarse entries
@@ -486,19 +488,23 @@ __global__ void __launch_bounds__(kTB) k_bm_lb(PushArgs a, Op op) {
       const int64_t x0 = o ? a.hpre[o - 1] : 0, x1 = a.hpre[o];
       const int64_t s0 = a.hstart[o], s1 = o + 1 < nh ? a.hstart[o + 1] : 0;
       const L v0 = (L)a.hval[o], v1 = o + 1 < nh ? (L)a.hval[o + 1] : L(0);
-      int64_t e[kV];
-      bool ok[kV];
-      L sv[kV];
+      for (int st = 0; st < kLBSteps; ++st) {
+        const int64_t gs = g0 + (int64_t)st * 32 * kV;
+        if (gs >= E) break;
+        int64_t e[kV];
+        bool ok[kV];
+        L sv[kV];
 #pragma unroll
-      for (int u = 0; u < kV; ++u) {
-        const int64_t g = g0 + u * 32 + lane;
-        ok[u] = g < E;
-        const bool second = g >= x1;
-        e[u] = second ? s1 + (g - x1) : s0 + (g - x0);
-        sv[u] = second ? v1 : v0;
+        for (int u = 0; u < kV; ++u) {
+          const int64_t g = gs + u * 32 + lane;
+          ok[u] = g < E;
+          const bool second = g >= x1;
+          e[u] = second ? s1 + (g - x1) : s0 + (g - x0);
+          sv[u] = second ? v1 : v0;
+        }
+        if (a.cta_edges) my_proc += count_ok(ok);
+        op.relax(a, e, ok, sv);
       }
-      if (a.cta_edges) my_proc += count_ok(ok);
-      op.relax(a, e, ok, sv);
     }
     cta_flush(a, my_proc, ctl->round);
     return;
