@@ -719,7 +719,11 @@ __global__ void __launch_bounds__(kTB) k_bm_compact(PushArgs a, Op op) {
   const uint32_t nwords = (a.nv + 31) / 32, lane = lane_id();
   const uint32_t warps = (gridDim.x * kTB) >> 5;
   uint32_t *q = a.q[0];
-  for (uint32_t w0 = ((blockIdx.x * kTB + threadIdx.x) >> 5) * 32; w0 < nwords; w0 += warps * 32) {
+  // warp-major over CTAs: consecutive 32-word blocks go to different CTAs
+  // (SMs), so a dense run of frontier bits -- the relabeled hot set -- is
+  // spread over the chip instead of the first few CTAs
+  const uint32_t gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  for (uint32_t w0 = gw * 32; w0 < nwords; w0 += warps * 32) {
     const uint32_t wi = w0 + lane;
     uint32_t bits = wi < nwords ? op.take(wi) : 0u;
     if (bits && wi * 32u + 31u >= a.zlo) {  // members without out-edges: count, do not queue
