@@ -141,18 +141,6 @@ __device__ __forceinline__ uint32_t owner_search(const int64_t *pre, uint32_t n,
   return lo;
 }
 
-// upper_bound over [lo, n): first i >= lo with pre[i] > g (pre[lo-1] <= g known)
-__device__ __forceinline__ uint32_t owner_search_from(const int64_t *pre, uint32_t lo, uint32_t n,
-                                                      int64_t g) {
-  uint32_t hi = n - 1;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (g < pre[mid]) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
-
 // Two-level find_owner for the LB kernels' chunk bisection: a shared-memory
 // sample of the huge prefix (every stride-th block end, <= kCoarse entries)
 // narrows the search to one stride-long block before the global-memory steps
