@@ -251,6 +251,45 @@ __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
   cta_flush(a, my_proc, ctl->round);
 }
 
+// ALB's PrefixWork (worklist.py:68-93) of the huge vertices the inspection
+// queued, by one CTA of any size: hstart, inclusive hpre, ctl->huge_edges.
+// The CTA-bin kernel's CTA 0 runs it before its batches (a.prefix_in_large),
+// which saves the round a kernel node; the LB kernel runs after the CTA bin.
+template <class Op>
+__device__ void huge_prefix_cta(const PushArgs &a, Op &op) {
+  __shared__ long long red[32];
+  __shared__ long long carry;
+  Ctl *ctl = a.ctl;
+  const uint32_t n = ctl->nhuge;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t b = 0; b < n; b += blockDim.x) {
+    const uint32_t i = b + threadIdx.x;
+    long long d = 0;
+    if (i < n) {
+      const uint32_t v = a.hugeq[i];
+      const int64_t s0 = a.off[v];
+      a.hstart[i] = s0;
+      d = a.off[v + 1] - s0;
+      if (!Op::kCarry) a.hval[i] = (unsigned long long)op.src_val(i, v);
+    }
+    const long long x = warp_incl_scan(d);
+    if (lane_id() == 31) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const long long y = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+      red[threadIdx.x] = warp_incl_scan(y);
+    }
+    __syncthreads();
+    const long long wpre = (threadIdx.x >> 5) ? red[(threadIdx.x >> 5) - 1] : 0;
+    if (i < n) a.hpre[i] = carry + wpre + x;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += wpre + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ctl->huge_edges = (unsigned long long)carry;
+}
+
 // TWC CTA bin: block-level gather over batches of kBatch queued vertices
 template <class Op>
 __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
@@ -259,6 +298,7 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
   using L = typename Op::L;
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
+  if (a.prefix_in_large && blockIdx.x == 0 && ctl->nhuge) huge_prefix_cta(a, op);
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
@@ -336,6 +376,7 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
   using W = typename Op::W;
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
+  if (a.prefix_in_large && blockIdx.x == 0 && ctl->nhuge) huge_prefix_cta(a, op);
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);
@@ -421,6 +462,7 @@ __global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
   __shared__ uint32_t item;
   Ctl *ctl = a.ctl;
   if (ctl->done) return;
+  if (a.prefix_in_large && blockIdx.x == 0 && ctl->nhuge) huge_prefix_cta(a, op);
   const uint32_t n = ctl->nlarge;
   if (!n) return;
   op.begin(ctl->round);

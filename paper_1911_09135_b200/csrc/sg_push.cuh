@@ -63,6 +63,7 @@ struct PushArgs {
   // vertices >= zlo have no out-edges in this view (relabeled store: they are
   // numbered last); the compaction counts them instead of queueing them
   uint32_t zlo = 0xffffffffu;
+  int prefix_in_large = 0;  // the CTA-bin kernel's CTA 0 builds the huge prefix (no k_huge_prefix)
   // SG_FLAG_CTA_COUNTS: edges processed per CTA per round ([round][cta_g]), the
   // hardware analogue of the reference's modeled per-CTA counters
   unsigned long long *cta_edges;

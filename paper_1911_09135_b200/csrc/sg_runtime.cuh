@@ -46,6 +46,9 @@ inline int grid_n(int64_t n, int block = 256) {
 #ifndef SG_PDL
 #define SG_PDL 1
 #endif
+#ifndef SG_PREFIX_IN_LARGE
+#define SG_PREFIX_IN_LARGE 1
+#endif
 struct Launcher {
   bool profile = false;
   std::vector<std::tuple<const char *, cudaEvent_t, cudaEvent_t>> pending;
@@ -600,17 +603,20 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
       c.L.go("compact", k_bm_compact<Op>, occupancy_grid(k_bm_compact<Op>, kTB), kTB, c.s, a, op);
     return;
   }
+  // the huge prefix is built by the CTA-bin kernel's CTA 0 (one node fewer)
+  PushArgs a2 = a;
+  a2.prefix_in_large = SG_PREFIX_IN_LARGE && a.threshold != kNoHuge;
   c.L.go_pdl("push_twc", k_bm_twc<Op>, occupancy_grid(k_bm_twc<Op>, kTB), kTB, c.s, a, op);
   if (classic)
     c.L.go_pdl("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
-           c.s, a, op);
+           c.s, a2, op);
   else if (SG_LARGE_PIPE)
     c.L.go_pdl("push_large", k_bm_large_pipe<Op>, occupancy_grid(k_bm_large_pipe<Op>, kTB), kTB, c.s,
-           a, op);
+           a2, op);
   else
-    c.L.go_pdl("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a, op);
+    c.L.go_pdl("push_large", k_bm_large<Op>, occupancy_grid(k_bm_large<Op>, kTB), kTB, c.s, a2, op);
   if (a.threshold != kNoHuge) {
-    c.L.go_pdl("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
+    if (!a2.prefix_in_large) c.L.go_pdl("huge_prefix", k_huge_prefix<Op>, 1, 1024, c.s, a, op);
     if (blocked)
       c.L.go_pdl("push_lb", k_bm_lb<Op, true>, occupancy_grid(k_bm_lb<Op, true>, kTB), kTB, c.s, a, op);
     else
