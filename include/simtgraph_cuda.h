@@ -170,6 +170,9 @@ int sg_run_profiled(sg_graph *g, const sg_params *p, double *labels_out, sg_roun
  * rank's aux / rank rows; kcore all-reduces alive flags (min) and neighbour
  * marks (max).  labels_out receives the merged labels on every rank. */
 int sg_nccl_unique_id(uint8_t id_out[128]);
+/* sg_dist_run keeps one NCCL communicator per (id, rank, world) across calls
+ * (a unique id bootstraps one communicator); sg_nccl_release destroys them. */
+void sg_nccl_release(void);
 int sg_dist_run(sg_graph *g, const sg_params *p, const uint8_t nccl_id[128], int32_t rank,
                 int32_t world, double *labels_out, sg_round *rounds_out, int64_t rounds_cap,
                 int64_t *nrounds, double *ms_out);

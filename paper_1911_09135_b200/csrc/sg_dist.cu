@@ -23,6 +23,10 @@
 //     libnccl is dlopen'ed (preferring the copy torch already loaded), so the
 //     single-GPU library has no NCCL dependency.
 // bfs runs as unit-weight relaxation (OpPair<1>): identical labels and rounds.
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
 #include <thread>
 
 #include "sg_comm.cuh"
@@ -724,15 +728,43 @@ int sg_nccl_unique_id(uint8_t id_out[128]) {
   });
 }
 
+namespace sg {
+namespace {
+// One NCCL communicator per (unique id, rank, world), created on first use and
+// reused by every later run: an ncclUniqueId bootstraps exactly one
+// communicator (its root listener serves one init), and init costs far more
+// than a BSP run.  Deliberately leaked at exit (destroying communicators after
+// the CUDA runtime has torn down is unsafe); sg_nccl_release frees them.
+std::mutex g_comm_mu;
+std::map<std::string, std::unique_ptr<NcclComm>> *g_comms = new std::map<std::string, std::unique_ptr<NcclComm>>();
+
+NcclComm &cached_comm(const uint8_t id[128], int rank, int world) {
+  std::string key(reinterpret_cast<const char *>(id), 128);
+  key += ":" + std::to_string(rank) + "/" + std::to_string(world);
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  auto it = g_comms->find(key);
+  if (it == g_comms->end())
+    it = g_comms->emplace(key, std::make_unique<NcclComm>(id, rank, world)).first;
+  return *it->second;
+}
+}  // namespace
+}  // namespace sg
+
 int sg_dist_run(sg_graph *gh, const sg_params *p, const uint8_t nccl_id[128], int32_t rank,
                 int32_t world, double *labels_out, sg_round *rounds_out, int64_t rounds_cap,
                 int64_t *nrounds, double *ms_out) {
   return sg::guard([&] {
     if (world < 1 || world > sg::kMaxParts || rank < 0 || rank >= world)
       throw Error(SG_ECONFIG, "bad rank / world size");
-    sg::NcclComm comm(nccl_id, rank, world);
+    sg::NcclComm &comm = sg::cached_comm(nccl_id, rank, world);
     sg::dist_run_rank(*gh->g, *p, comm, labels_out, rounds_out, rounds_cap, nrounds, ms_out);
   });
+}
+
+void sg_nccl_release(void) {
+  std::lock_guard<std::mutex> lk(sg::g_comm_mu);
+  cudaDeviceSynchronize();
+  sg::g_comms->clear();
 }
 
 int sg_dist_run_threads(sg_graph *gh, const sg_params *p, int32_t world, double *labels_out,

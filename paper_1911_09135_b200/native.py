@@ -31,7 +31,7 @@ EXPORTS = (
     "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run", "sg_dist_run_threads",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
     "sg_host_alloc", "sg_host_free", "sg_release_cached", "sg_run_cta_counts",
-    "sg_graph_load_sgb1",
+    "sg_graph_load_sgb1", "sg_nccl_release",
 )
 
 
@@ -103,6 +103,7 @@ def load(path: Path | None = None):
             "sg_host_free": ([P], None),
             "sg_release_cached": ([], None),
             "sg_graph_load_sgb1": ([ctypes.c_char_p, pp], ctypes.c_int),
+            "sg_nccl_release": ([], None),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

@@ -454,3 +454,21 @@ def test_relabel_edge_cases(sg, golden, O):
     lab, log = O.run(off, tgt, w, "sssp")
     assert O.labels_sha256(labels) == O.labels_sha256(lab)
     assert rounds == [[r.frontier_size, r.active_edges] for r in log]
+
+
+def test_nccl_communicator_reused_across_runs(sg, golden):
+    """sg_dist_run keeps one communicator per (id, rank, world): repeated runs
+    with the same unique id (the bench's warm-up / timed steps) reuse it --
+    an id bootstraps only one communicator -- and sg_nccl_release frees them."""
+    from paper_1911_09135_b200 import native
+    g = sg.attach_random_weights(_graph(sg, "rmat12"), 2)
+    info = golden["runs"]["rmat12"]["sssp/alb/d1"]
+    p = sg.engine._device_params(sg.apps.make_app("sssp"), sg.Scheduler("alb"),
+                                 sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
+    nid = native.nccl_unique_id()
+    for _ in range(3):
+        labels, log, _ = native.dist_run(g.device(), p, nid, 0, 1)
+        assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
+    native.load().sg_nccl_release()
+    labels, log, _ = native.dist_run(g.device(), p, native.nccl_unique_id(), 0, 1)
+    assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
