@@ -715,19 +715,6 @@ void run_push_local_partitions(Graph &g, const sg_params &p, int64_t thr, int64_
 
 }  // namespace sg
 
-using sg::Error;
-
-extern "C" {
-
-int sg_nccl_unique_id(uint8_t id_out[128]) {
-  return sg::guard([&] {
-    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-    ncclUniqueId id;
-    SG_NCCL(sg::nccl().getUniqueId(&id));
-    std::memcpy(id_out, &id, 128);
-  });
-}
-
 namespace sg {
 namespace {
 // One NCCL communicator per (unique id, rank, world), created on first use and
@@ -749,6 +736,20 @@ NcclComm &cached_comm(const uint8_t id[128], int rank, int world) {
 }
 }  // namespace
 }  // namespace sg
+
+using sg::Error;
+
+extern "C" {
+
+int sg_nccl_unique_id(uint8_t id_out[128]) {
+  return sg::guard([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    SG_NCCL(sg::nccl().getUniqueId(&id));
+    std::memcpy(id_out, &id, 128);
+  });
+}
+
 
 int sg_dist_run(sg_graph *gh, const sg_params *p, const uint8_t nccl_id[128], int32_t rank,
                 int32_t world, double *labels_out, sg_round *rounds_out, int64_t rounds_cap,
