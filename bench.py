@@ -17,6 +17,10 @@ BSP run (all rounds to convergence) of the device engine.
 * e2e    : the same metric through the C ABI with HOST buffers: per step
            sg_graph_create from pinned CSR/weights (H2D) + sg_run + labels /
            round log D2H, wall clock with device sync.
+* layout : the resident graph is re-run, so from the second warm-up run on the
+           engine uses its hot-vertex relabeled store (labels and
+           round logs in the reference's numbering); e2e builds a fresh graph
+           every step, which is run once in its original numbering.
 * roofline: dominant kernel of a profiled run (sg_run_profiled: CUDA events
            around every kernel) — algorithmic bytes / its time,
            against MEASURED_PEAKS.json hbm_gbs.
