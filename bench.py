@@ -223,7 +223,7 @@ def make_graph_device(sg, app, scale, uniform):
 
 def run_params(sg, app, sched_kind, threshold, nv, classic=False):
     sched = sg.Scheduler(sched_kind, threshold=threshold if sched_kind == "alb" else None)
-    p = sg.engine._device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), 1, 10 * nv + 256)
+    p = sg.engine.device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), 1, 10 * nv + 256)
     if classic:
         p.flags |= 4  # SG_FLAG_TWC_CLASSIC
     return sched, p

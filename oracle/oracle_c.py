@@ -119,3 +119,46 @@ def csr_from_pairs(src, dst, nv, weights=None):
         w_out = np.empty(len(src), dtype=np.int64)
     L.sgo_csr_from_pairs(len(src), nv, _p(src), _p(dst), _p(weights), _p(off), _p(tgt), _p(w_out))
     return off, tgt, w_out
+
+
+def _sig(name, args):
+    L = lib()
+    fn = getattr(L, name)
+    if not getattr(fn, "_sg_sig", False):
+        fn.argtypes = args
+        fn.restype = None
+        fn._sg_sig = True
+    return fn
+
+
+def transpose(off, tgt):
+    """Stable CSC of a CSR (== Graph.csc(), graph.py:95-113), in C."""
+    P = ctypes.c_void_p
+    nv = len(off) - 1
+    toff = np.empty(nv + 1, dtype=np.int64)
+    ttgt = np.empty(len(tgt), dtype=np.int32)
+    _sig("sgo_transpose", [ctypes.c_int64, P, P, P, P])(
+        nv, _p(np.ascontiguousarray(off, dtype=np.int64)),
+        _p(np.ascontiguousarray(tgt, dtype=np.int32)), _p(toff), _p(ttgt))
+    return toff, ttgt
+
+
+def symmetrize(off, tgt, coff=None, ctgt=None, threads=0):
+    """Symmetrized CSR (== Graph.symmetrized(), graph.py:115-128), in C."""
+    P = ctypes.c_void_p
+    if coff is None:
+        coff, ctgt = transpose(off, tgt)
+    nv = len(off) - 1
+    soff = np.empty(nv + 1, dtype=np.int64)
+    stgt = np.empty(len(tgt) + len(ctgt), dtype=np.int32)
+    _sig("sgo_symmetrize", [ctypes.c_int64, P, P, P, P, P, P, ctypes.c_int])(
+        nv, _p(off), _p(tgt), _p(coff), _p(ctgt), _p(soff), _p(stgt),
+        threads or (os.cpu_count() or 1))
+    return soff, stgt
+
+
+def rmat_csr(scale, edge_factor=16, seed=1, probs=(0.57, 0.19, 0.19, 0.05), threads=0):
+    """generate_rmat's CSR (graph.py:274-298) built in C (multi-threaded stream)."""
+    src, dst = rmat_pairs(scale, edge_factor, seed, probs, threads)
+    off, tgt, _ = csr_from_pairs(src, dst, 1 << scale)
+    return off, tgt

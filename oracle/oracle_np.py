@@ -217,7 +217,8 @@ def lb_kernel(off, tgt, w, huge, cum, values, out, aux, op, blocked, ctas, tpb, 
 # ----------------------------------------------------------------------------
 
 class Round:
-    __slots__ = ("frontier_size", "active_edges", "comm_sent", "comm_broadcast", "lb_launches")
+    __slots__ = ("frontier_size", "active_edges", "comm_sent", "comm_broadcast", "lb_launches",
+                 "pce", "accesses", "launches")
 
     def __init__(self, n):
         self.frontier_size = n
@@ -225,10 +226,18 @@ class Round:
         self.comm_sent = 0
         self.comm_broadcast = 0
         self.lb_launches = 0
+        self.pce = []          # per-device per-CTA edge arrays (simt.py:73-90)
+        self.accesses = 0      # modeled search accesses (lb kernel)
+        self.launches = {}     # kernel name -> launches (schedulers.py:252-298)
 
     def as_list(self):
         return [self.frontier_size, self.active_edges, self.comm_sent, self.comm_broadcast,
                 self.lb_launches]
+
+    def cta_cv(self):
+        e = np.concatenate(self.pce) if self.pce else np.zeros(0)
+        m = e.mean() if len(e) else 0.0
+        return float(e.std() / m) if m > 0 else 0.0
 
 
 def edge_cut(off, tgt, devices):
@@ -251,44 +260,64 @@ def edge_cut(off, tgt, devices):
 
 
 def alb_round(off, tgt, w, frontier, values, out, aux, op, threshold, ctas, tpb, ws,
-              kind="alb", blocked=False):
-    """schedulers.run_round for every scheduler kind (schedulers.py:252-298)."""
+              kind="alb", blocked=False, K=None, rec=None):
+    """schedulers.run_round for every scheduler kind (schedulers.py:252-298).
+
+    ``K`` is a module with the plugin's four kernels (default: this file's
+    restatement; tests pass ``paper_1911_09135_b200.cuda_backend``); ``rec``
+    collects per-CTA edges, search accesses and launches like RoundMetrics."""
+    import sys
+    K = K or sys.modules[__name__]
     pce = np.zeros(ctas, dtype=np.int64)
     pwp = np.zeros(ctas * tpb // ws, dtype=np.int64)
     lb = 0
+    acc = 0
+    launches = {}
+
+    def launch(name):
+        launches[name] = launches.get(name, 0) + 1
+
     deg = off[frontier + 1] - off[frontier]
-    if kind == "vertex":
-        vertex_kernel(off, tgt, w, frontier, values, out, aux, op, ctas, tpb, pce)
-        return int(pce.sum()), 0
-    if kind == "edge":
-        edge_kernel(off, tgt, w, frontier, values, out, aux, op, ctas, tpb, pce)
-        return int(pce.sum()), 0
-    if kind == "lb":
+    if kind in ("vertex", "edge"):
+        launch(kind)
+        (K.vertex_kernel if kind == "vertex" else K.edge_kernel)(
+            off, tgt, w, frontier, values, out, aux, op, ctas, tpb, pce)
+    elif kind == "lb":
         cum = np.cumsum(deg, dtype=np.int64)
         if len(cum) and cum[-1] > 0:
-            lb_kernel(off, tgt, w, frontier, cum, values, out, aux, op, blocked, ctas, tpb, ws,
-                      pce, pwp)
-            lb = 1
-        return int(pce.sum()), lb
-    if kind == "alb":
-        big = deg >= threshold
-        huge, rest, rdeg = frontier[big], frontier[~big], deg[~big]
-        if len(huge):
-            cum = np.cumsum(off[huge + 1] - off[huge], dtype=np.int64)
-            lb_kernel(off, tgt, w, huge, cum, values, out, aux, op, blocked, ctas, tpb, ws, pce, pwp)
+            launch("lb")
+            acc += int(K.lb_kernel(off, tgt, w, frontier, cum, values, out, aux, op, blocked,
+                                   ctas, tpb, ws, pce, pwp))
             lb = 1
     else:
-        rest, rdeg = frontier, deg
-    small = rdeg < ws
-    large = rdeg >= tpb
-    twc_kernel(off, tgt, w, rest[small], rest[~small & ~large], rest[large], values, out, aux,
-               op, ctas, tpb, ws, pce)
+        launch("inspect")
+        if kind == "alb":
+            big = deg >= threshold
+            huge, rest, rdeg = frontier[big], frontier[~big], deg[~big]
+            if len(huge):
+                cum = np.cumsum(off[huge + 1] - off[huge], dtype=np.int64)
+                launch("lb")
+                acc += int(K.lb_kernel(off, tgt, w, huge, cum, values, out, aux, op, blocked,
+                                       ctas, tpb, ws, pce, pwp))
+                lb = 1
+        else:
+            rest, rdeg = frontier, deg
+        small = rdeg < ws
+        large = rdeg >= tpb
+        launch("twc")
+        K.twc_kernel(off, tgt, w, rest[small], rest[~small & ~large], rest[large], values, out,
+                     aux, op, ctas, tpb, ws, pce)
+    if rec is not None:
+        rec.pce.append(pce)
+        rec.accesses += acc
+        for k, n in launches.items():
+            rec.launches[k] = rec.launches.get(k, 0) + n
     return int(pce.sum()), lb
 
 
 def run(off, tgt, weights, app, *, source=0, k=2, damping=0.85, tol=1e-6, kind="alb",
         threshold=None, blocked=False, ctas=84, tpb=256, ws=32, devices=1, max_rounds=None,
-        directed_off=None, directed_tgt=None):
+        directed_off=None, directed_tgt=None, K=None):
     """engine.run for one app over the graph ``(off, tgt, weights)``.
 
     For cc / kcore pass the SYMMETRIZED graph (engine.py:195).  For pr pass the
@@ -367,7 +396,7 @@ def run(off, tgt, weights, app, *, source=0, k=2, damping=0.85, tol=1e-6, kind="
             local = frontier[np.searchsorted(frontier, a):np.searchsorted(frontier, b)]
             if len(local):
                 m, lb = alb_round(voff, vtgt, vw, local, values, out, aux, op, threshold,
-                                  ctas, tpb, ws, kind, blocked)
+                                  ctas, tpb, ws, kind, blocked, K, rec)
                 rec.active_edges += m
                 rec.lb_launches += lb
             outs.append(out)

@@ -278,3 +278,39 @@ void sgo_csr_from_pairs(int64_t ne, int64_t nv, const int32_t *src, const int32_
   }
   free(cur);
 }
+
+/* Graph.csc() (graph.py:95-113): stable transpose.  Row v of the result lists
+ * the sources of v's in-edges in CSR edge order (a sequential scatter over
+ * the CSR is the stable counting sort). */
+void sgo_transpose(int64_t nv, const int64_t *off, const int32_t *tgt, int64_t *toff,
+                   int32_t *ttgt) {
+  int64_t ne = off[nv];
+  memset(toff, 0, sizeof(int64_t) * (size_t)(nv + 1));
+  for (int64_t e = 0; e < ne; ++e) toff[tgt[e] + 1]++;
+  for (int64_t v = 0; v < nv; ++v) toff[v + 1] += toff[v];
+  int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nv ? nv : 1));
+  memcpy(cur, toff, sizeof(int64_t) * (size_t)nv);
+  for (int64_t u = 0; u < nv; ++u)
+    for (int64_t e = off[u]; e < off[u + 1]; ++e) ttgt[cur[tgt[e]]++] = (int32_t)u;
+  free(cur);
+}
+
+/* Graph.symmetrized() (graph.py:115-128): from_edges(src ++ dst, dst ++ src)
+ * stable-sorted by source gives row v = CSR row v ++ CSC row v. */
+void sgo_symmetrize(int64_t nv, const int64_t *off, const int32_t *tgt, const int64_t *coff,
+                    const int32_t *ctgt, int64_t *soff, int32_t *stgt, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  soff[0] = 0;
+  for (int64_t v = 0; v < nv; ++v)
+    soff[v + 1] = soff[v] + (off[v + 1] - off[v]) + (coff[v + 1] - coff[v]);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < nv; ++v) {
+    int64_t p = soff[v];
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) stgt[p++] = tgt[e];
+    for (int64_t e = coff[v]; e < coff[v + 1]; ++e) stgt[p++] = ctgt[e];
+  }
+}

@@ -10,7 +10,7 @@ hand-written sm_100a CUDA kernels through libsimtgraph_cuda.so.
     r = simtgraph.engine.run_app(g, "bfs", simtgraph.schedulers.Scheduler("alb"))
 """
 
-from . import apps, engine, errors, graph, kernels, schedulers, simt, worklist  # noqa: F401
+from . import apps, engine, errors, graph, kernels, schedulers, simt  # noqa: F401
 from .engine import report, run, run_app  # noqa: F401
 from .graph import Graph, attach_random_weights, generate_rmat, load_graph  # noqa: F401
 from .schedulers import Scheduler  # noqa: F401

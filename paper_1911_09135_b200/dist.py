@@ -2,7 +2,7 @@
 
 The reference simulates devices in one process (engine.py:64-113, 215-234);
 here each rank owns one contiguous edge-balanced row block of the traversal
-view (the same cuts as ``engine.make_partition``), runs the ALB round on its
+view (the same cuts as ``engine.edge_cut_bounds``), runs the ALB round on its
 local frontier, and ``sg_dist_run`` exchanges labels with ncclAllReduce(min)
 plus a device-side diff and an all-reduced quiescence counter.  torch is only
 plumbing here: the process group shares the 128-byte NCCL id and reduces the
@@ -17,7 +17,7 @@ import numpy as np
 
 from . import native
 from .apps import make_app
-from .engine import RunResult, _device_params, _records_from_log
+from .engine import RunResult, device_params, records_from_log
 from .errors import ConfigError
 from .schedulers import Scheduler
 from .simt import KernelConfig
@@ -61,9 +61,9 @@ def run_app(graph, app_name: str, scheduler: Scheduler = Scheduler("alb"),
     app = make_app(app_name, **params)
     if max_rounds is None:
         max_rounds = 10 * max(graph.num_vertices, 1) + 256
-    p = _device_params(app, scheduler, config, world, max_rounds)
+    p = device_params(app, scheduler, config, world, max_rounds)
     labels, log, ms = native.dist_run(graph.device(), p, nccl_id, rank, world)
-    return RunResult(labels=labels, records=_records_from_log(log, scheduler, config),
+    return RunResult(labels=labels, records=records_from_log(log, scheduler, config),
                      app_name=app.name, scheduler=scheduler, config=config, devices=world,
                      num_vertices=graph.num_vertices, num_edges=graph.num_edges,
                      device_ms=ms, round_log=log)
@@ -76,15 +76,15 @@ def run_app_threads(graph, app_name: str, scheduler: Scheduler = Scheduler("alb"
     app = make_app(app_name, **params)
     if max_rounds is None:
         max_rounds = 10 * max(graph.num_vertices, 1) + 256
-    p = _device_params(app, scheduler, config, world, max_rounds)
+    p = device_params(app, scheduler, config, world, max_rounds)
     labels, log, ms = native.dist_run_threads(graph.device(), p, world)
-    return RunResult(labels=labels, records=_records_from_log(log, scheduler, config),
+    return RunResult(labels=labels, records=records_from_log(log, scheduler, config),
                      app_name=app.name, scheduler=scheduler, config=config, devices=world,
                      num_vertices=graph.num_vertices, num_edges=graph.num_edges,
                      device_ms=ms, round_log=log)
 
 
 def partition_bounds(offsets: np.ndarray, world: int):
-    """Row blocks [start, end) per rank — identical to engine.make_partition."""
+    """Row blocks [start, end) per rank — identical to the reference's make_partition."""
     from .engine import edge_cut_bounds
     return edge_cut_bounds(offsets, world)

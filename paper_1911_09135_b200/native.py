@@ -21,6 +21,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsimtgraph_cuda.so"
 
 SG_OK, SG_ECONFIG, SG_ERANGE, SG_ECONVERGE, SG_ECUDA, SG_ENOMEM = 0, -1, -2, -3, -4, -5
 SG_EPARSE, SG_EIO = -6, -7
+FLAG_TIMING, FLAG_PROFILE, FLAG_TWC_CLASSIC, FLAG_RELABEL, FLAG_NO_RELABEL = 1, 2, 4, 8, 16
 APP_IDS = {"bfs": 0, "sssp": 1, "cc": 2, "pr": 3, "kcore": 4}
 SCHED_IDS = {"alb": 0, "twc": 1, "lb": 2, "vertex": 3, "edge": 4}
 
@@ -259,22 +260,28 @@ class DeviceGraph:
 
     def run(self, params: Params, rounds_cap=1 << 16, profile=False):
         """Run the BSP loop on the device.  Returns (labels, round log, ms) or,
-        with ``profile``, (labels, round log, ms, {kernel: (launches, ms)})."""
+        with ``profile``, (labels, round log, ms, {kernel: (launches, ms)}).
+        A run longer than ``rounds_cap`` rounds is repeated with a log large
+        enough for all of it (runs are deterministic), never truncated."""
         nv, _, _ = self.info()
         labels = pinned_empty(nv, np.float64)
-        rounds = np.zeros(rounds_cap, dtype=ROUND_DTYPE)
-        n = ctypes.c_int64(0)
-        ms = ctypes.c_double(0.0)
-        kt = (KernelTime * 64)()
-        nkt = ctypes.c_int32(0)
-        if profile:
-            code = load().sg_run_profiled(self.handle, ctypes.byref(params), ptr(labels),
-                                          ptr(rounds), rounds_cap, ctypes.byref(n),
-                                          ctypes.byref(ms), kt, 64, ctypes.byref(nkt))
-        else:
-            code = load().sg_run(self.handle, ctypes.byref(params), ptr(labels), ptr(rounds),
-                                 rounds_cap, ctypes.byref(n), ctypes.byref(ms))
-        log = rounds[: min(n.value, rounds_cap)].copy()
+        while True:
+            rounds = np.zeros(max(int(rounds_cap), 1), dtype=ROUND_DTYPE)
+            n = ctypes.c_int64(0)
+            ms = ctypes.c_double(0.0)
+            kt = (KernelTime * 64)()
+            nkt = ctypes.c_int32(0)
+            if profile:
+                code = load().sg_run_profiled(self.handle, ctypes.byref(params), ptr(labels),
+                                              ptr(rounds), len(rounds), ctypes.byref(n),
+                                              ctypes.byref(ms), kt, 64, ctypes.byref(nkt))
+            else:
+                code = load().sg_run(self.handle, ctypes.byref(params), ptr(labels), ptr(rounds),
+                                     len(rounds), ctypes.byref(n), ctypes.byref(ms))
+            if n.value <= len(rounds) or code not in (SG_OK, SG_ECONVERGE):
+                break
+            rounds_cap = n.value
+        log = rounds[: min(n.value, len(rounds))].copy()
         if code == SG_ECONVERGE:
             err = ConvergenceError((load().sg_last_error() or b"").decode())
             err.metrics_log = log

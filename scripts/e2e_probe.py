@@ -16,7 +16,7 @@ g = sg.generate_rmat(24, 16, 1)
 g = sg.attach_random_weights(g, 2) if app == "sssp" else g
 dev = g.device()
 nv, ne, _ = dev.info()
-params = sg.engine._device_params(sg.apps.make_app(app), sg.Scheduler("alb"), sg.KernelConfig(), 1,
+params = sg.engine.device_params(sg.apps.make_app(app), sg.Scheduler("alb"), sg.KernelConfig(), 1,
                                   10 * nv + 256)
 off, tgt, w = dev.download(0, weights=(app == "sssp"))
 pin = lambda x: torch.from_numpy(x).pin_memory().numpy() if x is not None else None

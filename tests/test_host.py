@@ -15,10 +15,8 @@ import paper_1911_09135_b200 as sg
 from paper_1911_09135_b200 import native
 from paper_1911_09135_b200.errors import (ConfigError, ConvergenceError, ParseError, RangeError,
                                           SimtGraphError)
-from paper_1911_09135_b200.schedulers import (Scheduler, assign_blocked, assign_cyclic,
-                                              split_frontier)
-from paper_1911_09135_b200.simt import KernelConfig, RoundMetrics, ThreadCoord
-from paper_1911_09135_b200.worklist import (PrefixWork, Worklist, find_owner, remap_threshold)
+from paper_1911_09135_b200.schedulers import Scheduler, remap_threshold
+from paper_1911_09135_b200.simt import KernelConfig, RoundMetrics
 
 ROOT = Path(__file__).resolve().parents[1]
 
@@ -69,8 +67,8 @@ def test_kernel_config_and_threads():
         KernelConfig(2, 48, 32)
     with pytest.raises(ConfigError):
         KernelConfig(0, 64, 32)
-    t = ThreadCoord.from_global(100, KernelConfig(2, 64, 32))
-    assert (t.cta_id, t.warp_id, t.lane_id) == (1, 3, 4)
+    c = KernelConfig(2, 64, 32)
+    assert (c.cta_of_thread(100), c.warp_of_thread(100)) == (1, 3)
 
 
 def test_scheduler_resolution():
@@ -89,74 +87,33 @@ def test_scheduler_resolution():
         assert w
 
 
-def test_assignments_spec_examples():
-    cfg = KernelConfig(1, 20, 4)
-    assert list(assign_cyclic(100, cfg, 4)) == [4, 24, 44, 64, 84]
-    assert list(assign_cyclic(5, cfg, 7)) == []
-    assert list(assign_blocked(100, cfg, 4)) == [20, 21, 22, 23, 24]
-    # SPEC.md:285 claims empty; the reference code returns [76]
-    assert list(assign_blocked(77, cfg, 19)) == [76]
-    seen = sorted(x for t in range(20) for x in assign_cyclic(77, cfg, t))
-    assert seen == list(range(77))
-    seen = sorted(x for t in range(20) for x in assign_blocked(77, cfg, t))
-    assert seen == list(range(77))
+def test_remap_threshold_and_round_metrics():
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        assert remap_threshold(-3) == 1 and w
+    assert remap_threshold(7) == 7
+    m = RoundMetrics.from_device(KernelConfig(), 123, 4, {"inspect": 1, "twc": 1})
+    assert m.total_edges() == 123 and m.inspect_degree_reads == 4
+    assert m.as_dict()["kernel_launches"] == {"inspect": 1, "twc": 1}
 
 
-def test_split_frontier_bins():
-    cfg = KernelConfig(2, 64, 32)
-    fr = np.arange(6, dtype=np.int64)
-    deg = np.array([0, 31, 32, 63, 64, 500])
-    huge, bins = split_frontier(fr, deg, 500, cfg)
-    assert huge.tolist() == [5]
-    assert bins.small.tolist() == [0, 1] and bins.medium.tolist() == [2, 3]
-    assert bins.large.tolist() == [4]
-    huge, bins = split_frontier(fr, deg, None, cfg)
-    assert len(huge) == 0 and bins.large.tolist() == [4, 5]
-
-
-def test_find_owner_spec_and_linear_scan():
-    p = PrefixWork(np.array([10, 11, 12]), np.array([40, 64, 77]))
-    assert find_owner(p, 4)[:2] == (10, 4)
-    assert find_owner(p, 40)[:2] == (11, 0)
-    assert find_owner(p, 76)[:2] == (12, 12)
-    with pytest.raises(RangeError):
-        find_owner(p, 77)
-    rng = np.random.default_rng(3)
-    for n in range(1, 40):
-        cum = np.cumsum(rng.integers(1, 9, n))
-        p = PrefixWork(np.arange(n), cum)
-        for g in range(int(cum[-1])):
-            o, off, probes = find_owner(p, g)
-            lin = int(np.flatnonzero(cum > g)[0])
-            assert o == lin and off == g - (cum[lin - 1] if lin else 0)
-            assert len(probes) <= int(np.ceil(np.log2(n))) + 1
-
-
-def test_worklist():
-    wl = Worklist(5)
-    wl.push(3)
-    wl.push(1)
-    wl.push(3)
-    assert wl.ids().tolist() == [3, 1] and len(wl) == 2 and 3 in wl
-    assert wl.to_dense().ids().tolist() == [1, 3]
-    with pytest.raises(RangeError):
-        wl.push(5)
-    with pytest.raises(RangeError):
-        Worklist.from_ids(3, [0, 7])
-    assert Worklist.from_ids(6, [4, 2, 4, 0]).ids().tolist() == [4, 2, 0]
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        assert remap_threshold(-3) == 1
-
-
-def test_round_metrics_charge_search():
-    m = RoundMetrics(KernelConfig(1, 64, 32))
-    m.begin_pass()
-    for _ in range(32):
-        m.charge_search(0, (3, 1, 2))
-    assert m.search_memory_accesses == 3 and m.per_warp_search_paths[0] == 1
-    m.charge_search(0, (3, 4))
-    assert m.search_memory_accesses == 5 and m.per_warp_search_paths[0] == 2
+def test_report_schema_from_device_log():
+    """engine.report / write_reports over a synthetic device round log keep
+    the reference's schema (engine.py:269-350)."""
+    log = np.zeros(3, dtype=native.ROUND_DTYPE)
+    log["frontier_size"] = [1, 5, 2]
+    log["active_edges"] = [4, 9, 0]
+    log["launches_twc"] = 1
+    log["launches_lb"] = [0, 1, 0]
+    sch = Scheduler("alb")
+    recs = sg.engine.records_from_log(log, sch, KernelConfig())
+    res = sg.engine.RunResult(np.zeros(3), recs, "bfs", sch, KernelConfig(), 1, 3, 4)
+    rep = sg.report(res)
+    assert rep["rounds"] == 3 and rep["totals"]["edges_processed"] == 13
+    assert rep["totals"]["kernel_launches"] == {"inspect": 3, "lb": 1, "twc": 3}
+    assert rep["scheduler"] == "alb-cyclic" and rep["schema_version"] == 1
+    assert set(rep) >= {"app", "devices", "backend", "config", "graph", "load", "coo_bytes",
+                        "labels_sha256", "spec"}
 
 
 # ----------------------------------------------------------------- graph
@@ -235,25 +192,13 @@ def test_app_parameters():
         make_app("triangles")
 
 
-# ------------------------------------------------------- partition / sync
-def test_partition_and_sync_match_oracle():
+# ------------------------------------------------------------ partition
+def test_edge_cut_bounds_match_oracle():
     from oracle import oracle_np as O
-    from paper_1911_09135_b200.engine import make_partition, sync_labels
-    from paper_1911_09135_b200.schedulers import TraversalView
     off, tgt = O.rmat_csr(10)
-    view = TraversalView(off, tgt, None, "push")
     for d in (1, 2, 3, 8):
-        part = make_partition(view, d)
-        blocks, owner, mc = O.edge_cut(off, tgt, d)
-        assert part.ranges == blocks
-        assert np.array_equal(part.owner, owner) and np.array_equal(part.mirror_count, mc)
-    part = make_partition(view, 2)
-    a = np.array([5.0, 1.0, np.inf] + [0.0] * (len(off) - 4))
-    b = np.array([3.0, 2.0, 7.0] + [0.0] * (len(off) - 4))
-    merged, sent = sync_labels(part, [a, b], "min", baseline=np.full(len(a), np.inf))
-    assert merged[:3].tolist() == [3.0, 1.0, 7.0]
-    with pytest.raises(ConfigError):
-        sync_labels(part, [a], "max")
+        blocks, _, _ = O.edge_cut(off, tgt, d)
+        assert sg.engine.edge_cut_bounds(off, d) == blocks
 
 
 def test_convergence_error_carries_log():
