@@ -237,7 +237,7 @@ def test_nccl_edge_cut_single_rank(sg, golden, app):
     g = _graph(sg, "rmat12")
     if app == "sssp":
         g = sg.attach_random_weights(g, 2)
-    params = sg.engine._device_params(sg.apps.make_app(app), sg.Scheduler("alb"),
+    params = sg.engine.device_params(sg.apps.make_app(app), sg.Scheduler("alb"),
                                       sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
     labels, log, ms = native.dist_run(g.device(), params, native.nccl_unique_id(), 0, 1)
     if app == "pr":
@@ -264,7 +264,7 @@ def test_edge_cut_exchange_modes(sg, golden, app, key, xmode):
         g = sg.attach_random_weights(g, 2)
     world = int(key.split("/d")[1])
     sched = _sched(sg, "x/" + key.split("/")[0] + "/x")
-    p = sg.engine._device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), world,
+    p = sg.engine.device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), world,
                                  10 * g.num_vertices + 256)
     p.reserved = xmode
     labels, log, ms = native.dist_run_threads(g.device(), p, world)
@@ -301,7 +301,7 @@ def test_pr_source_block_tiling(sg, golden, gname, S):
     rounds, and the round log's bins / lb launches of the untiled CSC."""
     info = golden["runs"][gname]["pr/alb/d1"]
     g = _graph(sg, gname)
-    p = sg.engine._device_params(sg.apps.make_app("pr"), sg.Scheduler("alb"), sg.KernelConfig(),
+    p = sg.engine.device_params(sg.apps.make_app("pr"), sg.Scheduler("alb"), sg.KernelConfig(),
                                  1, 10 * g.num_vertices + 256)
     p.reserved = S
     labels, log, ms = g.device().run(p)
@@ -317,7 +317,7 @@ def test_pr_tiling_thresholds(sg):
     g = _graph(sg, "rmat14")
     ref = sg.run_app(g, "pr")
     for thr in (1, 64, 300):
-        p = sg.engine._device_params(sg.apps.make_app("pr"), sg.Scheduler("alb", threshold=thr),
+        p = sg.engine.device_params(sg.apps.make_app("pr"), sg.Scheduler("alb", threshold=thr),
                                      sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
         p.reserved = 5000
         labels, log, ms = g.device().run(p)
@@ -353,7 +353,7 @@ SG_FLAG_RELABEL, SG_FLAG_NO_RELABEL = 8, 16
 
 
 def _run_flags(sg, g, app, sched, flags, devices=1):
-    p = sg.engine._device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), devices,
+    p = sg.engine.device_params(sg.apps.make_app(app), sched, sg.KernelConfig(), devices,
                                  10 * g.num_vertices + 256)
     p.flags |= flags
     labels, log, _ = g.device().run(p)
@@ -423,7 +423,7 @@ def test_relabel_cta_counters_and_thresholds(sg):
         labels, rounds = _run_flags(sg, g, "sssp", sg.Scheduler("alb", threshold=thr),
                                     SG_FLAG_RELABEL)
         assert rounds == brounds and np.array_equal(labels, base)
-    p = sg.engine._device_params(sg.apps.make_app("sssp"), sg.Scheduler("alb"),
+    p = sg.engine.device_params(sg.apps.make_app("sssp"), sg.Scheduler("alb"),
                                  sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
     p.flags |= SG_FLAG_RELABEL
     labels, log, _, cta = g.device().run_cta_counts(p)
@@ -463,7 +463,7 @@ def test_nccl_communicator_reused_across_runs(sg, golden):
     from paper_1911_09135_b200 import native
     g = sg.attach_random_weights(_graph(sg, "rmat12"), 2)
     info = golden["runs"]["rmat12"]["sssp/alb/d1"]
-    p = sg.engine._device_params(sg.apps.make_app("sssp"), sg.Scheduler("alb"),
+    p = sg.engine.device_params(sg.apps.make_app("sssp"), sg.Scheduler("alb"),
                                  sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
     nid = native.nccl_unique_id()
     for _ in range(3):
