@@ -11,6 +11,7 @@
 
 #include <cstdlib>
 #include "sg_runtime.cuh"
+#include "sg_prx.cuh"
 
 
 namespace sg {
@@ -269,20 +270,26 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
 constexpr int64_t kPrTileBytes = 64ll << 20;  // rank-vector slice per source block
 constexpr double kPrTileCoverage = 0.6;       // see prep_pr
 
+// Exact-order pr (sg_prx.cuh): rows shorter than exact_hs() go to the SELL
+// slices, longer ones to 256-edge chunks (split over all warps for ALB's huge
+// rows, walked by one warp otherwise).  SG_EXACT_HS overrides (tuning runs).
+int64_t exact_hs() {
+  static const int64_t hs = [] {
+    const char *e = std::getenv("SG_EXACT_HS");
+    const int64_t x = e ? std::atoll(e) : 512;
+    return std::max<int64_t>(2, std::min<int64_t>(x, 8192));
+  }();
+  return hs;
+}
+
 void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d, int64_t thr,
              int64_t max_rounds, const Layout &lay) {
-  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.csc();
   const int64_t nv = v.nv;
   rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
   PullArgs a = rb.pull_args(v, thr, 0);
   a.vertex = p.sched == SG_SCHED_VERTEX;
-  // relabeled store (in-edge-first order): rows >= zin have no in-edges, so
-  // their rank stays 1 - d from the start (apps.py:162, 180) -- every dense
-  // pass stops at zin; both aux buffers carry their constant aux
-  const uint32_t rows = lay.zin >= 0 && lay.zin <= nv && p.devices == 1 ? (uint32_t)lay.zin
-                                                                         : (uint32_t)nv;
-  a.row_n = rows;
+  a.row_n = (uint32_t)nv;
   // devices > 1: CSC-row edge cut; pulls write only owned rows, so comm_sent
   // is 0 and every changed rank is broadcast to its mirrors (engine.py:88-113)
   const Cuts cuts = make_cuts(v, p.devices);
@@ -292,109 +299,135 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   a.mcount = mc;
   int parts_nonempty = 0;
   for (int d = 0; d < cuts.D; ++d) parts_nonempty += cuts.c[d + 1] > cuts.c[d];
-  double *inv = P.buf<double>(nv), *aux0 = P.buf<double>(nv), *aux1 = P.buf<double>(nv),
-         *hacc = P.buf<double>(nv);
+  double *inv = P.buf<double>(nv), *aux0 = P.buf<double>(nv), *aux1 = P.buf<double>(nv);
   unsigned long long *gmax = P.buf<unsigned long long>(1);
-  uint32_t *gbig = P.buf<uint32_t>(nv), *nbig = P.buf<uint32_t>(1);
   const double d = p.damping, omd = 1.0 - p.damping;
   const int64_t *csr_off = g.csr.off.p;
   Ctl *ctl = rb.ctl.p;
+  RoundStat *stats = rb.stats.p;
   uint32_t *largeq = rb.largeq.p, *hugeq = rb.hugeq.p;
   const int64_t *voff = v.off.p;
-  const uint32_t *vcol = v.col.p;
-  const int64_t vne = v.ne;
-  P.init = [=](Launcher &L, cudaStream_t s) {
-    L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
-    L.go("init", k_pr_init, grid_n(nv), 256, s, csr_off, nv, omd, inv, labels_d, aux0);
-    if (rows < nv) L.go("init", k_copy_f64, grid_n(nv), 256, s, (const double *)aux0, nv, aux1);
-    fill<double>(L, hacc, nv, 0.0, s);
-    fill<unsigned long long>(L, gmax, 1, 0ull, s);
-    if (vne) {
-      fill<uint32_t>(L, nbig, 1, 0u, s);
-      L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, voff, vcol, nv, inv, gmax);
-      L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, voff, vcol, nv, inv, gmax, gbig,
-           nbig);
-      L.go("pr_gain", k_pr_gain_big, sm_info().sms * 4, 256, s, voff, vcol, (const double *)inv,
-           (const uint32_t *)gbig, (const uint32_t *)nbig, gmax);
-    }
-    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, rows, thr, largeq, hugeq,
-         ctl, cuts);
-    if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
-  };
-  PrOp op{aux0, aux1, aux1, aux0, labels_d, inv, d, omd};
-  op.mcount = mc;
-  const bool blocked = p.blocked != 0;
   const int64_t ne = v.ne;
   const double tol = p.tol;
+  const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
+  PrFold fold{aux0, aux1, aux1, aux0, labels_d, inv, d, omd, mc};
 
   // Source-block tiling: once the rank vector (V * 8 B) outgrows the L2, one
   // pull pass per source block gathers from an L2-resident slice (Tiles,
-  // sg_graph.cu); rows carry their partial sums between passes.  Without it a
-  // uniform rmat25 round moves ~95 B of DRAM per 8-byte gather (ncu).
-  // Automatic choice (p.reserved == 0): tile when the rank vector exceeds the
-  // slice AND the graph's sources are not already skewed enough for the L2 to
-  // catch the hot ranks by itself (rmat: the top quarter of vertices by
-  // out-degree source most edges; tiling only adds row passes there).
+  // sg_graph.cu); rows carry their partial sums between passes (the blocks
+  // are consecutive source ranges, i.e. consecutive stretches of every CSC
+  // row, so the carried sum continues the reference's order).  Automatic
+  // choice (p.reserved == 0): tile when the rank vector exceeds the slice AND
+  // the graph's sources are not already skewed enough for the L2 to catch the
+  // hot ranks by itself (rmat: the top quarter of vertices by out-degree
+  // source most edges; tiling only adds row passes there).  A relabeled store
+  // keeps its CSC rows in the reference's source order, which is not the
+  // renamed id order the blocks cut, so it is never tiled.
   int64_t S = p.reserved > 0 ? (int64_t)p.reserved : 0;
   if (!S && nv * 8 > kPrTileBytes) {
     const int64_t B = (nv * 8 + kPrTileBytes - 1) / kPrTileBytes;
     const int64_t S0 = ((nv + B - 1) / B + 1023) / 1024 * 1024;
     if (g.source_coverage(S0) < kPrTileCoverage) S = S0;
   }
-  if (S > 0 && S < nv && p.devices == 1 && !a.vertex) {
-    const Tiles &T = g.tiles(S);
-    const int B = (int)T.blk.size();
-    double *carry = P.buf<double>(nv);
-    long long *meta = P.buf<long long>(4 * (B + 1));  // per block + the full CSC (reference bins)
-    std::vector<PullArgs> ab((size_t)B);
-    for (int b = 0; b < B; ++b) {
-      PullArgs x = a;
-      x.off = T.blk[(size_t)b].off.p;
-      x.col = T.blk[(size_t)b].col.p;
-      x.largeq = P.buf<uint32_t>(nv), x.hugeq = P.buf<uint32_t>(nv);
-      x.hpre = P.buf<int64_t>(nv), x.hstart = P.buf<int64_t>(nv);
-      ab[(size_t)b] = x;
-    }
-    auto base_init = P.init;
-    P.init = [=](Launcher &L, cudaStream_t s) {
-      base_init(L, s);  // ranks, gain, full-CSC bins + prefix (for the round log)
-      L.go("init", k_tile_store, 1, 1, s, ctl, meta + 4 * B);
-      for (int b = 0; b < B; ++b) {
-        const PullArgs &x = ab[(size_t)b];
-        L.go("init", k_static_bins, grid_n(nv), 256, s, x.off, 0u, rows, thr, x.largeq,
-             x.hugeq, ctl, cuts);
-        if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, x);
-        L.go("init", k_tile_store, 1, 1, s, ctl, meta + 4 * b);
+  if (lay.perm || p.devices != 1 || S >= nv) S = 0;
+  const int64_t hs = exact_hs();
+  const int nb = S > 0 ? (int)((nv + S - 1) / S) : 1;
+  double *carry = nb > 1 ? P.buf<double>(nv) : nullptr;
+  uint32_t *heads = P.buf<uint32_t>(nb);
+  long long *meta = P.buf<long long>(4);  // the reference's bins of the full CSC (round log)
+  const int64_t split_min = std::max<int64_t>(thr, hs);
+  std::vector<PrxArgs> xa((size_t)nb);
+  for (int b = 0; b < nb; ++b) {
+    const ExactLayout &L = nb > 1 ? g.tile_exact(S, hs, b) : g.exact(hs);
+    const View &bv = nb > 1 ? g.tiles(S).blk[(size_t)b] : v;
+    PrxArgs x{};
+    x.off = bv.off.p, x.col = bv.col.p;
+    x.srow = L.srow.p, x.sflag = L.sflag.p, x.soff = L.soff.p, x.scol = L.scol.p;
+    x.nslices = (uint32_t)L.nslices;
+    x.big = L.big.p, x.bflag = L.bflag.p;
+    int64_t nsplit = 0, nchunks = 0;
+    if (thr != kNoHuge)
+      for (int64_t dg : L.big_deg) {
+        if (dg < split_min) break;
+        ++nsplit;
+        nchunks += (dg + kXChunk - 1) / kXChunk;
       }
-    };
-    P.round = [=, &rb](RoundCtx &c) {
-      for (int b = 0; b < B; ++b) {
-        PrOp ob = op;
-        ob.carry = carry;
-        ob.tmode = b == 0 ? 1 : b < B - 1 ? 2 : 3;
-        c.L.go("tile_select", k_tile_select, 1, 1, c.s, ctl, (const long long *)meta + 4 * b);
-        pull_round(c, ab[(size_t)b], ob, blocked, hacc, classic);
-        if (b < B - 1) {
-          c.L.go("pr_fold", k_pull_finish<PrOp, false>, 1, 1024, c.s, ab[(size_t)b], ob, hacc,
-                 PrStop{});
-        } else {
-          PrStop stop{gmax, d, tol, ne, std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds,
-                      c.cond, c.use_cond, parts_nonempty};
-          stop.bins = meta + 4 * B;
-          c.L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, c.s, ab[(size_t)b], ob, hacc,
-                 stop);
-        }
-      }
-    };
-    P.finish = [](Launcher &, cudaStream_t) {};
-    return;
+    if (nchunks > 0xffffffffLL) throw Error(SG_ERANGE, "pr: too many huge-row chunks");
+    x.nsplit = (uint32_t)nsplit, x.nself = (uint32_t)(L.nbig - nsplit);
+    x.nchunks = (uint32_t)nchunks;
+    x.ck_first = P.buf<uint32_t>(nsplit + 1);
+    x.ck_row = P.buf<uint32_t>(nchunks);
+    x.ck_T = P.buf<long long>(nchunks);
+    x.ck_meta = P.buf<uint32_t>(nchunks);
+    x.ck_guess = P.buf<int>(nchunks);
+    x.head = heads + b;
+    x.ctl = ctl;
+    x.carry = carry;
+    x.gain_bits = gmax;
+    x.cta_edges = rb.cta.p, x.cta_g = rb.cta_g, x.cta_rounds = rb.cta_rounds;
+    xa[(size_t)b] = x;
   }
-  P.round = [=, &rb](RoundCtx &c) {
-    pull_round(c, a, op, blocked, hacc, classic);
-    PrStop stop{gmax, d, tol, ne, std::min<int64_t>(max_rounds, rb.stats_cap), max_rounds, c.cond,
-                c.use_cond, parts_nonempty};
-    c.L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, c.s, a, op, hacc, stop);
+  const int gx = occupancy_grid(k_prx, kTB);
+  P.init = [=](Launcher &L, cudaStream_t s) {
+    L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
+    L.go("init", k_pr_init, grid_n(nv), 256, s, csr_off, nv, omd, inv, labels_d, aux0);
+    L.go("init", k_copy_f64, grid_n(nv), 256, s, (const double *)aux0, nv, aux1);
+    fill<unsigned long long>(L, gmax, 1, 0ull, s);
+    fill<uint32_t>(L, heads, nb, 0u, s);
+    // the reference's bins of the full CSC, for the round log (schedulers.py:144-167)
+    L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, (uint32_t)nv, thr, largeq, hugeq,
+         ctl, cuts);
+    L.go("init", k_tile_store, 1, 1, s, ctl, meta);
+    for (int b = 0; b < nb; ++b) {
+      const PrxArgs &x = xa[(size_t)b];
+      fill<uint32_t>(L, x.ck_meta, x.nchunks, 0u, s);
+      if (x.nsplit) {
+        L.go("init", k_prx_chunks, 1, 1024, s, x.off, x.big, x.nsplit, (uint32_t *)x.ck_first,
+             (uint32_t *)x.ck_row);
+        L.go("pr_guess", k_prx_guess_sums, grid_n((int64_t)x.nchunks * 32, kTB), kTB, s, x,
+             (const double *)inv);
+        L.go("pr_guess", k_prx_guess_scan, grid_n((int64_t)x.nsplit * 32, kTB), kTB, s, x);
+      }
+    }
+    // eps_stop's gain (apps.py:163-171): one exact pass with aux = inv_outdeg
+    if (ne)
+      for (int b = 0; b < nb; ++b) {
+        PrxArgs x = xa[(size_t)b];
+        x.gain = 1;
+        L.go("pr_gain", k_prx, gx, kTB, s, x, fold);
+      }
+    fill<uint32_t>(L, heads, nb, 0u, s);
+    for (int b = 0; b < nb; ++b) {  // round 0's binades (aux0 = (1-d) * inv_outdeg)
+      const PrxArgs &x = xa[(size_t)b];
+      if (x.nsplit) {
+        L.go("pr_guess", k_prx_guess_sums, grid_n((int64_t)x.nchunks * 32, kTB), kTB, s, x,
+             (const double *)aux0);
+        L.go("pr_guess", k_prx_guess_scan, grid_n((int64_t)x.nsplit * 32, kTB), kTB, s, x);
+      }
+    }
   };
+  PrStop stop{gmax, d, tol, ne, limit, max_rounds, cudaGraphConditionalHandle{}, 0, parts_nonempty};
+  stop.bins = meta;
+  if (a.vertex) {  // vertex scheduler (_kernels_py.py:88-97): one thread folds one row, in order
+    PrOp op{aux0, aux1, aux1, aux0, labels_d, inv, d, omd};
+    op.mcount = mc;
+    double *hacc = P.buf<double>(1);
+    P.round = [=](RoundCtx &c) {
+      pull_round(c, a, op, false, hacc, false);
+      PrStop st = stop;
+      st.cond = c.cond, st.use_cond = c.use_cond;
+      c.L.go("pr_finish", k_prx_finish, 1, 32, c.s, ctl, stats, (uint32_t)nv, st, cuts.D, heads,
+             nb);
+    };
+  } else {
+    P.round = [=](RoundCtx &c) {
+      for (int b = 0; b < nb; ++b) c.L.go("pr_pull", k_prx, gx, kTB, c.s, xa[(size_t)b], fold);
+      PrStop st = stop;
+      st.cond = c.cond, st.use_cond = c.use_cond;
+      c.L.go("pr_finish", k_prx_finish, 1, 32, c.s, ctl, stats, (uint32_t)nv, st, cuts.D, heads,
+             nb);
+    };
+  }
   P.finish = [](Launcher &, cudaStream_t) {};
 }
 

@@ -558,6 +558,36 @@ Relabel &Graph::hot(int64_t K, bool in_first) {
     SG_CUDA(cudaMemset(h->csr.off.p, 0, sizeof(int64_t)));
     if (weighted) h->weighted = true, h->w64.alloc(1);
   }
+  // pull layout (pr): the relabeled CSC is the original CSC with its rows
+  // permuted and its sources renamed -- NOT the transpose of the relabeled
+  // CSR, which would order every row by new source id.  The reference sums a
+  // row in CSC order (ascending original source id, np.add.at), and with
+  // floating point the order is the result (sg_prx.cuh).
+  if (in_first && nv) {
+    const View &c = csc();
+    auto pv = std::make_unique<View>();
+    pv->nv = nv, pv->ne = ne;
+    pv->off.alloc(nv + 1);
+    pv->col.alloc(ne ? ne : 1);
+    DBuf<int64_t> len(nv + 1);
+    SG_LAUNCH(k_perm_len, grid_for(nv), 256, 0, 0, c.off.p, R->perm.p, nv, len.p);
+    SG_CUDA(cudaMemset(len.p + nv, 0, sizeof(int64_t)));
+    size_t t4 = 0;
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t4, len.p, pv->off.p, nv + 1));
+    DBuf<char> t(t4);
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, t4, len.p, pv->off.p, nv + 1));
+    const int64_t nbig = std::min<int64_t>(K, 4096);
+    if (nbig)
+      SG_LAUNCH(k_perm_rows, dim3((unsigned)nbig, 16), 256, 0, 0, c.off.p, c.col.p,
+                (const int64_t *)nullptr, (const uint32_t *)nullptr, R->perm.p, R->inv.p,
+                pv->off.p, nv, nbig, K, false, pv->col.p, (int64_t *)nullptr,
+                (uint32_t *)nullptr);
+    SG_LAUNCH(k_perm_rows, grid_for(nv * 32), 256, 0, 0, c.off.p, c.col.p,
+              (const int64_t *)nullptr, (const uint32_t *)nullptr, R->perm.p, R->inv.p, pv->off.p,
+              nv, nbig, K, false, pv->col.p, (int64_t *)nullptr, (uint32_t *)nullptr);
+    SG_CUDA(cudaDeviceSynchronize());
+    h->csc_ = std::move(pv);
+  }
   R->g = std::move(h);
   Relabel &out = *R;
   hot_[key] = std::move(R);

@@ -20,10 +20,46 @@ struct View {
 // sub-range of the CSC row, since CSC rows are sorted by source.  A pull pass
 // over one block gathers from an S*8-byte slice of the rank vector that stays
 // resident in L2 (the whole vector does not once V*8 B exceeds the L2).
+struct ExactLayout;
 struct Tiles {
   int64_t S = 0;
   std::vector<View> blk;
+  // exact-order pr layouts of the blocks (built lazily, per Hs)
+  int64_t ex_hs = 0;
+  std::vector<std::unique_ptr<ExactLayout>> ex;
 };
+
+// Exact-order layout of a pull view for pr (sg_prx.cu).  The reference sums a
+// row's in-edges one by one in CSC order starting from 0.0 (np.add.at applies
+// them in array order, _kernels_py.py:73-75; the CSC keeps source order,
+// graph.py:95-113), and with floating point that order IS the result.  So:
+//  * rows with 1 <= deg < hs are stored sliced-ELL (SELL-32): slices of 32
+//    rows (degree-sorted inside windows of 4096 consecutive rows), entry j of
+//    the slice's lane l at scol[soff[s] + 32 j + l] -- one lane sums one row
+//    left to right with fully coalesced adjacency loads;
+//  * rows with deg >= hs (`big`, degree-descending) are summed in 256-edge
+//    chunks whose exact sequential sum is formed in integer units of the
+//    running sum's ulp (sg_prx.cuh).
+// In a source block of a tiled CSC, a row's segment continues the row's sum:
+// kFirst marks the first block holding edges of the row (start from 0.0),
+// kLast the last one (fold the row); other blocks carry the partial sum.
+struct ExactLayout {
+  static constexpr uint8_t kFirst = 1, kLast = 2;
+  static constexpr uint32_t kEmpty = 0xffffffffu;  // empty lane / padding entry
+  int64_t hs = 0;
+  int64_t nshort = 0, nslices = 0, sell_entries = 0, sell_edges = 0;
+  DBuf<uint32_t> srow;   // [nslices * 32] row id (kEmpty: no row)
+  DBuf<uint8_t> sflag;   // [nslices * 32] kFirst | kLast
+  DBuf<int64_t> soff;    // [nslices + 1] slice start in scol
+  DBuf<uint32_t> scol;   // [sell_entries]
+  int64_t nbig = 0, big_edges = 0;
+  DBuf<uint32_t> big;    // [nbig] rows with deg >= hs, degree descending (ties by id)
+  DBuf<uint8_t> bflag;   // [nbig]
+  std::vector<int64_t> big_deg;  // host copy of their degrees (descending)
+  double build_ms = 0;
+};
+void build_exact_layout(ExactLayout &L, const View &v, int64_t hs, const View &full, int64_t lo,
+                        int64_t hi);
 
 struct Relabel;
 
@@ -40,6 +76,10 @@ struct Graph {
   const View &sym();
   std::unique_ptr<Tiles> tiles_;  // pr source blocks of the CSC, built lazily per S
   const Tiles &tiles(int64_t S);
+  // exact-order pr layout of the CSC (and of the tiles' blocks), lazily per hs
+  std::unique_ptr<ExactLayout> exact_;
+  const ExactLayout &exact(int64_t hs);
+  const ExactLayout &tile_exact(int64_t S, int64_t hs, int64_t b);
   // fraction of the edges whose source is among the K highest out-degree
   // vertices (cached per K): how much of a pull's gather traffic a cache of K
   // rank values absorbs on its own
