@@ -276,7 +276,7 @@ constexpr double kPrTileCoverage = 0.6;       // see prep_pr
 int64_t exact_hs() {
   static const int64_t hs = [] {
     const char *e = std::getenv("SG_EXACT_HS");
-    const int64_t x = e ? std::atoll(e) : 512;
+    const int64_t x = e ? std::atoll(e) : 2048;
     return std::max<int64_t>(2, std::min<int64_t>(x, 8192));
   }();
   return hs;
@@ -335,7 +335,9 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   double *carry = nb > 1 ? P.buf<double>(nv) : nullptr;
   uint32_t *heads = P.buf<uint32_t>(nb);
   long long *meta = P.buf<long long>(4);  // the reference's bins of the full CSC (round log)
-  const int64_t split_min = std::max<int64_t>(thr, hs);
+  // SG_PR_SPLIT_ALL (experiments): every long row through the split path
+  static const bool split_all = std::getenv("SG_PR_SPLIT_ALL") && std::atoi(std::getenv("SG_PR_SPLIT_ALL"));
+  const int64_t split_min = split_all && thr != kNoHuge ? hs : std::max<int64_t>(thr, hs);
   std::vector<PrxArgs> xa((size_t)nb);
   for (int b = 0; b < nb; ++b) {
     const ExactLayout &L = nb > 1 ? g.tile_exact(S, hs, b) : g.exact(hs);
@@ -344,6 +346,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
     x.off = bv.off.p, x.col = bv.col.p;
     x.srow = L.srow.p, x.sflag = L.sflag.p, x.soff = L.soff.p, x.scol = L.scol.p;
     x.nslices = (uint32_t)L.nslices;
+    x.gfirst = L.gfirst.p, x.ngroups = (uint32_t)L.ngroups;
     x.big = L.big.p, x.bflag = L.bflag.p;
     int64_t nsplit = 0, nchunks = 0;
     if (thr != kNoHuge)

@@ -52,6 +52,9 @@ struct ExactLayout {
   DBuf<uint8_t> sflag;   // [nslices * 32] kFirst | kLast
   DBuf<int64_t> soff;    // [nslices + 1] slice start in scol
   DBuf<uint32_t> scol;   // [sell_entries]
+  int64_t ngroups = 0;   // dynamic-fetch units: runs of consecutive slices of >= kGroupEntries
+  DBuf<uint32_t> gfirst; // [ngroups + 1] first slice of each group
+  static constexpr int64_t kGroupEntries = 256;
   int64_t nbig = 0, big_edges = 0;
   DBuf<uint32_t> big;    // [nbig] rows with deg >= hs, degree descending (ties by id)
   DBuf<uint8_t> bflag;   // [nbig]

@@ -156,6 +156,23 @@ void build_exact_layout(ExactLayout &L, const View &v, int64_t hs, const View &f
   if (L.nslices)
     SG_LAUNCH(k_ex_fill, grid_of(L.nslices * 32), 256, 0, 0, v.off.p, v.col.p, L.srow.p, L.soff.p,
               L.nslices, L.scol.p);
+  // fetch groups: consecutive slices until >= kGroupEntries entries (one
+  // atomic per group instead of one per slice of a few short rows)
+  {
+    std::vector<int64_t> so((size_t)L.nslices + 1);
+    SG_CUDA(cudaMemcpy(so.data(), L.soff.p, sizeof(int64_t) * so.size(), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> gf;
+    for (int64_t s0 = 0; s0 < L.nslices;) {
+      gf.push_back((uint32_t)s0);
+      int64_t s1 = s0 + 1;
+      while (s1 < L.nslices && so[(size_t)s1] - so[(size_t)s0] < ExactLayout::kGroupEntries) ++s1;
+      s0 = s1;
+    }
+    gf.push_back((uint32_t)L.nslices);
+    L.ngroups = (int64_t)gf.size() - 1;
+    L.gfirst.alloc(gf.size());
+    SG_CUDA(cudaMemcpy(L.gfirst.p, gf.data(), sizeof(uint32_t) * gf.size(), cudaMemcpyHostToDevice));
+  }
   // big rows
   L.big.alloc(std::max<int64_t>(L.nbig, 1));
   L.bflag.alloc(std::max<int64_t>(L.nbig, 1));

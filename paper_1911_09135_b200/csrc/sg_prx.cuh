@@ -35,7 +35,6 @@ namespace sg {
 
 constexpr int kXV = 8;              // values per lane per 256-edge chunk
 constexpr int kXChunk = 32 * kXV;   // edges per chunk
-constexpr uint32_t kSellGrab = 2;   // SELL slices per dynamic fetch
 constexpr int kNoGuess = INT_MIN;
 
 struct PrxArgs {
@@ -47,6 +46,8 @@ struct PrxArgs {
   const int64_t *soff;
   const uint32_t *scol;
   uint32_t nslices;
+  const uint32_t *gfirst;     // [ngroups + 1] slice groups (dynamic-fetch units)
+  uint32_t ngroups;
   const uint32_t *big;
   const uint8_t *bflag;
   uint32_t nsplit, nself;     // big[0, nsplit): ALB huge rows, [nsplit, nsplit + nself): walked
@@ -174,20 +175,23 @@ __device__ __forceinline__ void row_end(const PrxArgs &a, PrFold &op, uint32_t v
   else a.carry[v] = acc;
 }
 
-// one warp walks row v's chunks [k0, nk) in order from s
+// one warp walks row v's chunks [k0, nk) in order from s; software-pipelined:
+// chunk k is added while the values of k + 1 and the columns of k + 2 load
 __device__ __forceinline__ double walk_chunks(const PrxArgs &a, const PrFold &op, int64_t s0,
                                               int64_t d, int64_t k0, int64_t nk, double s,
                                               unsigned long long &proc) {
   if (k0 >= nk) return s;
-  uint32_t src[kXV], srcn[kXV] = {};
-  double x[kXV];
-  gather_src(a.col + s0 + k0 * kXChunk, d - k0 * kXChunk, src);
+  uint32_t sb[kXV], sc[kXV] = {};
+  double xa[kXV], xb[kXV];
+  gather_src(a.col + s0 + k0 * kXChunk, d - k0 * kXChunk, sb);
+  gather_val(op.aux, sb, xa);
+  if (k0 + 1 < nk) gather_src(a.col + s0 + (k0 + 1) * kXChunk, d - (k0 + 1) * kXChunk, sb);
   for (int64_t k = k0; k < nk; ++k) {
-    gather_val(op.aux, src, x);
-    if (k + 1 < nk) gather_src(a.col + s0 + (k + 1) * kXChunk, d - (k + 1) * kXChunk, srcn);
-    s = ex_step(s, x);
+    if (k + 1 < nk) gather_val(op.aux, sb, xb);
+    if (k + 2 < nk) gather_src(a.col + s0 + (k + 2) * kXChunk, d - (k + 2) * kXChunk, sc);
+    s = ex_step(s, xa);
 #pragma unroll
-    for (int u = 0; u < kXV; ++u) src[u] = srcn[u];
+    for (int u = 0; u < kXV; ++u) xa[u] = xb[u], sb[u] = sc[u];
   }
   if (lane_id() == 0) proc += (unsigned long long)(d - k0 * kXChunk);
   return s;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(kTB) k_prx(PrxArgs a, PrFold op) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   unsigned long long proc = 0;
   const uint32_t n1 = a.nchunks, n2 = n1 + a.nsplit, n3 = n2 + a.nself;
-  const uint32_t ntick = n3 + (a.nslices + kSellGrab - 1) / kSellGrab;
+  const uint32_t ntick = n3 + a.ngroups;
   for (;;) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(a.head, 1u);
@@ -330,8 +334,7 @@ __global__ void __launch_bounds__(kTB) k_prx(PrxArgs a, PrFold op) {
                                    row_start(a, v, f), proc);
       if (lane == 0) row_end(a, op, v, f, s);
     } else {
-      const uint32_t g0 = (t - n3) * kSellGrab;
-      const uint32_t g1 = min(g0 + kSellGrab, a.nslices);
+      const uint32_t g0 = a.gfirst[t - n3], g1 = a.gfirst[t - n3 + 1];
       for (uint32_t s = g0; s < g1; ++s) sell_slice(a, op, s, proc);
     }
   }
