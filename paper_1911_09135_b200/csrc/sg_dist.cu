@@ -30,6 +30,7 @@
 #include <thread>
 
 #include "sg_comm.cuh"
+#include "sg_prx.cuh"
 
 namespace sg {
 namespace {
@@ -526,10 +527,14 @@ __global__ void k_dist_kc_advance(PullArgs a, long long *acc, Loop lp) {
   loop_test(ctl, round, stop, lp);
 }
 
+// pr over NCCL: this rank folds its edge-cut rows [lo, hi) with the exact-order
+// pull (sg_prx.cuh, on a layout of its own rows), then every rank's new aux
+// slice is broadcast, max |delta|, comm_broadcast and the bin counters are
+// all-reduced, and the stop test runs on the reduced values.  eps_stop's gain
+// is the maximum over ranks of the exact row sums of their own rows.
 void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, Comm &cm,
                  double *labels_out, sg_round *rounds_out, int64_t cap, int64_t *nrounds,
                  double *ms_out) {
-  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.csc();
   const int64_t nv = v.nv;
   const Cuts cuts = make_cuts(v, cm.world);
@@ -544,48 +549,65 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
     mirror_counts(v, cuts, mc.p);
     a.mcount = mc.p;
   }
-  DBuf<double> inv(nv), aux0(nv), aux1(nv), hacc(nv), rank(nv);
+  DBuf<double> inv(nv), aux0(nv), aux1(nv), hacc(1), rank(nv);
   DBuf<unsigned long long> gmax(1);
   DBuf<long long> acc(kDistN);
+  DBuf<uint32_t> head(1);
   const double d = p.damping, omd = 1.0 - p.damping;
   PrOp op{aux0.p, aux1.p, aux1.p, aux0.p, rank.p, inv.p, d, omd};
   op.mcount = a.mcount;
+  PrFold fold{aux0.p, aux1.p, aux1.p, aux0.p, rank.p, inv.p, d, omd, a.mcount};
   Cuts one{};
   one.D = 1, one.c[0] = 0, one.c[1] = nv;
+  Ctl *ctl = rb.ctl.p;
+  const int64_t hs = exact_hs();
+  const ExactLayout &XL = g.exact(hs, lo, hi);
+  std::vector<std::unique_ptr<DBuf<char>>> keep;
+  PrxArgs xa = prx_args(v, XL, std::max<int64_t>(thr, hs), thr != kNoHuge, ctl, nullptr, gmax.p,
+                        head.p, [&](size_t bytes) {
+                          keep.emplace_back(new DBuf<char>(bytes));
+                          return (void *)keep.back()->p;
+                        });
+  const int gx = occupancy_grid(k_prx, kTB);
   DistLoop dl;
   cudaStream_t s = dl.s;
   Launcher L;
-  Ctl *ctl = rb.ctl.p;
   const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
-  PrStop st1{gmax.p, d, p.tol, v.ne, limit, max_rounds, cudaGraphConditionalHandle{}, 0, 1, 1,
-             nullptr};
-  PrStop st2 = st1;
-  st2.mode = 2, st2.dist = acc.p;
+  PrStop st2{gmax.p, d, p.tol, v.ne, limit, max_rounds, cudaGraphConditionalHandle{}, 0, 1, 2,
+             acc.p};
   SG_CUDA(cudaEventRecord(dl.e0, s));
   L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
   L.go("init", k_pr_init, grid_n(nv), 256, s, g.csr.off.p, nv, omd, inv.p, rank.p, aux0.p);
-  fill<double>(L, hacc.p, nv, 0.0, s);
+  L.go("init", k_copy_f64, grid_n(nv), 256, s, (const double *)aux0.p, nv, aux1.p);
   fill<unsigned long long>(L, gmax.p, 1, 0ull, s);
   fill<long long>(L, acc.p, kDistN, 0ll, s);
-  if (v.ne) {  // the gain over ALL rows: every rank holds the whole view
-    DBuf<uint32_t> big(nv), nbig(1);
-    fill<uint32_t>(L, nbig.p, 1, 0u, s);
-    L.go("pr_gain", k_pr_gain_rows, grid_n(nv), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p);
-    L.go("pr_gain", k_pr_gain_max, grid_n(nv * 32), 256, s, v.off.p, v.col.p, nv, inv.p, gmax.p,
-         big.p, nbig.p);
-    L.go("pr_gain", k_pr_gain_big, sm_info().sms * 4, 256, s, v.off.p, v.col.p,
-         (const double *)inv.p, (const uint32_t *)big.p, (const uint32_t *)nbig.p, gmax.p);
-    SG_CUDA(cudaStreamSynchronize(s));
+  fill<uint32_t>(L, head.p, 1, 0u, s);
+  fill<uint32_t>(L, xa.ck_meta, xa.nchunks, 0u, s);
+  if (xa.nsplit) {
+    L.go("init", k_prx_chunks, 1, 1024, s, xa.off, xa.big, xa.nsplit, (uint32_t *)xa.ck_first,
+         (uint32_t *)xa.ck_row);
+    L.go("pr_guess", k_prx_guess_sums, grid_n((int64_t)xa.nchunks * 32, kTB), kTB, s, xa,
+         (const double *)inv.p);
+    L.go("pr_guess", k_prx_guess_scan, grid_n((int64_t)xa.nsplit * 32, kTB), kTB, s, xa);
+  }
+  if (v.ne) {  // gain: exact sums of this rank's rows, then the max over ranks
+    PrxArgs xg = xa;
+    xg.gain = 1;
+    L.go("pr_gain", k_prx, gx, kTB, s, xg, fold);
+    cm.allreduce(gmax.p, 1, CType::U64, COp::Max, s);
+  }
+  fill<uint32_t>(L, head.p, 1, 0u, s);
+  if (xa.nsplit) {
+    L.go("pr_guess", k_prx_guess_sums, grid_n((int64_t)xa.nchunks * 32, kTB), kTB, s, xa,
+         (const double *)aux0.p);
+    L.go("pr_guess", k_prx_guess_scan, grid_n((int64_t)xa.nsplit * 32, kTB), kTB, s, xa);
   }
   L.go("init", k_static_bins, grid_n(hi - lo), 256, s, v.off.p, lo, hi - lo, thr, rb.largeq.p,
        rb.hugeq.p, ctl, one);
-  if (thr != kNoHuge) L.go("huge_prefix", k_pull_prefix, 1, 1024, s, a);
   for (int64_t r = 0; r <= limit; ++r) {
-    RoundCtx c{L, s, cudaGraphConditionalHandle{}, 0};
-    pull_round(c, a, op, p.blocked != 0, hacc.p, classic);
-    L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, s, a, op, hacc.p, st1);
+    L.go("pr_pull", k_prx, gx, kTB, s, xa, fold);
     L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
-    double *auxn = (r & 1) ? aux0.p : aux1.p;  // PrOp: round r writes next1 / next0
+    double *auxn = (r & 1) ? aux0.p : aux1.p;  // round r writes next1 / next0
     cm.group_begin();
     for (int q = 0; q < cm.world; ++q)
       cm.bcast(auxn + cuts.c[q], (size_t)(cuts.c[q + 1] - cuts.c[q]), CType::F64, q, s);
@@ -594,6 +616,7 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
     cm.allreduce(&ctl->comm_bcast, 1, CType::U64, COp::Sum, s);
     cm.allreduce(acc.p, 6, CType::I64, COp::Sum, s);
     L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, s, a, op, hacc.p, st2);
+    fill<uint32_t>(L, head.p, 1, 0u, s);
     if (dl.done(ctl)) break;
   }
   cm.group_begin();  // every rank's rows -> the full label vector

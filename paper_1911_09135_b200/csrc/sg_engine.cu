@@ -148,10 +148,6 @@ struct Layout {
   int64_t zin = -1;                // first id without in-edges (pull layouts), -1: none known
 };
 
-__global__ void k_copy_f64(const double *__restrict__ a, int64_t n, double *__restrict__ b) {
-  const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) b[i] = a[i];
-}
 
 __global__ void k_copy_u32(const uint32_t *__restrict__ a, int64_t n, uint32_t *__restrict__ b) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
@@ -270,18 +266,6 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
 constexpr int64_t kPrTileBytes = 64ll << 20;  // rank-vector slice per source block
 constexpr double kPrTileCoverage = 0.6;       // see prep_pr
 
-// Exact-order pr (sg_prx.cuh): rows shorter than exact_hs() go to the SELL
-// slices, longer ones to 256-edge chunks (split over all warps for ALB's huge
-// rows, walked by one warp otherwise).  SG_EXACT_HS overrides (tuning runs).
-int64_t exact_hs() {
-  static const int64_t hs = [] {
-    const char *e = std::getenv("SG_EXACT_HS");
-    const int64_t x = e ? std::atoll(e) : 2048;
-    return std::max<int64_t>(2, std::min<int64_t>(x, 8192));
-  }();
-  return hs;
-}
-
 void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labels_d, int64_t thr,
              int64_t max_rounds, const Layout &lay) {
   const View &v = g.csc();
@@ -342,31 +326,8 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   for (int b = 0; b < nb; ++b) {
     const ExactLayout &L = nb > 1 ? g.tile_exact(S, hs, b) : g.exact(hs);
     const View &bv = nb > 1 ? g.tiles(S).blk[(size_t)b] : v;
-    PrxArgs x{};
-    x.off = bv.off.p, x.col = bv.col.p;
-    x.srow = L.srow.p, x.sflag = L.sflag.p, x.soff = L.soff.p, x.scol = L.scol.p;
-    x.nslices = (uint32_t)L.nslices;
-    x.gfirst = L.gfirst.p, x.ngroups = (uint32_t)L.ngroups;
-    x.big = L.big.p, x.bflag = L.bflag.p;
-    int64_t nsplit = 0, nchunks = 0;
-    if (thr != kNoHuge)
-      for (int64_t dg : L.big_deg) {
-        if (dg < split_min) break;
-        ++nsplit;
-        nchunks += (dg + kXChunk - 1) / kXChunk;
-      }
-    if (nchunks > 0xffffffffLL) throw Error(SG_ERANGE, "pr: too many huge-row chunks");
-    x.nsplit = (uint32_t)nsplit, x.nself = (uint32_t)(L.nbig - nsplit);
-    x.nchunks = (uint32_t)nchunks;
-    x.ck_first = P.buf<uint32_t>(nsplit + 1);
-    x.ck_row = P.buf<uint32_t>(nchunks);
-    x.ck_T = P.buf<long long>(nchunks);
-    x.ck_meta = P.buf<uint32_t>(nchunks);
-    x.ck_guess = P.buf<int>(nchunks);
-    x.head = heads + b;
-    x.ctl = ctl;
-    x.carry = carry;
-    x.gain_bits = gmax;
+    PrxArgs x = prx_args(bv, L, split_min, thr != kNoHuge, ctl, carry, gmax, heads + b,
+                         [&](size_t bytes) { return (void *)P.buf<char>((int64_t)bytes); });
     x.cta_edges = rb.cta.p, x.cta_g = rb.cta_g, x.cta_rounds = rb.cta_rounds;
     xa[(size_t)b] = x;
   }

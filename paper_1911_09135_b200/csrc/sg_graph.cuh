@@ -2,6 +2,8 @@
 #pragma once
 #include <map>
 #include <memory>
+#include <mutex>
+#include <tuple>
 
 #include "sg_common.cuh"
 
@@ -47,6 +49,7 @@ struct ExactLayout {
   static constexpr uint8_t kFirst = 1, kLast = 2;
   static constexpr uint32_t kEmpty = 0xffffffffu;  // empty lane / padding entry
   int64_t hs = 0;
+  int64_t rlo = 0, rhi = -1;  // the rows it covers
   int64_t nshort = 0, nslices = 0, sell_entries = 0, sell_edges = 0;
   DBuf<uint32_t> srow;   // [nslices * 32] row id (kEmpty: no row)
   DBuf<uint8_t> sflag;   // [nslices * 32] kFirst | kLast
@@ -61,8 +64,9 @@ struct ExactLayout {
   std::vector<int64_t> big_deg;  // host copy of their degrees (descending)
   double build_ms = 0;
 };
+// rows [rlo, rhi) of the view only (rhi < 0: all rows) -- one rank's edge-cut rows
 void build_exact_layout(ExactLayout &L, const View &v, int64_t hs, const View &full, int64_t lo,
-                        int64_t hi);
+                        int64_t hi, int64_t rlo = 0, int64_t rhi = -1);
 
 struct Relabel;
 
@@ -80,8 +84,10 @@ struct Graph {
   std::unique_ptr<Tiles> tiles_;  // pr source blocks of the CSC, built lazily per S
   const Tiles &tiles(int64_t S);
   // exact-order pr layout of the CSC (and of the tiles' blocks), lazily per hs
-  std::unique_ptr<ExactLayout> exact_;
-  const ExactLayout &exact(int64_t hs);
+  // (keyed by hs and the row range: ranks-as-threads runs build theirs concurrently)
+  std::map<std::tuple<int64_t, int64_t, int64_t>, std::unique_ptr<ExactLayout>> exact_;
+  std::mutex exact_mu_;
+  const ExactLayout &exact(int64_t hs, int64_t rlo = 0, int64_t rhi = -1);
   const ExactLayout &tile_exact(int64_t S, int64_t hs, int64_t b);
   // fraction of the edges whose source is among the K highest out-degree
   // vertices (cached per K): how much of a pull's gather traffic a cache of K

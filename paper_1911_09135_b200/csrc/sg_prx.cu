@@ -37,13 +37,13 @@ __device__ __forceinline__ void append64(bool p, unsigned long long k, unsigned 
   if (p) list[base + __popc(m & lanemask_lt())] = k;
 }
 
-__global__ void k_ex_classify(const int64_t *__restrict__ off, int64_t nv, int64_t hs,
+__global__ void k_ex_classify(const int64_t *__restrict__ off, int64_t rlo, int64_t rhi, int64_t hs,
                               unsigned long long *__restrict__ skeys, uint32_t *__restrict__ ns,
                               unsigned long long *__restrict__ bkeys, uint32_t *__restrict__ nb) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < nv; b += st) {
+  for (int64_t b = rlo + (int64_t)blockIdx.x * blockDim.x; b < rhi; b += st) {
     const int64_t v = b + threadIdx.x;
-    const int64_t d = v < nv ? off[v + 1] - off[v] : 0;
+    const int64_t d = v < rhi ? off[v + 1] - off[v] : 0;
     const bool sh = d >= 1 && d < hs, bg = d >= hs;
     const unsigned long long sk = ((unsigned long long)(v >> kWinBits) << (kDegBits + kWinBits)) |
                                   ((unsigned long long)(hs - 1 - d) << kWinBits) |
@@ -116,7 +116,7 @@ __global__ void k_ex_big(const unsigned long long *__restrict__ keys, int64_t n,
 }  // namespace
 
 void build_exact_layout(ExactLayout &L, const View &v, int64_t hs, const View &full, int64_t lo,
-                        int64_t hi) {
+                        int64_t hi, int64_t rlo, int64_t rhi) {
   if (hs < 2 || hs > (1 << kDegBits)) throw Error(SG_ECONFIG, "exact layout: hs out of range");
   const auto t0 = std::chrono::steady_clock::now();
   L.hs = hs;
@@ -124,7 +124,10 @@ void build_exact_layout(ExactLayout &L, const View &v, int64_t hs, const View &f
   DBuf<unsigned long long> sk(std::max<int64_t>(nv, 1)), bk(std::max<int64_t>(nv, 1));
   DBuf<uint32_t> cnt(2);
   SG_CUDA(cudaMemset(cnt.p, 0, 2 * sizeof(uint32_t)));
-  if (nv) SG_LAUNCH(k_ex_classify, grid_of(nv), 256, 0, 0, v.off.p, nv, hs, sk.p, cnt.p, bk.p, cnt.p + 1);
+  if (rhi < 0) rhi = nv;
+  if (rhi > rlo)
+    SG_LAUNCH(k_ex_classify, grid_of(rhi - rlo), 256, 0, 0, v.off.p, rlo, rhi, hs, sk.p, cnt.p,
+              bk.p, cnt.p + 1);
   uint32_t h[2];
   SG_CUDA(cudaMemcpy(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost));
   L.nshort = h[0], L.nbig = h[1];
@@ -196,14 +199,18 @@ void build_exact_layout(ExactLayout &L, const View &v, int64_t hs, const View &f
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
-const ExactLayout &Graph::exact(int64_t hs) {
-  if (!exact_ || exact_->hs != hs) {
+const ExactLayout &Graph::exact(int64_t hs, int64_t rlo, int64_t rhi) {
+  if (rhi < 0) rhi = nv;
+  std::lock_guard<std::mutex> lk(exact_mu_);
+  auto &slot = exact_[std::make_tuple(hs, rlo, rhi)];
+  if (!slot) {
     const View &c = csc();
     auto L = std::make_unique<ExactLayout>();
-    build_exact_layout(*L, c, hs, c, 0, nv);
-    exact_ = std::move(L);
+    build_exact_layout(*L, c, hs, c, 0, nv, rlo, rhi);
+    L->rlo = rlo, L->rhi = rhi;
+    slot = std::move(L);
   }
-  return *exact_;
+  return *slot;
 }
 
 const ExactLayout &Graph::tile_exact(int64_t S, int64_t hs, int64_t b) {

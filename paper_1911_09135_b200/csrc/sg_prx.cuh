@@ -28,14 +28,32 @@
 //    long row of a TWC-only run) are walked chunk by chunk by one warp.
 #pragma once
 #include <climits>
+#include <cstdlib>
 
 #include "sg_pull.cuh"
 
 namespace sg {
+namespace {  // per translation unit, like sg_runtime.cuh
 
 constexpr int kXV = 8;              // values per lane per 256-edge chunk
 constexpr int kXChunk = 32 * kXV;   // edges per chunk
 constexpr int kNoGuess = INT_MIN;
+
+// rows shorter than exact_hs() go to the SELL slices, longer ones to 256-edge
+// chunks (swept 128..8192 on rmat24: profiles/r2d, r2f); SG_EXACT_HS overrides
+inline int64_t exact_hs() {
+  static const int64_t hs = [] {
+    const char *e = std::getenv("SG_EXACT_HS");
+    const int64_t x = e ? std::atoll(e) : 2048;
+    return std::max<int64_t>(2, std::min<int64_t>(x, 8192));
+  }();
+  return hs;
+}
+
+__global__ void k_copy_f64(const double *__restrict__ a, int64_t n, double *__restrict__ b) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) b[i] = a[i];
+}
 
 struct PrxArgs {
   const int64_t *off;
@@ -461,4 +479,40 @@ __global__ void k_prx_finish(Ctl *ctl, RoundStat *stats, uint32_t nv, PrStop sto
   if (stop.use_cond) cudaGraphSetConditional(stop.cond, ctl->done ? 0u : 1u);
 }
 
+// host: the arguments of one k_prx pass over view `bv` with layout `L`.  Big
+// rows of degree >= split_min are ALB huge rows (split; none when !huge_on);
+// `alloc(bytes)` provides the pass's device buffers (owned by the caller).
+template <class Alloc>
+PrxArgs prx_args(const View &bv, const ExactLayout &L, int64_t split_min, bool huge_on, Ctl *ctl,
+                 double *carry, unsigned long long *gmax, uint32_t *head, Alloc &&alloc) {
+  PrxArgs x{};
+  x.off = bv.off.p, x.col = bv.col.p;
+  x.srow = L.srow.p, x.sflag = L.sflag.p, x.soff = L.soff.p, x.scol = L.scol.p;
+  x.nslices = (uint32_t)L.nslices;
+  x.gfirst = L.gfirst.p, x.ngroups = (uint32_t)L.ngroups;
+  x.big = L.big.p, x.bflag = L.bflag.p;
+  int64_t nsplit = 0, nchunks = 0;
+  if (huge_on)
+    for (int64_t dg : L.big_deg) {
+      if (dg < split_min) break;
+      ++nsplit;
+      nchunks += (dg + kXChunk - 1) / kXChunk;
+    }
+  if (nchunks > 0xffffffffLL) throw Error(SG_ERANGE, "pr: too many huge-row chunks");
+  x.nsplit = (uint32_t)nsplit, x.nself = (uint32_t)(L.nbig - nsplit);
+  x.nchunks = (uint32_t)nchunks;
+  auto n1 = [](int64_t n) { return (size_t)std::max<int64_t>(n, 1); };
+  x.ck_first = (uint32_t *)alloc(sizeof(uint32_t) * n1(nsplit + 1));
+  x.ck_row = (uint32_t *)alloc(sizeof(uint32_t) * n1(nchunks));
+  x.ck_T = (long long *)alloc(sizeof(long long) * n1(nchunks));
+  x.ck_meta = (uint32_t *)alloc(sizeof(uint32_t) * n1(nchunks));
+  x.ck_guess = (int *)alloc(sizeof(int) * n1(nchunks));
+  x.head = head;
+  x.ctl = ctl;
+  x.carry = carry;
+  x.gain_bits = gmax;
+  return x;
+}
+
+}  // namespace
 }  // namespace sg

@@ -296,16 +296,16 @@ def test_edge_cut_ranks_as_threads(sg, golden, app, key):
                                      ("uniform16", 20000), ("rmat16", 1 << 15)])
 def test_pr_source_block_tiling(sg, golden, gname, S):
     """pr over the CSC split into source blocks of S vertices (the L2-resident
-    tiling large graphs use): ranks within the reference tolerance, the same
-    rounds, and the round log's bins / lb launches of the untiled CSC."""
+    tiling large graphs use): every row's sum carried from block to block in
+    source order, so the labels are still the reference's bit for bit; the
+    same rounds and the round log's bins / lb launches of the untiled CSC."""
     info = golden["runs"][gname]["pr/alb/d1"]
     g = _graph(sg, gname)
     p = sg.engine.device_params(sg.apps.make_app("pr"), sg.Scheduler("alb"), sg.KernelConfig(),
                                  1, 10 * g.num_vertices + 256)
     p.reserved = S
     labels, log, ms = g.device().run(p)
-    ref = sg.run_app(g, "pr")
-    assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
+    assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
     got = [[int(r["frontier_size"]), int(r["active_edges"])] for r in log]
     assert got == [x[:2] for x in info["per_round"]]
     assert [int(r["launches_lb"]) for r in log] == [x[4] for x in info["per_round"]]
@@ -320,8 +320,54 @@ def test_pr_tiling_thresholds(sg):
                                      sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
         p.reserved = 5000
         labels, log, ms = g.device().run(p)
-        assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
+        assert np.array_equal(labels, ref.labels)
         assert len(log) == len(ref.records)
+
+
+_SMALL_HS = r"""
+import json, sys
+sys.path.insert(0, %r)
+import paper_1911_09135_b200 as sg
+gold = json.loads(open(%r).read())
+bad = []
+for gname, runs in gold["runs"].items():
+    kind, scale = gname[:-2], int(gname[-2:])
+    g = sg.generate_rmat(scale, 16, 1, sg.graph.RMAT_SKEWED if kind == "rmat" else sg.graph.RMAT_UNIFORM)
+    for key, info in runs.items():
+        if not key.startswith("pr/"):
+            continue
+        _, sched, dev = key.split("/")
+        k = sched.split("-")[0]
+        thr = int(sched.split("-t")[1]) if "-t" in sched else None
+        for tile in (0, 300):
+            p = sg.engine.device_params(sg.apps.make_app("pr"), sg.Scheduler(k, threshold=thr),
+                                         sg.KernelConfig(), int(dev[1:]), 10 * g.num_vertices + 256)
+            p.reserved = tile
+            lab, log, ms = g.device().run(p)
+            if sg.engine.labels_sha256(lab) != info["labels_sha256"] or len(log) != info["rounds"]:
+                bad.append((gname, key, tile))
+print(json.dumps(bad))
+"""
+
+
+@pytest.mark.parametrize("hs", [2, 17, 300])
+def test_pr_exact_paths_with_small_hs(hs):
+    """SG_EXACT_HS shrinks the SELL rows so that the small golden graphs drive
+    every long-row path (split huge rows + walkers, walked rows, the exact
+    chunk step's binade crossings and guesses), untiled and tiled: still the
+    reference's labels bit for bit, for every scheduler and device count."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = _SMALL_HS % (str(root), str(root / "tests" / "golden" / "golden.json"))
+    env = dict(os.environ, SG_EXACT_HS=str(hs))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert json.loads(out.stdout.strip().splitlines()[-1]) == []
 
 
 @pytest.mark.parametrize("sched", ["alb", "twc", "lb", "vertex", "edge"])
