@@ -26,6 +26,17 @@ BSP run (all rounds to convergence) of the device engine.
            against MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline: the C oracle (oracle/sg_oracle.c, a restatement of the
            reference path) on this host, 1 thread, full workload.
+* labels : every workload's float64 labels are hashed (sha256, the
+           reference's numbering) and compared with tests/golden/
+           scale_golden.json (the C oracle pinned to the reference) together
+           with the round count -- pr included (bit-exact sums, sg_prx.cuh).
+* configs: BASELINE.json configs[2..4] at their own scales on this GPU --
+           C3 cc rmat25, C4 pr rmat25 skewed and uniform, C5 bfs / kcore
+           rmat27 -- each with its label check, dominant-kernel roofline and
+           ALB / TWC-only ratio.
+* ablation_heavy_skew: ALB vs TWC-only on rmat24 with the reference's
+           probabilities knob at (0.8, 0.1, 0.05, 0.05) (graph.py:274,
+           cli.py:113-114), every app, labels checked.
 ``--impl reference`` times that CPU path alone with all host threads.
 """
 
@@ -48,6 +59,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "GTEPS for BFS/SSSP/CC/PR on RMAT power-law graphs at 1/2/4/8 B200"
 SKEWED = (0.57, 0.19, 0.19, 0.05)
+HEAVY = (0.8, 0.1, 0.05, 0.05)   # SURVEY §7.6 heavier skew (the reference's probabilities knob)
 DEFAULT_THRESHOLD = 84 * 256  # KernelConfig().total_threads (simt.py:20-22)
 
 # algorithmic bytes (SURVEY §8d canonical widths)
@@ -77,6 +89,10 @@ def parse():
                     help="pr source-block size in vertices (0 = automatic, -1 = never tile)")
     ap.add_argument("--cta-bin", default="batched", choices=["batched", "classic"],
                     help="TWC CTA bin: edge-balanced batches (default) or one vertex per CTA")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the BASELINE configs C3-C5 at their own scales")
+    ap.add_argument("--no-heavy", action="store_true",
+                    help="skip the heavy-skew ALB vs TWC-only ablation")
     return ap.parse_args()
 
 
@@ -169,10 +185,9 @@ def algorithmic_bytes(app, log):
     mh = log["huge_edges"].astype(np.int64)
     ml = log["large_edges"].astype(np.int64)
     u = log["updated"].astype(np.int64)
-    if app == "pr":
+    if app == "pr":  # one exact-order pull kernel per round (sg_prx.cuh)
         nv = int(n[0]) if len(n) else 0
-        return {"pull_twc": int((eb * (m - mh - ml)).sum() + 40 * nv * len(n)),
-                "pull_large": int((eb * ml).sum()), "pull_lb": int((eb * mh).sum())}
+        return {"pr_pull": int((eb * m).sum() + 40 * nv * len(n))}
     if app == "kcore":
         return {"pull_twc": int((eb * (m - mh - ml) + VERTEX_BYTES * n).sum()),
                 "pull_large": int((eb * ml).sum()), "pull_lb": int((eb * mh).sum())}
@@ -186,13 +201,14 @@ def kernel_edges(log):
     m = log["active_edges"].astype(np.int64)
     mh = log["huge_edges"].astype(np.int64)
     ml = log["large_edges"].astype(np.int64)
-    return {"twc": int((m - mh - ml).sum()), "large": int(ml.sum()), "lb": int(mh.sum())}
+    return {"twc": int((m - mh - ml).sum()), "large": int(ml.sum()), "lb": int(mh.sum()),
+            "pull": int(m.sum())}
 
 
 # profiled-run kernel names -> the CUDA kernels ncu lists
 NCU_NAME = {"push_twc": "k_bm_twc", "push_large": "k_bm_large_pipe", "push_lb": "k_bm_lb",
             "compact": "k_bm_compact", "pull_twc": "k_pull_twc", "pull_large": "k_pull_large",
-            "pull_lb": "k_pull_lb"}
+            "pull_lb": "k_pull_lb", "pr_pull": "k_prx"}
 # random 4-byte gathers per second the chip sustains (scripts/micro/gather.cu on
 # B200: 272-275 G/s, one L1TEX wavefront per scattered lane)
 GATHER_CEILING = 272e9
@@ -203,20 +219,75 @@ def total_algorithmic_bytes(app, log, nv):
     return sum(b.values())
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+def ncu_traffic(kernel, workload):
+    """dram bytes per launch of `kernel` on `workload` from the committed ncu
+    summaries (profiles/ncu_summary.json, keyed "kernel|workload"); null when
+    that kernel was not captured on that workload."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get("dram_bytes_per_launch", {}).get(kernel)
+        return d.get("dram_bytes_per_launch", {}).get(f"{kernel}|{workload}")
     except (ValueError, OSError):
         return None
 
 
-def make_graph_device(sg, app, scale, uniform):
-    probs = (0.25,) * 4 if uniform else SKEWED
+def workload_name(app, scale, probs):
+    kind = "uniform" if tuple(probs) == (0.25,) * 4 else "heavy" if tuple(probs) == HEAVY else "rmat"
+    return f"{app}/{kind}{scale}"
+
+
+_GOLDEN = None
+
+
+def scale_golden():
+    global _GOLDEN
+    if _GOLDEN is None:
+        p = ROOT / "tests" / "golden" / "scale_golden.json"
+        _GOLDEN = json.loads(p.read_text()) if p.exists() else {}
+    return _GOLDEN
+
+
+def label_check(key, labels, log):
+    """sha256 of the float64 labels and the round count vs the committed golden."""
+    import hashlib
+    info = scale_golden().get(key)
+    if info is None:
+        return {"golden": None}
+    sha = hashlib.sha256(np.ascontiguousarray(labels, dtype=np.float64).tobytes()).hexdigest()
+    return {"labels_match": sha == info["labels_sha256"], "rounds_match": len(log) == info["rounds"],
+            "rounds": len(log), "golden_rounds": info["rounds"], "golden": "tests/golden/scale_golden.json:" + key}
+
+
+def roofline_of(app, kernels, plog, step_ms, workload):
+    """Dominant kernel of a profiled run vs the measured HBM peak."""
+    ab = algorithmic_bytes(app, plog)
+    timed = {k: v for k, v in kernels.items() if k in ab}
+    if not timed:
+        return None
+    dom = max(timed, key=lambda k: timed[k][1])
+    peak, peak_kind = peaks()
+    n_l, ms_l = kernels[dom]
+    achieved = ab[dom] / (ms_l / 1e3) / 1e9
+    name = NCU_NAME.get(dom, dom)
+    ke = kernel_edges(plog).get("pull" if dom == "pr_pull" else dom.split("_")[-1], 0)
+    return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_kind,
+            "traffic": ncu_traffic(name, workload),
+            "algorithmic_bytes_per_launch": ab[dom] / max(n_l, 1),
+            "avg_launch_ms": ms_l / max(n_l, 1), "launches": n_l,
+            "share_of_step": ms_l / sum(v[1] for v in kernels.values()),
+            "loop_bytes_per_s_GBps": sum(ab.values()) / (step_ms / 1e3) / 1e9,
+            "loop_frac": sum(ab.values()) / (step_ms / 1e3) / 1e9 / peak,
+            "gather_ceiling": {"unit": "G random label accesses/s", "peak": GATHER_CEILING / 1e9,
+                               "achieved": ke / (ms_l / 1e3) / 1e9,
+                               "frac": ke / (ms_l / 1e3) / GATHER_CEILING,
+                               "source": "scripts/micro/gather.cu (B200, measured)"}}
+
+
+def make_graph_device(sg, app, scale, uniform, probs=None):
+    probs = probs or ((0.25,) * 4 if uniform else SKEWED)
     g = sg.generate_rmat(scale, 16, 1, probs)
     return (sg.attach_random_weights(g, 2) if app == "sssp" else g), g
 
@@ -229,7 +300,7 @@ def run_params(sg, app, sched_kind, threshold, nv, classic=False):
     return sched, p
 
 
-def device_steps(torch, dev, params, steps, warmup, flush):
+def device_steps(torch, dev, params, steps, warmup, flush, keep=False):
     """W untimed + K timed BSP runs; per-run CUDA-event time of sg_run, L2 flushed before each."""
     for _ in range(max(1, warmup)):
         labels, log, ms = dev.run(params)
@@ -240,8 +311,51 @@ def device_steps(torch, dev, params, steps, warmup, flush):
         labels, log, ms = dev.run(params)
         out.append(ms)
     edges = int(log["active_edges"].sum())
-    return {"gteps": edges * len(out) / (sum(out) / 1e3) / 1e9,
-            "ms_per_step": sum(out) / len(out), "rounds": len(log), "edges_processed": edges}
+    r = {"gteps": edges * len(out) / (sum(out) / 1e3) / 1e9,
+         "ms_per_step": sum(out) / len(out), "rounds": len(log), "edges_processed": edges}
+    if keep:
+        r["_labels"], r["_log"] = labels, log
+    return r
+
+
+def config_entry(sg, torch, app, scale, probs, flush, threshold, steps, ablate=True,
+                 classic=True):
+    """One workload at its own scale: ALB runs (the graph stays resident, so
+    from the second run on it uses the relabeled store), labels vs the golden,
+    the dominant kernel's roofline, ALB / TWC-only.  The graph is dropped after."""
+    from paper_1911_09135_b200 import native
+    t0 = time.perf_counter()
+    g, _ = make_graph_device(sg, app, scale, False, probs)
+    dev = g.device()
+    nv, ne, _ = dev.info()
+    gen_s = time.perf_counter() - t0
+    wl = workload_name(app, scale, probs)
+    first = dev.run(run_params(sg, app, "alb", threshold, nv)[1])
+    r = device_steps(torch, dev, run_params(sg, app, "alb", threshold, nv)[1], steps, 1, flush,
+                     keep=True)
+    chk = label_check(wl, r.pop("_labels"), r.pop("_log"))
+    _, plog, pms, kernels = dev.run(run_params(sg, app, "alb", threshold, nv)[1], profile=True)
+    out = {"workload": wl, "num_vertices": nv, "num_edges": ne, **r, **chk,
+           "value_first_run": r["edges_processed"] / (first[2] / 1e3) / 1e9,
+           "build_ms": {k: round(v, 1) for k, v in dev.build_ms().items()},
+           "generate_s": round(gen_s, 2),
+           "roofline": roofline_of(app, kernels, plog, r["ms_per_step"], wl)}
+    if ablate:
+        tw = device_steps(torch, dev, run_params(sg, app, "twc", None, nv)[1], steps, 1, flush)
+        out["twc_gteps"] = tw["gteps"]
+        out["alb_over_twc"] = r["gteps"] / tw["gteps"]
+        if classic and app != "pr":
+            twc_c = device_steps(torch, dev, run_params(sg, app, "twc", None, nv, True)[1], steps,
+                                 1, flush)["gteps"]
+            alb_c = device_steps(torch, dev, run_params(sg, app, "alb", threshold, nv, True)[1],
+                                 steps, 1, flush)["gteps"]
+            out["classic_cta_bin"] = {"alb_gteps": alb_c, "twc_gteps": twc_c,
+                                      "alb_over_twc": alb_c / twc_c, "alb_over_twc_classic": r["gteps"] / twc_c}
+    del dev, g
+    import gc
+    gc.collect()
+    native.load().sg_release_cached()
+    return {k: (round(v, 4) if isinstance(v, float) else v) for k, v in out.items()}
 
 
 def cpu_oracle_run(app, off, tgt, w, threads):
@@ -322,10 +436,13 @@ def main():
             return native.dist_run(d, params, nccl_id, rank, world)
         return d.run(params)
 
+    warm_ms = []
     for _ in range(max(1, a.warmup)):
         labels, log, ms = step(dev)
+        warm_ms.append(ms)
     edges = int(log["active_edges"].sum())
     rounds = len(log)
+    workload = workload_name(a.app, a.scale, (0.25,) * 4 if a.uniform else SKEWED)
 
     # ---------------- timed region (device-resident inputs) ----------------
     if world > 1:
@@ -348,6 +465,7 @@ def main():
         total_ms = sgdist.max_over_ranks(torch.distributed, total_ms)
     # whole-job throughput: the (fixed) graph's processed edges per second
     value = edges * a.steps / (total_ms / 1e3) / 1e9
+    check = label_check(workload, labels, log2) if rank == 0 else None
 
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
@@ -361,46 +479,26 @@ def main():
             _warm = native.DeviceGraph.from_csr(off_p, tgt_p, w_p).run(params)
         torch.cuda.synchronize()
         e2e_s = []
-        for _ in range(max(1, min(a.steps, 3))):
+        for _ in range(max(1, a.steps)):
             t0 = time.perf_counter()
             dg = native.DeviceGraph.from_csr(off_p, tgt_p, w_p)
             lab_e, log_e, _ = step(dg)
             torch.cuda.synchronize()
             e2e_s.append(time.perf_counter() - t0)
             del dg
-        e2e_med = statistics.median(e2e_s)
+        e2e_tot = sum(e2e_s)
         if world > 1:
-            e2e_med = sgdist.max_over_ranks(torch.distributed, e2e_med)
-        e2e = {"value": edges / e2e_med / 1e9, "unit": "GTEPS",
+            e2e_tot = sgdist.max_over_ranks(torch.distributed, e2e_tot)
+        e2e = {"value": edges * len(e2e_s) / e2e_tot / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * statistics.median(e2e_s)}
-        assert np.array_equal(lab_e, labels) or a.app == "pr"
+               "ms_per_step": 1e3 * e2e_tot / len(e2e_s), "steps": len(e2e_s),
+               "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights), sg_run "
+                       "(original numbering: a fresh graph's first run), labels + round log D2H"}
+        assert np.array_equal(lab_e, labels)
 
     # ---------------- roofline from a profiled run ----------------
     _, plog, pms, kernels = dev.run(params, profile=True)
-    ab = algorithmic_bytes(a.app, plog)
-    timed = {k: v for k, v in kernels.items() if k in ab}
-    dom = max(timed, key=lambda k: timed[k][1]) if timed else None
-    peak, peak_kind = peaks()
-    roofline = None
-    if dom:
-        n_l, ms_l = kernels[dom]
-        achieved = ab[dom] / (ms_l / 1e3) / 1e9
-        traffic = ncu_traffic(NCU_NAME.get(dom, dom))
-        ke = kernel_edges(plog).get(dom.split("_")[-1], 0)
-        roofline = {"bound": "hbm", "kernel": NCU_NAME.get(dom, dom), "achieved": achieved,
-                    "peak": peak,
-                    "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
-                    "traffic": traffic, "algorithmic_bytes_per_launch": ab[dom] / max(n_l, 1),
-                    "avg_launch_ms": ms_l / max(n_l, 1), "launches": n_l,
-                    "share_of_step": ms_l / sum(v[1] for v in kernels.values()),
-                    "loop_bytes_per_s_GBps": sum(ab.values()) / (statistics.median(step_ms) / 1e3) / 1e9,
-                    # the bound that actually binds an irregular gather kernel
-                    "gather_ceiling": {"unit": "G random label accesses/s",
-                                       "peak": GATHER_CEILING / 1e9,
-                                       "achieved": ke / (ms_l / 1e3) / 1e9,
-                                       "frac": ke / (ms_l / 1e3) / GATHER_CEILING,
-                                       "source": "scripts/micro/gather.cu (B200, measured)"}}
+    roofline = roofline_of(a.app, kernels, plog, statistics.median(step_ms), workload)
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
@@ -411,8 +509,7 @@ def main():
         cpu = {"value": e_c / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "port",
                "sample": f"full {a.app} run on the same rmat{a.scale} graph, "
                          f"oracle/sg_oracle.c single thread ({dt:.1f} s)",
-               "labels_match": bool(np.array_equal(lab_c, labels)) if a.app != "pr" else
-               float(np.max(np.abs(lab_c - labels)))}
+               "labels_match": bool(np.array_equal(lab_c, labels))}
 
     # ------------- other apps + ALB vs TWC-only ablation (rank 0, N=1) -------------
     extra, ablation = {}, {}
@@ -421,22 +518,31 @@ def main():
         apps = [x for x in a.extra.split(",") if x]
         for app in apps:
             d = g.device() if app == "sssp" else g_base.device()
-            extra[app] = device_steps(torch, d, run_params(sg, app, "alb", a.threshold, nv)[1],
-                                      steps_x, 1, flush)
+            r = device_steps(torch, d, run_params(sg, app, "alb", a.threshold, nv)[1], steps_x, 1,
+                             flush, keep=True)
+            wl = workload_name(app, a.scale, (0.25,) * 4 if a.uniform else SKEWED)
+            r.update(label_check(wl, r.pop("_labels"), r.pop("_log")))
+            _, pl, _, ks = d.run(run_params(sg, app, "alb", a.threshold, nv)[1], profile=True)
+            rf = roofline_of(app, ks, pl, r["ms_per_step"], wl)
+            if rf:
+                r["roofline"] = {k: rf[k] for k in ("kernel", "achieved", "frac", "traffic",
+                                                    "share_of_step", "loop_frac")}
+            extra[app] = r
         if not a.no_ablation:
             for app in sorted(set([a.app] + apps)):
                 d = g.device() if app == "sssp" else g_base.device()
                 alb = extra[app]["gteps"] if app in extra else value
                 tw_b = device_steps(torch, d, run_params(sg, app, "twc", None, nv)[1], steps_x, 1,
                                     flush)["gteps"]
-                tw_c = device_steps(torch, d, run_params(sg, app, "twc", None, nv, True)[1],
-                                    steps_x, 1, flush)["gteps"]
-                alb_c = device_steps(torch, d, run_params(sg, app, "alb", a.threshold, nv, True)[1],
-                                     steps_x, 1, flush)["gteps"]
-                ablation[app] = {"alb_gteps": alb, "twc_gteps": tw_b,
-                                 "alb_over_twc": alb / tw_b,
-                                 "classic_cta_bin": {"alb_gteps": alb_c, "twc_gteps": tw_c,
-                                                     "alb_over_twc": alb_c / tw_c}}
+                ablation[app] = {"alb_gteps": alb, "twc_gteps": tw_b, "alb_over_twc": alb / tw_b}
+                if app != "pr":  # the exact pr kernel has one CTA-bin form (sg_prx.cuh)
+                    tw_c = device_steps(torch, d, run_params(sg, app, "twc", None, nv, True)[1],
+                                        steps_x, 1, flush)["gteps"]
+                    alb_c = device_steps(torch, d,
+                                         run_params(sg, app, "alb", a.threshold, nv, True)[1],
+                                         steps_x, 1, flush)["gteps"]
+                    ablation[app]["classic_cta_bin"] = {"alb_gteps": alb_c, "twc_gteps": tw_c,
+                                                        "alb_over_twc": alb_c / tw_c}
 
     # hardware load balance (paper Fig. 1 / 7 analogue): per-round edges per SM
     # from sg_run_cta_counts, worst round's max/mean and CV
@@ -465,6 +571,28 @@ def main():
             schedulers[kind] = round(device_steps(
                 torch, dev, run_params(sg, a.app, kind, a.threshold, nv)[1],
                 max(2, min(a.steps, 3)), 1, flush)["gteps"], 2)
+    build_ms = {k: round(v, 1) for k, v in dev.build_ms().items()}
+    value_first_run = edges / (warm_ms[0] / 1e3) / 1e9
+
+    # --------- the graphs of the other BASELINE configs / the skew ablation ---------
+    heavy, configs = {}, {}
+    if rank == 0 and world == 1 and (not a.no_heavy or not a.no_configs):
+        del dev, g, g_base
+        import gc
+        gc.collect()
+        native.load().sg_release_cached()
+        steps_c = 2
+        if not a.no_heavy:  # the paper's >= 1.5x claim needs real skew
+            for app in ("bfs", "sssp", "cc", "pr", "kcore"):
+                heavy[app] = config_entry(sg, torch, app, 24, HEAVY, flush, a.threshold, steps_c)
+        if not a.no_configs:
+            for key, (app, scale, probs) in (("C3_cc_rmat25", ("cc", 25, SKEWED)),
+                                             ("C4_pr_rmat25", ("pr", 25, SKEWED)),
+                                             ("C4_pr_uniform25", ("pr", 25, (0.25,) * 4)),
+                                             ("C5_bfs_rmat27", ("bfs", 27, SKEWED)),
+                                             ("C5_kcore_rmat27", ("kcore", 27, SKEWED))):
+                configs[key] = config_entry(sg, torch, app, scale, probs, flush, a.threshold,
+                                            steps_c, classic=False)
 
     if rank != 0:
         return
@@ -485,8 +613,12 @@ def main():
                    else "single",
                    "l2": "flushed (512 MB write) before every step",
                    "timing": "sum of per-step CUDA-event durations of sg_run (one graph launch "
-                             "per BSP run), max over ranks",
+                             "per BSP run, float64 labels in the reference's numbering included), "
+                             "max over ranks",
                    "wall_s_timed_region": wall},
+        "labels": check,
+        "value_first_run": value_first_run,
+        "build_ms": build_ms,
         "e2e": e2e,
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -496,6 +628,8 @@ def main():
         "apps": {k: {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                  for k, v in extra.items()},
         "ablation_alb_vs_twc": ablation,
+        "ablation_heavy_skew": heavy,
+        "configs": configs,
         "schedulers_gteps": schedulers,
     }
     print(json.dumps(line), flush=True)

@@ -139,6 +139,14 @@ int sg_graph_info(sg_graph *g, int64_t *nv, int64_t *ne, int32_t *weighted);
 int sg_graph_download(sg_graph *g, int32_t which, int64_t *offsets, int32_t *targets,
                       int64_t *weights);
 int sg_graph_view_size(sg_graph *g, int32_t which, int64_t *ne);
+/* The derived layouts a graph caches in HBM (like Graph.csc() / symmetrized(),
+ * graph.py:102, 117): CSC, symmetrized CSR, pr source blocks, the hot-vertex
+ * relabeled store (at most one at a time) and the exact-order pr layouts.
+ * sg_graph_release_views drops them all (rebuilt on demand);
+ * sg_graph_build_ms reports the last build time of each, in ms:
+ * {csc, symmetrized, relabeled store, exact pr layout}. */
+int sg_graph_release_views(sg_graph *g);
+int sg_graph_build_ms(sg_graph *g, double out[4]);
 void sg_graph_destroy(sg_graph *g);
 
 /* --- run level: engine.run (engine.py:190-246) -------------------------- */

@@ -220,7 +220,7 @@ struct PartRunner {
     mc.alloc(std::max<int64_t>(nv, 1));
     mirror_counts(*v, cuts, mc.p);
     rb.resize(nlocal);
-    stats_cap = std::min<int64_t>(max_rounds, 1 << 20);
+    stats_cap = ::sg::stats_cap(max_rounds);
     for (int i = 0; i < nlocal; ++i) rb[i].alloc_common(nv, 1);
     gctl.alloc(1);
     acc.alloc(1);
@@ -540,7 +540,7 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
   const Cuts cuts = make_cuts(v, cm.world);
   const uint32_t lo = (uint32_t)cuts.c[cm.rank], hi = (uint32_t)cuts.c[cm.rank + 1];
   RunBufs rb;
-  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.alloc_common(nv, stats_cap(max_rounds));
   PullArgs a = rb.pull_args(v, thr, 0);
   a.row_lo = lo, a.row_n = hi - lo;
   DBuf<uint32_t> mc;
@@ -640,7 +640,7 @@ void run_kcore_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_round
   const Cuts cuts = make_cuts(v, cm.world);
   const uint32_t lo = (uint32_t)cuts.c[cm.rank], hi = (uint32_t)cuts.c[cm.rank + 1];
   RunBufs rb;
-  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.alloc_common(nv, stats_cap(max_rounds));
   rb.dying.alloc(std::max<int64_t>(nv, 1));
   PullArgs a = rb.pull_args(v, thr, 1);
   a.row_lo = lo, a.row_n = hi - lo;

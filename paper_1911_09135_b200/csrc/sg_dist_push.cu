@@ -188,7 +188,7 @@ void run_dist_push(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds
     mirror_counts(v, cuts, mc.p);
   }
   RunBufs rb;
-  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.alloc_common(nv, stats_cap(max_rounds));
   PushArgs a = rb.push_args(v, thr);
   a.q[1] = a.q[0];
   a.dense_lo = lo, a.dense_n = hi - lo;

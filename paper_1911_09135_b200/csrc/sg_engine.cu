@@ -168,7 +168,7 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
   const bool cc = p.app == SG_APP_CC;
   const View &v = cc ? g.sym() : g.csr;
   const int64_t nv = v.nv;
-  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.alloc_common(nv, stats_cap(max_rounds));
   PushArgs a = rb.push_args(v, thr);
   a.q[1] = a.q[0];  // one frontier array: k_bm_compact rewrites it after the round
   if (lay.perm && p.devices == 1) {  // relabeled store: edgeless vertices are numbered last
@@ -270,7 +270,7 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
              int64_t max_rounds, const Layout &lay) {
   const View &v = g.csc();
   const int64_t nv = v.nv;
-  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.alloc_common(nv, stats_cap(max_rounds));
   PullArgs a = rb.pull_args(v, thr, 0);
   a.vertex = p.sched == SG_SCHED_VERTEX;
   a.row_n = (uint32_t)nv;
@@ -400,7 +400,7 @@ void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *l
   const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
   const View &v = g.sym();  // count rows: CSC(sym) and CSR(sym) rows hold the same multiset
   const int64_t nv = v.nv;
-  rb.alloc_common(nv, std::min<int64_t>(max_rounds, 1 << 20));
+  rb.alloc_common(nv, stats_cap(max_rounds));
   rb.dying.alloc(std::max<int64_t>(nv, 1));
   PullArgs a = rb.pull_args(v, thr, 1);
   a.vertex = p.sched == SG_SCHED_VERTEX;
@@ -451,6 +451,11 @@ void prep_kcore(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *l
     L.go("labels", k_labels_alive, grid_n(nv), 256, s, alive, nv, labels_d);
   };
 }
+
+// the device round log filled up before the run ended (see stats_cap)
+struct CapError : Error {
+  explicit CapError(const std::string &m) : Error(SG_ENOMEM, m) {}
+};
 
 struct RunResultC {
   int64_t rounds = 0;
@@ -553,6 +558,9 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
       SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     }
     Launcher &L = prof ? *prof : plain;
+    // the run's output -- float64 labels in the reference's numbering -- is
+    // produced on the device inside the timed region; only the D2H is outside
+    double *lab_out_d = lay.inv ? P.buf<double>(g.nv) : labels_d;
     SG_CUDA(cudaEventRecord(e0, s));
     if (rb.cta.p)
       SG_CUDA(cudaMemsetAsync(rb.cta.p, 0, rb.cta.bytes(), s));
@@ -572,6 +580,9 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
         if (h.done) break;
       }
     }
+    P.finish(L, s);
+    if (lay.inv) L.go("labels", k_unpermute, grid_n(g.nv), 256, s, (const double *)labels_d, lay.inv,
+                      g.nv, lab_out_d);
     SG_CUDA(cudaEventRecord(e1, s));
     SG_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
@@ -581,7 +592,6 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
     SG_CUDA(cudaMemcpy(&h, rb.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
     rounds = h.round;
     if (!prof) g_launches.fetch_add((int64_t)body_nodes * rounds, std::memory_order_relaxed);
-    P.finish(L, s);
     if (prof) {
       SG_CUDA(cudaStreamSynchronize(s));
       L.collect();
@@ -602,18 +612,12 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
         SG_CUDA(cudaMemcpy(cta->host, rb.cta.p, sizeof(uint64_t) * rb.cta_g * r,
                            cudaMemcpyDeviceToHost));
     }
-    if (labels_out && lay.inv) {
-      double *tmp = P.buf<double>(g.nv);
-      SG_LAUNCH(k_unpermute, grid_n(g.nv), 256, 0, s, labels_d, lay.inv, g.nv, tmp);
-      SG_CUDA(cudaMemcpyAsync(labels_out, tmp, sizeof(double) * g.nv, cudaMemcpyDeviceToHost, s));
-      SG_CUDA(cudaStreamSynchronize(s));
-    } else if (labels_out) {
-      SG_CUDA(cudaMemcpy(labels_out, labels_d, sizeof(double) * g.nv, cudaMemcpyDeviceToHost));
-    }
+    if (labels_out)
+      SG_CUDA(cudaMemcpy(labels_out, lab_out_d, sizeof(double) * g.nv, cudaMemcpyDeviceToHost));
     if (h.error == SG_ECONVERGE)
       throw Error(SG_ECONVERGE, "did not converge within " + std::to_string(max_rounds) + " rounds");
     if (h.error)
-      throw Error(h.error, "round log capacity (" + std::to_string(rb.stats_cap) + ") exhausted");
+      throw CapError("round log capacity (" + std::to_string(rb.stats_cap) + ") exhausted");
   } catch (...) {
     cleanup();
     throw;
@@ -649,15 +653,50 @@ constexpr int64_t kRelabelMinV = (int64_t)1 << 20;
 // 1 % of vertices source < 10 % of the edges keep their numbering.
 constexpr double kRelabelMinSkew = 0.10;
 
+// a relabeled store that does not fit next to what the device holds is not
+// built (the run keeps the original numbering): free HBM after returning the
+// allocator's cached blocks must exceed its size by 25 %
+bool relabel_fits(Graph &g, bool in_first) {
+  const int64_t need = g.relabel_bytes(in_first) + g.relabel_bytes(in_first) / 4;
+  size_t fr = 0, tot = 0;
+  SG_CUDA(cudaMemGetInfo(&fr, &tot));
+  if ((int64_t)fr >= need) return true;
+  dev_release_cached();
+  SG_CUDA(cudaMemGetInfo(&fr, &tot));
+  return (int64_t)fr >= need;
+}
+
 bool use_relabel(Graph &g, const sg_params &p) {
   if (p.devices != 1 || (p.flags & SG_FLAG_NO_RELABEL) || g.nv == 0) return false;
-  if (p.flags & SG_FLAG_RELABEL) return true;
+  const bool in_first = p.app == SG_APP_PR;
+  if (p.flags & SG_FLAG_RELABEL) return relabel_fits(g, in_first);
   if (g.nv < kRelabelMinV || g.runs++ < 1) return false;
-  return g.top1_share() >= kRelabelMinSkew;
+  return g.top1_share() >= kRelabelMinSkew && relabel_fits(g, in_first);
 }
+
+void run_app_layout(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out,
+                    int64_t cap, int64_t *nrounds, double *ms_out, Launcher *prof,
+                    const CtaOut *cta);
 
 void run_app(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out, int64_t cap,
              int64_t *nrounds, double *ms_out, Launcher *prof, const CtaOut *cta = nullptr) {
+  struct Restore {
+    int64_t v = stats_cap_limit();
+    ~Restore() { stats_cap_limit() = v; }
+  } restore;
+  try {
+    run_app_layout(g, p, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta);
+  } catch (const CapError &) {  // a longer run than the first log holds: repeat with room
+    const int64_t mr = p.max_rounds > 0 ? p.max_rounds : 10 * std::max<int64_t>(g.nv, 1) + 256;
+    if (stats_cap_limit() >= std::min(mr, kStatsCapMax)) throw;
+    stats_cap_limit() = std::min(mr, kStatsCapMax);
+    run_app_layout(g, p, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta);
+  }
+}
+
+void run_app_layout(Graph &g, const sg_params &p, double *labels_out, sg_round *rounds_out,
+                    int64_t cap, int64_t *nrounds, double *ms_out, Launcher *prof,
+                    const CtaOut *cta) {
   if (!use_relabel(g, p)) {
     run_app_on(g, p, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta, Layout{});
     return;
@@ -822,6 +861,20 @@ int sg_graph_download(sg_graph *gh, int32_t which, int64_t *offsets, int32_t *ta
       if (g.ne)
         SG_CUDA(cudaMemcpy(weights, g.w64.p, sizeof(int64_t) * g.ne, cudaMemcpyDeviceToHost));
     }
+  });
+}
+
+int sg_graph_release_views(sg_graph *g) {
+  return sg::guard([&] {
+    if (!g) throw Error(SG_ECONFIG, "null graph");
+    g->g->release_views();
+  });
+}
+
+int sg_graph_build_ms(sg_graph *g, double out[4]) {
+  return sg::guard([&] {
+    if (!g) throw Error(SG_ECONFIG, "null graph");
+    for (int i = 0; i < 4; ++i) out[i] = g->g->build_ms[i];
   });
 }
 

@@ -8,6 +8,7 @@
 //   generate_rmat / attach_random_weights: numpy PCG64 streams (graph.py:274-305)
 // The LSD radix sort (CUB) is stable, which is what makes these identical.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -466,11 +467,38 @@ __global__ void k_perm_rows(const int64_t *__restrict__ off, const uint32_t *__r
 }
 }  // namespace
 
+int64_t Graph::relabel_bytes(bool in_first) const {
+  int64_t b = (nv + 1) * 8 + ne * 4 + nv * 4 * 2;  // CSR copy + perm / inv
+  b += nv * 4 * 5 + nv * 8;                         // build temporaries
+  if (weighted) b += ne * 4;
+  if (in_first) b += (nv + 1) * 8 + ne * 4;         // the permuted CSC
+  return b;
+}
+
+void Graph::release_views() {
+  hot_.clear();
+  {
+    std::lock_guard<std::mutex> lk(exact_mu_);
+    exact_.clear();
+  }
+  tiles_.reset();
+  sym_.reset();
+  csc_.reset();
+  cov_k_ = -1;
+  top1_ = -1.0;
+  dev_release_cached();
+}
+
 Relabel &Graph::hot(int64_t K, bool in_first) {
   K = std::max<int64_t>(0, std::min(K, nv));
   const int64_t key = 2 * K + (in_first ? 1 : 0);
   auto it = hot_.find(key);
   if (it != hot_.end()) return *it->second;
+  // one relabeled store at a time: each is a full copy of the CSR (plus its
+  // own CSC / symmetrized views), so a graph run by push, pull and kcore apps
+  // would otherwise hold several
+  hot_.clear();
+  const auto t_build = std::chrono::steady_clock::now();
   auto R = std::make_unique<Relabel>();
   R->K = K;
   R->in_first = in_first;
@@ -591,14 +619,20 @@ Relabel &Graph::hot(int64_t K, bool in_first) {
   R->g = std::move(h);
   Relabel &out = *R;
   hot_[key] = std::move(R);
+  build_ms[2] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_build)
+                    .count();
   return out;
 }
 
 const View &Graph::csc() {
   if (!csc_) {
+    const auto t0 = std::chrono::steady_clock::now();
     auto v = std::make_unique<View>();
     build_transpose(*v, csr);
+    SG_CUDA(cudaDeviceSynchronize());
     csc_ = std::move(v);
+    build_ms[0] =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
   return *csc_;
 }
@@ -606,9 +640,13 @@ const View &Graph::csc() {
 const View &Graph::sym() {
   if (!sym_) {
     const View &c = csc();
+    const auto t0 = std::chrono::steady_clock::now();
     auto v = std::make_unique<View>();
     build_symmetrized(*v, csr, c);
+    SG_CUDA(cudaDeviceSynchronize());
     sym_ = std::move(v);
+    build_ms[1] =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
   return *sym_;
 }

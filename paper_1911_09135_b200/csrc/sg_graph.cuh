@@ -99,6 +99,11 @@ struct Graph {
   std::map<int64_t, std::unique_ptr<Relabel>> hot_;
   Relabel &hot(int64_t K, bool in_first = false);
   int64_t runs = 0;  // single-device runs on this graph (the relabeling is built from the 2nd)
+  // last build times (ms) of the derived layouts: csc, sym, relabeled store, exact pr
+  double build_ms[4] = {0, 0, 0, 0};
+  // HBM a relabeled store of this graph needs (estimate, bytes)
+  int64_t relabel_bytes(bool in_first) const;
+  void release_views();
   // share of the edges leaving the top 1 % of vertices by out-degree (cached;
   // rmat skewed: ~0.5, uniform: ~0.03) -- whether a degree relabeling pays
   double top1_share();

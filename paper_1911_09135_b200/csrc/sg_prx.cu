@@ -208,6 +208,7 @@ const ExactLayout &Graph::exact(int64_t hs, int64_t rlo, int64_t rhi) {
     auto L = std::make_unique<ExactLayout>();
     build_exact_layout(*L, c, hs, c, 0, nv, rlo, rhi);
     L->rlo = rlo, L->rhi = rhi;
+    build_ms[3] = L->build_ms;
     slot = std::move(L);
   }
   return *slot;

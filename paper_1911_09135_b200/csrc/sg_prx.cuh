@@ -323,7 +323,10 @@ __device__ __forceinline__ void sell_slice(const PrxArgs &a, PrFold &op, uint32_
   if (v != ExactLayout::kEmpty) row_end(a, op, v, f, acc);
 }
 
-__global__ void __launch_bounds__(kTB) k_prx(PrxArgs a, PrFold op) {
+#ifndef SG_PRX_MINB
+#define SG_PRX_MINB 1  // min resident CTAs per SM (register cap) for k_prx
+#endif
+__global__ void __launch_bounds__(kTB, SG_PRX_MINB) k_prx(PrxArgs a, PrFold op) {
   __shared__ double redd[kWarpsTB];
   __shared__ unsigned long long redb[kWarpsTB];
   Ctl *ctl = a.ctl;

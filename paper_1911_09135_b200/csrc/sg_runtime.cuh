@@ -471,6 +471,19 @@ __global__ void k_kcore_advance(Ctl *ctl, Loop lp) {
 }
 
 // ------------------------------------------------------------ run state --
+// Device round-log capacity of a run: min(max_rounds, 2^20) records first; a
+// run that outgrows it is repeated with room for max_rounds (up to 2^26
+// records, 5.9 GB), so the only round limit is the reference's max_rounds
+// (engine.py:206-209).  Runs are deterministic, so the repeat is identical.
+inline int64_t &stats_cap_limit() {
+  static thread_local int64_t lim = (int64_t)1 << 20;
+  return lim;
+}
+inline int64_t stats_cap(int64_t max_rounds) {
+  return std::max<int64_t>(1, std::min<int64_t>(max_rounds, stats_cap_limit()));
+}
+constexpr int64_t kStatsCapMax = (int64_t)1 << 26;
+
 struct RunBufs {
   DBuf<Ctl> ctl;
   DBuf<RoundStat> stats;

@@ -32,7 +32,7 @@ EXPORTS = (
     "sg_lb_kernel", "sg_nccl_unique_id", "sg_dist_run", "sg_dist_run_threads",
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
     "sg_host_alloc", "sg_host_free", "sg_release_cached", "sg_run_cta_counts",
-    "sg_graph_load_sgb1", "sg_nccl_release",
+    "sg_graph_load_sgb1", "sg_nccl_release", "sg_graph_release_views", "sg_graph_build_ms",
 )
 
 
@@ -105,6 +105,8 @@ def load(path: Path | None = None):
             "sg_release_cached": ([], None),
             "sg_graph_load_sgb1": ([ctypes.c_char_p, pp], ctypes.c_int),
             "sg_nccl_release": ([], None),
+            "sg_graph_release_views": ([P], ctypes.c_int),
+            "sg_graph_build_ms": ([P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -246,6 +248,17 @@ class DeviceGraph:
         h = ctypes.c_void_p()
         check(load().sg_graph_with_weights(self.handle, ptr(weights), ctypes.byref(h)))
         return DeviceGraph(h)
+
+    def release_views(self):
+        """Drop the cached derived layouts (CSC, symmetrized, relabeled store,
+        exact pr layouts); they are rebuilt on demand."""
+        check(load().sg_graph_release_views(self.handle))
+
+    def build_ms(self):
+        """Last build times (ms) of {csc, sym, relabel, exact}."""
+        out = np.zeros(4, dtype=np.float64)
+        check(load().sg_graph_build_ms(self.handle, ptr(out)))
+        return dict(zip(("csc", "sym", "relabel", "exact"), out.tolist()))
 
     def download(self, which=0, weights=False):
         """Host copies of a view: 0 CSR, 1 CSC, 2 symmetrized CSR."""

@@ -1,6 +1,6 @@
 """Summarise ncu outputs (launch list CSV + --set full report) into profiles/.
 
-usage: python scripts/ncu_summary.py TAG [--kernel k_push_twc]
+usage: python scripts/ncu_summary.py TAG --workload sssp/rmat24
 reads  gpurun_out/TAG_launches.csv, gpurun_out/TAG_prof.ncu-rep
 writes profiles/TAG_ncu.json (+ updates profiles/ncu_summary.json, which
 bench.py reads for roofline.traffic)
@@ -75,7 +75,7 @@ def full(tag):
 
 def main():
     tag = sys.argv[1]
-    kern = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else "k_push_twc"
+    wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else "sssp/rmat24"
     summary = {"tag": tag, "launch_list": launches(tag), "full": full(tag)}
     per = collections.defaultdict(list)
     for d in summary["full"] or []:
@@ -94,7 +94,7 @@ def main():
         b = [d.get("dram__bytes_read.sum", 0) * scale[units["dram__bytes_read.sum"]]
              + d.get("dram__bytes_write.sum", 0) * scale[units["dram__bytes_write.sum"]] for d in lst]
         t = [d.get("gpu__time_duration.sum", 0) for d in lst]
-        summary["dram_bytes_per_launch"][k] = sum(b) / len(b)
+        summary["dram_bytes_per_launch"][f"{k}|{wl}"] = sum(b) / len(b)
         summary.setdefault("captured_launches", {})[k] = {"n": len(lst), "dram_bytes": b,
                                                           "time": t,
                                                           "time_unit": units["gpu__time_duration.sum"]}
@@ -103,7 +103,10 @@ def main():
     agg = ROOT / "profiles" / "ncu_summary.json"
     prev = json.loads(agg.read_text()) if agg.exists() else {}
     prev.setdefault("dram_bytes_per_launch", {}).update(summary["dram_bytes_per_launch"])
-    prev["source"] = f"profiles/{tag}_ncu.json"
+    prev.setdefault("sources", {}).update({k: f"profiles/{tag}_ncu.json"
+                                           for k in summary["dram_bytes_per_launch"]})
+    prev["note"] = ("dram bytes per launch (ncu --set full) keyed 'kernel|workload'; bench.py "
+                    "reports traffic only for the workload a kernel was captured on")
     agg.write_text(json.dumps(prev, indent=1) + "\n")
     print(json.dumps({k: v for k, v in summary.items() if k != "full"}, indent=1)[:3000])
 
