@@ -21,7 +21,7 @@ for i in range(4):
     ms.append(t)
 _, plog, pms, kernels = dev.run(params, profile=True)
 import os
-print(json.dumps({"scale": scale, "uniform": uni, "hs": os.environ.get("SG_EXACT_HS", "512"),
+print(json.dumps({"scale": scale, "uniform": uni, "hs": os.environ.get("SG_EXACT_HS", "2048 (default)"),
                   "rounds": len(log), "ms_runs": [round(x, 2) for x in ms],
                   "gteps": round(int(log["active_edges"].sum()) / (min(ms[1:]) / 1e3) / 1e9, 1),
                   "kernels": {k: [v[0], round(v[1], 3)] for k, v in kernels.items()}}), flush=True)
