@@ -103,6 +103,8 @@ typedef struct sg_round { /* one BSP round (engine.py:116-163) */
 
 const char *sg_last_error(void);
 int sg_device_count(int *count);
+/* the CUDA device this thread's later calls use (one process per GPU: LOCAL_RANK) */
+int sg_set_device(int32_t device);
 
 /* Memory.  Device buffers come from a caching allocator (no cudaMalloc /
  * cudaFree per graph or run after warm-up); sg_release_cached returns the
@@ -188,6 +190,46 @@ int sg_dist_run(sg_graph *g, const sg_params *p, const uint8_t nccl_id[128], int
  * GPU (collectives = device kernels over the ranks' buffers): the multi-rank
  * protocol on one device.  Outputs are rank 0's. */
 int sg_dist_run_threads(sg_graph *g, const sg_params *p, int32_t world, double *labels_out,
+                        sg_round *rounds_out, int64_t rounds_cap, int64_t *nrounds,
+                        double *ms_out);
+
+/* --- multi-GPU edge cut over NVLink peer memory (the B200 transport) ------
+ * Replaces the reference's per-device loop + sync_labels (engine.py:64-113,
+ * 205-235) with one process per GPU, no collective library in the loop.
+ *
+ * sg_graph_partition: rows [cuts[rank], cuts[rank+1]) of one view of g (the
+ * reference's make_partition cuts, engine.py:64-75) as a graph of their own:
+ * kind 0 = CSR rows (+ weights; bfs / sssp), 1 = CSC rows (pr; the full CSR
+ * offsets are kept for the out-degrees), 2 = symmetrized rows (cc / kcore).
+ * Only the block's edges are stored, so g can be destroyed afterwards.
+ * sg_graph_part_info: kind / rank / world, cuts_out[world + 1], edges of the
+ * full view.  A partition is run only through sg_team_run.
+ *
+ * sg_team_create allocates this rank's symmetric region for nv vertices and
+ * exports it (handle_out: 64-byte CUDA IPC handle); after exchanging the
+ * handles out of band (e.g. torch.distributed all_gather), sg_team_connect
+ * maps every peer's region (handles: world x 64 bytes in rank order).
+ * sg_team_run: one BSP run of this rank's partition, the whole loop one
+ * CUDA-graph launch; the round's kernels store label updates straight into
+ * the owners' / mirrors' regions and synchronise with a device-side barrier
+ * (20 s timeout -> SG_ECUDA, the team is then unusable).  p->devices must be
+ * the team size.  labels_out gets the merged labels on every rank, rounds_out
+ * the global round log (comm_sent / comm_broadcast as engine.py:105-109,
+ * 232-234). */
+int sg_graph_partition(sg_graph *g, int32_t kind, int32_t world, int32_t rank, sg_graph **out);
+int sg_graph_part_info(sg_graph *g, int32_t *kind, int32_t *rank, int32_t *world,
+                       int64_t *cuts_out, int64_t *full_ne);
+typedef struct sg_team sg_team;
+int sg_team_create(int32_t rank, int32_t world, int64_t nv, sg_team **out,
+                   uint8_t handle_out[64]);
+int sg_team_connect(sg_team *t, const uint8_t *handles);
+int sg_team_run(sg_team *t, sg_graph *part, const sg_params *p, double *labels_out,
+                sg_round *rounds_out, int64_t rounds_cap, int64_t *nrounds, double *ms_out);
+void sg_team_destroy(sg_team *t);
+/* The peer transport with `world` ranks as host threads on this GPU (each
+ * with its own partition of g and region; peers are plain device pointers).
+ * Outputs are rank 0's. */
+int sg_peer_run_threads(sg_graph *g, const sg_params *p, int32_t world, double *labels_out,
                         sg_round *rounds_out, int64_t rounds_cap, int64_t *nrounds,
                         double *ms_out);
 

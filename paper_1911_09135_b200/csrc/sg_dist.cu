@@ -31,6 +31,7 @@
 
 #include "sg_comm.cuh"
 #include "sg_prx.cuh"
+#include "sg_distk.cuh"
 
 namespace sg {
 namespace {
@@ -448,85 +449,6 @@ void dispatch_push(PartRunner &R, Comm *comm, double *labels_out, sg_round *roun
 // Reference: the pull view's row blocks (engine.py:64-85); a pull round writes
 // only owned rows, so comm_sent is 0 and every changed value is broadcast to
 // its mirrors (comm_broadcast, engine.py:232-234).
-constexpr int kDistN = 12;  // counter block summed over ranks each round
-
-// pr: {twc launches, lb launches, nhuge, huge_edges, nlarge, large_edges}
-__global__ void k_dist_pr_collect(const Ctl *ctl, int has_rows, long long *acc) {
-  if (threadIdx.x || ctl->done) return;
-  acc[0] = has_rows;
-  acc[1] = ctl->nhuge > 0;
-  acc[2] = ctl->nhuge;
-  acc[3] = (long long)ctl->huge_edges;
-  acc[4] = ctl->nlarge;
-  acc[5] = (long long)ctl->large_edges;
-}
-
-// kcore, after the count phase and the kill: this rank's round counters
-__global__ void k_dist_kc_collect(PullArgs a, long long *acc) {
-  const Ctl *ctl = a.ctl;
-  if (threadIdx.x || ctl->done) return;
-  const long long fs = ctl->dense ? a.row_n : ctl->fsize;
-  acc[0] = fs;
-  acc[1] = (long long)ctl->edges;
-  acc[2] = ctl->nhuge;
-  acc[3] = (long long)ctl->huge_edges;
-  acc[4] = ctl->nlarge;
-  acc[5] = (long long)ctl->large_edges;
-  acc[6] = ctl->ndying;
-  acc[7] = (long long)ctl->comm_bcast;
-  acc[8] = fs > 0;            // run_round only for a non-empty local frontier (engine.py:216)
-  acc[9] = ctl->nhuge > 0;
-}
-
-// owned vertices marked this round (alive neighbours of any rank's dying
-// vertices, after the mark all-reduce) -> this rank's next local frontier
-__global__ void k_dist_kc_compact(const Ctl *ctl, const uint32_t *mark, uint32_t lo, uint32_t hi,
-                                  uint32_t *q0, uint32_t *q1, uint32_t *nsize) {
-  if (ctl->done) return;
-  const uint32_t round = ctl->round, stamp = round + 1;
-  uint32_t *q = (round & 1) ? q0 : q1;
-  const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < hi - lo; b += st) {
-    const uint64_t i = b + threadIdx.x;
-    const bool m = i < hi - lo && mark[lo + i] == stamp;
-    warp_append(m, lo + (uint32_t)i, q, nsize);
-  }
-}
-
-__global__ void k_dist_kc_next(const Ctl *ctl, long long *acc) {
-  if (threadIdx.x || ctl->done) return;
-  acc[10] = ctl->nsize;
-}
-
-// kcore round bookkeeping from the rank-summed counters (apps.py:220-232)
-__global__ void k_dist_kc_advance(PullArgs a, long long *acc, Loop lp) {
-  Ctl *ctl = a.ctl;
-  if (threadIdx.x || ctl->done) return;
-  const uint32_t round = ctl->round;
-  RoundStat &s = a.stats[round];
-  s.frontier_size = acc[0];
-  s.active_edges = acc[1];
-  s.huge_count = acc[2];
-  s.huge_edges = acc[3];
-  s.large_count = acc[4];
-  s.large_edges = acc[5];
-  s.updated = acc[6];
-  s.comm_sent = 0;
-  s.comm_broadcast = acc[7];
-  s.launches_twc = acc[8];
-  s.launches_lb = acc[9];
-  const bool stop = acc[6] == 0 || acc[10] == 0;
-  ctl->fsize = ctl->nsize;
-  ctl->nsize = 0;
-  ctl->ndying = 0;
-  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
-  ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_bcast = 0;
-  ctl->dense = 0;
-  ctl->round = round + 1;
-  for (int i = 0; i < kDistN; ++i) acc[i] = 0;
-  loop_test(ctl, round, stop, lp);
-}
-
 // pr over NCCL: this rank folds its edge-cut rows [lo, hi) with the exact-order
 // pull (sg_prx.cuh, on a layout of its own rows), then every rank's new aux
 // slice is broadcast, max |delta|, comm_broadcast and the bin counters are

@@ -23,26 +23,10 @@
 //      frontier (quiescence).
 // bfs runs as unit-weight relaxation (identical labels and rounds).
 #include "sg_comm.cuh"
+#include "sg_distk.cuh"
 
 namespace sg {
 namespace {
-
-constexpr int kDP = 12;  // counter block: fsize, edges, nhuge, huge_edges, nlarge,
-                         // large_edges, sent, bcast, twc, lb, next, pad
-
-__global__ void k_dp_collect(PushArgs a, long long *acc) {
-  const Ctl *ctl = a.ctl;
-  if (threadIdx.x || ctl->done) return;
-  const long long fs = ctl->dense ? a.dense_n : ctl->fsize;
-  acc[0] = fs;
-  acc[1] = (long long)ctl->edges;
-  acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
-  acc[3] = a.sched >= 2 ? 0 : (long long)ctl->huge_edges;
-  acc[4] = a.sched >= 2 ? 0 : ctl->nlarge;
-  acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
-  acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
-  acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
-}
 
 // marked vertices owned by each rank (this rank's own rows excluded)
 __global__ void __launch_bounds__(256) k_dp_count(const uint32_t *nb, int64_t nv, Cuts cuts,
@@ -132,40 +116,6 @@ __global__ void k_dp_next(const Ctl *ctl, long long *acc, unsigned long long *se
   if (threadIdx.x || ctl->done) return;
   acc[10] = ctl->nsize;
   acc[6] = (long long)*sent;
-}
-
-__global__ void k_dp_advance(PushArgs a, long long *acc, Loop lp) {
-  Ctl *ctl = a.ctl;
-  if (threadIdx.x || ctl->done) return;
-  const uint32_t round = ctl->round;
-  RoundStat &s = a.stats[round];
-  s.frontier_size = acc[0];
-  s.active_edges = acc[1];
-  s.huge_count = acc[2];
-  s.huge_edges = acc[3];
-  s.large_count = acc[4];
-  s.large_edges = acc[5];
-  s.updated = acc[10];
-  s.comm_sent = acc[6];
-  s.comm_broadcast = acc[7];
-  s.launches_twc = acc[8];
-  s.launches_lb = acc[9];
-  ctl->fsize = ctl->nsize;
-  ctl->nsize = 0;
-  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
-  ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
-  ctl->dense = 0;
-  ctl->round = round + 1;
-  const bool empty = acc[10] == 0;
-  for (int i = 0; i < kDP; ++i) acc[i] = 0;
-  loop_test(ctl, round, empty, lp);
-}
-
-template <class T>
-__global__ void k_iota_from(T *p, int64_t n, int64_t base) {
-  const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
-    p[i] = (T)(base + i);
 }
 
 template <int KIND>

@@ -474,6 +474,8 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
   if (p.app < SG_APP_BFS || p.app > SG_APP_KCORE) throw Error(SG_ECONFIG, "unknown app");
   if (p.devices < 1) throw Error(SG_ECONFIG, "device count must be >= 1");
   if (g.nv > 0x7fffffffLL) throw Error(SG_ERANGE, "vertex ids must fit int32");
+  if (g.is_part())
+    throw Error(SG_ECONFIG, "an edge-cut partition runs with sg_team_run (one rank per GPU)");
   if ((p.app == SG_APP_BFS || p.app == SG_APP_SSSP) && (p.source < 0 || p.source >= g.nv))
     throw Error(SG_ECONFIG, "source " + std::to_string(p.source) + " outside graph");
   if (p.app == SG_APP_PR && !(p.damping > 0.0 && p.damping < 1.0))
@@ -741,6 +743,10 @@ void sg_host_free(void *p) {
 
 void sg_release_cached(void) { sg::dev_release_cached(); }
 
+int sg_set_device(int32_t device) {
+  return sg::guard([&] { SG_CUDA(cudaSetDevice(device)); });
+}
+
 int sg_device_count(int *count) {
   return sg::guard([&] { SG_CUDA(cudaGetDeviceCount(count)); });
 }
@@ -842,7 +848,9 @@ int sg_graph_info(sg_graph *g, int64_t *nv, int64_t *ne, int32_t *weighted) {
 
 int sg_graph_view_size(sg_graph *g, int32_t which, int64_t *ne) {
   return sg::guard([&] {
-    *ne = which == 2 ? 2 * g->g->ne : g->g->ne;
+    const sg::Graph &G = *g->g;
+    *ne = which == 0 ? G.csr.ne : which == 1 ? (G.csc_ ? G.csc_->ne : G.ne)
+                                             : (G.sym_ ? G.sym_->ne : 2 * G.ne);
   });
 }
 

@@ -477,6 +477,12 @@ int64_t Graph::relabel_bytes(bool in_first) const {
 
 void Graph::release_views() {
   hot_.clear();
+  if (is_part()) {  // a partition's view is its data, not a derived layout
+    std::lock_guard<std::mutex> lk(exact_mu_);
+    exact_.clear();
+    dev_release_cached();
+    return;
+  }
   {
     std::lock_guard<std::mutex> lk(exact_mu_);
     exact_.clear();
@@ -625,6 +631,9 @@ Relabel &Graph::hot(int64_t K, bool in_first) {
 }
 
 const View &Graph::csc() {
+  if (is_part() && !csc_)
+    throw Error(SG_ECONFIG, "this edge-cut partition holds no CSC rows (partition kind " +
+                                std::to_string(part.kind) + ")");
   if (!csc_) {
     const auto t0 = std::chrono::steady_clock::now();
     auto v = std::make_unique<View>();
@@ -638,6 +647,9 @@ const View &Graph::csc() {
 }
 
 const View &Graph::sym() {
+  if (is_part() && !sym_)
+    throw Error(SG_ECONFIG, "this edge-cut partition holds no symmetrized rows (partition kind " +
+                                std::to_string(part.kind) + ")");
   if (!sym_) {
     const View &c = csc();
     const auto t0 = std::chrono::steady_clock::now();

@@ -73,6 +73,22 @@ struct Relabel;
 struct Graph {
   int64_t nv = 0, ne = 0;
   View csr;
+  // Edge-cut partition (sg_peer.cu, Gluon's outgoing edge cut, engine.py:64-85):
+  // this graph holds only rows [lo, hi) of one traversal view of a full graph
+  // -- kind 0 the CSR (bfs / sssp, with the rows' weights), 1 the CSC (pr; csr
+  // then keeps only the full CSR offsets, the out-degrees pr divides by),
+  // 2 the symmetrized CSR (cc / kcore).  The view keeps V + 1 offsets (rows
+  // outside the block are empty) so the single-device kernels index it by
+  // global vertex id; its edges are the block's only.
+  struct Part {
+    int kind = -1;
+    int rank = 0, world = 1;
+    std::vector<long long> cuts;  // the reference's cuts of the full view (world + 1)
+    int64_t lo = 0, hi = 0;
+    int64_t full_ne = 0;          // edges of the full view
+    std::shared_ptr<void> mirrors;  // the peer transport's mirror masks (sg_peer.cu)
+  } part;
+  bool is_part() const { return part.kind >= 0; }
   bool weighted = false;
   int64_t wmin = 0, wmax = 0;
   DBuf<int64_t> w64;  // the reference's int64 weights (graph.py:35-37)

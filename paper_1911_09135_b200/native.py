@@ -33,6 +33,8 @@ EXPORTS = (
     "sg_twc_kernel", "sg_vertex_kernel", "sg_edge_kernel", "sg_kernel_launches",
     "sg_host_alloc", "sg_host_free", "sg_release_cached", "sg_run_cta_counts",
     "sg_graph_load_sgb1", "sg_nccl_release", "sg_graph_release_views", "sg_graph_build_ms",
+    "sg_graph_partition", "sg_graph_part_info", "sg_team_create", "sg_team_connect",
+    "sg_team_run", "sg_team_destroy", "sg_peer_run_threads", "sg_set_device",
 )
 
 
@@ -107,6 +109,15 @@ def load(path: Path | None = None):
             "sg_nccl_release": ([], None),
             "sg_graph_release_views": ([P], ctypes.c_int),
             "sg_graph_build_ms": ([P, P], ctypes.c_int),
+            "sg_set_device": ([i32], ctypes.c_int),
+            "sg_graph_partition": ([P, i32, i32, i32, pp], ctypes.c_int),
+            "sg_graph_part_info": ([P, P, P, P, P, P], ctypes.c_int),
+            "sg_team_create": ([i32, i32, i64, pp, P], ctypes.c_int),
+            "sg_team_connect": ([P, P], ctypes.c_int),
+            "sg_team_run": ([P, P, ctypes.POINTER(Params), P, P, i64, P, P], ctypes.c_int),
+            "sg_team_destroy": ([P], None),
+            "sg_peer_run_threads": ([P, ctypes.POINTER(Params), i32, P, P, i64, P, P],
+                                    ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -178,6 +189,11 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     check(load().sg_device_count(ctypes.byref(n)))
     return n.value
+
+
+def set_device(device: int):
+    """Select the CUDA device for this thread's later library calls."""
+    check(load().sg_set_device(int(device)))
 
 
 def kernel_launches() -> int:
@@ -357,6 +373,100 @@ def dist_run_threads(dev: DeviceGraph, params: Params, world: int, rounds_cap=1 
     check(load().sg_dist_run_threads(dev.handle, ctypes.byref(params), world, ptr(labels),
                                      ptr(rounds), rounds_cap, ctypes.byref(n), ctypes.byref(ms)))
     return labels, rounds[: min(n.value, rounds_cap)].copy(), ms.value
+
+
+def _run_with_log(call, nv, rounds_cap):
+    """call(labels, rounds, n, ms) -> code; repeated with a larger round log
+    when the run outgrew it (runs are deterministic), never truncated."""
+    labels = pinned_empty(nv, np.float64)
+    while True:
+        rounds = np.zeros(max(int(rounds_cap), 1), dtype=ROUND_DTYPE)
+        n = ctypes.c_int64(0)
+        ms = ctypes.c_double(0.0)
+        code = call(labels, rounds, n, ms)
+        if n.value <= len(rounds) or code not in (SG_OK, SG_ECONVERGE):
+            break
+        rounds_cap = n.value
+    log = rounds[: min(n.value, len(rounds))].copy()
+    if code == SG_ECONVERGE:
+        err = ConvergenceError((load().sg_last_error() or b"").decode())
+        err.metrics_log = log
+        raise err
+    check(code)
+    return labels, log, ms.value
+
+
+PART_CSR, PART_CSC, PART_SYM = 0, 1, 2
+
+
+class DevicePartition(DeviceGraph):
+    """One rank's edge-cut rows of a traversal view (sg_graph_partition):
+    only rows [cuts[rank], cuts[rank+1]) and their edges live in HBM."""
+
+    @classmethod
+    def of(cls, dev: DeviceGraph, kind: int, world: int, rank: int):
+        h = ctypes.c_void_p()
+        check(load().sg_graph_partition(dev.handle, kind, world, rank, ctypes.byref(h)))
+        return cls(h)
+
+    def part_info(self):
+        kind, rank, world = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        cuts = np.zeros(64, dtype=np.int64)
+        full = ctypes.c_int64()
+        check(load().sg_graph_part_info(self.handle, ctypes.byref(kind), ctypes.byref(rank),
+                                        ctypes.byref(world), ptr(cuts), ctypes.byref(full)))
+        return {"kind": kind.value, "rank": rank.value, "world": world.value,
+                "cuts": cuts[: world.value + 1].copy(), "full_edges": full.value}
+
+
+class Team:
+    """One rank's symmetric HBM region of the NVLink peer transport
+    (sg_team_create / sg_team_connect): every rank exports its region as a
+    CUDA IPC handle, the handles are exchanged out of band, and each rank maps
+    its peers' regions.  Runs are sg_team_run on this rank's partition."""
+
+    def __init__(self, rank: int, world: int, num_vertices: int):
+        self._h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 64)()
+        check(load().sg_team_create(rank, world, num_vertices, ctypes.byref(self._h), buf))
+        self.handle_bytes = bytes(buf)
+        self.rank, self.world, self.num_vertices = rank, world, num_vertices
+
+    def connect(self, handles):
+        blob = b"".join(bytes(h) for h in handles)
+        if len(blob) != 64 * self.world:
+            raise SimtGraphError("need one 64-byte IPC handle per rank")
+        arr = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(load().sg_team_connect(self._h, arr))
+
+    def run(self, part: DevicePartition, params: Params, rounds_cap=1 << 16):
+        nv, _, _ = part.info()
+        return _run_with_log(
+            lambda lab, rounds, n, ms: load().sg_team_run(
+                self._h, part.handle, ctypes.byref(params), ptr(lab), ptr(rounds), len(rounds),
+                ctypes.byref(n), ctypes.byref(ms)), nv, rounds_cap)
+
+    def close(self):
+        if self._h and _lib is not None:
+            _lib.sg_team_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
+
+
+def peer_run_threads(dev: DeviceGraph, params: Params, world: int, rounds_cap=1 << 16):
+    """The NVLink peer transport with `world` ranks as host threads on this GPU
+    (peers = the other ranks' regions in the same HBM): rank 0's labels and the
+    global round log."""
+    nv, _, _ = dev.info()
+    return _run_with_log(
+        lambda lab, rounds, n, ms: load().sg_peer_run_threads(
+            dev.handle, ctypes.byref(params), world, ptr(lab), ptr(rounds), len(rounds),
+            ctypes.byref(n), ctypes.byref(ms)), nv, rounds_cap)
 
 
 def pcg64_words(seed) -> np.ndarray:
