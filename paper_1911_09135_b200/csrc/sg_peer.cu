@@ -43,6 +43,7 @@
 // threads on one GPU (peers = plain device pointers), which is how the
 // single-GPU tests drive it.
 #include <chrono>
+#include <condition_variable>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -425,6 +426,38 @@ struct ConvAlive {
 };
 
 // ===================================================================== host
+// Ranks as host threads on one GPU: a thread that launches a kernel for the
+// first time may make the driver load it (lazy loading), which waits for the
+// whole device -- including a peer's barrier kernel that spins until this
+// thread launches its own barrier.  So every host-launched barrier is preceded
+// by a host rendezvous of the threads: a barrier kernel spins only after every
+// rank has issued everything (and loaded every kernel) before it.
+struct HostBarrier {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  bool failed = false;
+  explicit HostBarrier(int w) : world(w) {}
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0, ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g || failed; });
+    }
+    if (failed) throw Error(SG_ECUDA, "a peer rank failed");
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lk(mu);
+    failed = true;
+    cv.notify_all();
+  }
+};
+
 std::atomic<uint64_t> g_team_ids{0};
 struct Team {
   uint64_t id = ++g_team_ids;
@@ -434,6 +467,7 @@ struct Team {
   char *peer[kMaxParts] = {};
   bool ipc[kMaxParts] = {};
   bool connected = false, poisoned = false;
+  HostBarrier *host = nullptr;  // ranks as threads: rendezvous before device barriers
   TeamDev dev() const {
     TeamDev d{};
     for (int q = 0; q < world; ++q) d.base[q] = peer[q];
@@ -486,6 +520,7 @@ struct Stream {
 };
 
 void barrier(Team &T, cudaStream_t s) {
+  if (T.host) T.host->wait();
   k_team_barrier<<<1, 32, 0, s>>>(T.dev(), nullptr);
   SG_CUDA(cudaGetLastError());
 }
@@ -572,8 +607,11 @@ void finish_run(Team &T, Stream &S, RunBufs &rb, double *labels_d, int64_t nv, c
   SG_CUDA(cudaMemcpy(&hh, T.base, sizeof(Hdr), cudaMemcpyDeviceToHost));
   if (hh.err || h.error == SG_ECUDA) {
     T.poisoned = true;
-    throw Error(SG_ECUDA, "peer barrier timed out: a rank did not arrive within 20 s "
-                          "(the team is unusable; create a new one)");
+    throw Error(SG_ECUDA, std::string("peer barrier timed out: a rank did not arrive within 20 s "
+                          "(the team is unusable; create a new one)") +
+                          (T.host ? "; ranks as threads share one GPU's hardware queues: set "
+                                    "CUDA_DEVICE_MAX_CONNECTIONS >= world + 2 before CUDA starts"
+                                  : ""));
   }
   const int64_t rounds = h.round;
   g_launches.fetch_add((int64_t)body_nodes * rounds, std::memory_order_relaxed);
@@ -1002,9 +1040,11 @@ void run_peer_threads(Graph &g, const sg_params &p, int world, const Out &o) {
     SG_CUDA(cudaMemset(T->base, 0, sizeof(Hdr)));
     teams.push_back(std::move(T));
   }
+  HostBarrier hb(world);
   for (auto &T : teams) {
     for (int q = 0; q < world; ++q) T->peer[q] = teams[(size_t)q]->base;
     T->connected = true;
+    T->host = &hb;
   }
   SG_CUDA(cudaDeviceSynchronize());
   std::vector<std::string> err(world);
@@ -1022,12 +1062,16 @@ void run_peer_threads(Graph &g, const sg_params &p, int world, const Out &o) {
         team_run(*teams[(size_t)r], *parts[(size_t)r], p, ro);
       } catch (const Error &e) {
         err[r] = e.what(), code[r] = e.code;
+        hb.fail();
       } catch (const std::exception &e) {
         err[r] = e.what(), code[r] = SG_ECUDA;
+        hb.fail();
       }
     });
   for (auto &t : th) t.join();
   SG_CUDA(cudaDeviceSynchronize());
+  for (int r = 0; r < world; ++r)  // the first real failure (not "a peer rank failed")
+    if (code[r] != SG_OK && err[r] != "a peer rank failed") throw Error(code[r], err[r]);
   for (int r = 0; r < world; ++r)
     if (code[r] != SG_OK) throw Error(code[r], err[r]);
 }

@@ -1,5 +1,13 @@
+import os
 import sys
 from pathlib import Path
+
+# Ranks as threads on one GPU (tests/test_gpu_peer.py) run up to 8 streams whose
+# barrier kernels spin until every rank arrives; with the default 8 hardware
+# queues two ranks' streams can share one and serialise behind a spinning
+# kernel.  Read by the driver when the CUDA context is created (before any test
+# initialises CUDA).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import pytest
 
