@@ -413,12 +413,17 @@ def main():
         return run_reference(a)
     rank, local_rank, world = dist_env()
     import torch
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import paper_1911_09135_b200 as sg
+    from paper_1911_09135_b200 import dist as sgdist
     from paper_1911_09135_b200 import native
+    device = sgdist.init_device() if world > 1 else local_rank
+    torch.cuda.set_device(device)
+    if world > 1:  # plumbing only (IPC handle exchange, max over ranks); gloo when
+        import torch.distributed as dist  # ranks share a GPU (NCCL refuses duplicate GPUs)
+        if native.device_count() >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group("gloo")
 
     g, g_base = make_graph_device(sg, a.app, a.scale, a.uniform)
     dev = g.device()
@@ -426,14 +431,22 @@ def main():
     sched, params = run_params(sg, a.app, a.sched, a.threshold, nv, a.cta_bin == "classic")
     params.reserved = a.pr_block if a.pr_block > 0 else (1 << 31) - 1 if a.pr_block < 0 else 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    nccl_id = None
-    if world > 1:  # edge cut: one partition per rank, NCCL label exchange
-        from paper_1911_09135_b200 import dist as sgdist
-        nccl_id = sgdist.share_nccl_id(torch.distributed)
+    team = part = None
+    if world > 1:
+        # edge cut over NVLink peer memory: this rank keeps only its rows (the
+        # full graph is generated, sliced and dropped), the label exchange is
+        # done by the round's kernels in the peers' HBM (sg_peer.cu)
+        params.devices = world
+        part = sgdist.partition(g if a.app == "sssp" else g_base, a.app, rank, world)
+        host_csr = None if a.no_e2e else dev.download(0, weights=(a.app == "sssp"))
+        del g, g_base, dev
+        native.release_cached()
+        team = sgdist.make_team(torch.distributed, nv)
+        dev = part.device()
 
     def step(d):
         if world > 1:
-            return native.dist_run(d, params, nccl_id, rank, world)
+            return team.run(d, params)
         return d.run(params)
 
     warm_ms = []
@@ -470,18 +483,25 @@ def main():
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
     if not a.no_e2e:
-        off, tgt, w = dev.download(0, weights=(a.app == "sssp"))
+        off, tgt, w = host_csr if world > 1 else dev.download(0, weights=(a.app == "sssp"))
         pin = lambda x: torch.from_numpy(x).pin_memory().numpy() if x is not None else None
         off_p, tgt_p, w_p = pin(off), pin(tgt), pin(w)
         h2d = off_p.nbytes + tgt_p.nbytes + (w_p.nbytes if w_p is not None else 0)
         d2h = 8 * nv + native.ROUND_DTYPE.itemsize * rounds
+        def upload():
+            dg = native.DeviceGraph.from_csr(off_p, tgt_p, w_p)
+            if world == 1:
+                return dg
+            kind = sgdist.PART_KIND[a.app]
+            return native.DevicePartition.of(dg, kind, world, rank)
+
         for _ in range(2):  # warm the device / pinned block caches (steady state)
-            _warm = native.DeviceGraph.from_csr(off_p, tgt_p, w_p).run(params)
+            _warm = step(upload())
         torch.cuda.synchronize()
         e2e_s = []
         for _ in range(max(1, a.steps)):
             t0 = time.perf_counter()
-            dg = native.DeviceGraph.from_csr(off_p, tgt_p, w_p)
+            dg = upload()
             lab_e, log_e, _ = step(dg)
             torch.cuda.synchronize()
             e2e_s.append(time.perf_counter() - t0)
@@ -493,12 +513,18 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * e2e_tot / len(e2e_s), "steps": len(e2e_s),
                "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights), sg_run "
-                       "(original numbering: a fresh graph's first run), labels + round log D2H"}
+                       "(original numbering: a fresh graph's first run), labels + round log D2H"
+                       if world == 1 else
+                       "per step and rank: sg_graph_create of the full CSR (+ int64 weights) "
+                       "from pinned host memory, sg_graph_partition (this rank's rows), "
+                       "sg_team_run, labels + round log D2H; max over ranks"}
         assert np.array_equal(lab_e, labels)
 
     # ---------------- roofline from a profiled run ----------------
-    _, plog, pms, kernels = dev.run(params, profile=True)
-    roofline = roofline_of(a.app, kernels, plog, statistics.median(step_ms), workload)
+    roofline, kernels = None, {}
+    if world == 1:
+        _, plog, pms, kernels = dev.run(params, profile=True)
+        roofline = roofline_of(a.app, kernels, plog, statistics.median(step_ms), workload)
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
@@ -595,6 +621,10 @@ def main():
                                             steps_c, classic=False)
 
     if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            team.close()
+            torch.distributed.destroy_process_group()
         return
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
@@ -609,7 +639,9 @@ def main():
                    "scheduler": sched.describe(), "threshold": a.threshold,
                    "num_vertices": nv, "num_edges": ne, "edges_processed": edges,
                    "rounds": rounds,
-                   "parallelism": f"edge-cut x{world} (NCCL all-reduce min)" if world > 1
+                   "parallelism": f"edge-cut x{world}: per-rank partitions, label exchange by "
+                                  "the round's kernels over NVLink peer memory, device "
+                                  "barrier + quiescence (sg_peer.cu)" if world > 1
                    else "single",
                    "l2": "flushed (512 MB write) before every step",
                    "timing": "sum of per-step CUDA-event durations of sg_run (one graph launch "
@@ -634,6 +666,8 @@ def main():
     }
     print(json.dumps(line), flush=True)
     if world > 1:
+        torch.distributed.barrier()
+        team.close()
         torch.distributed.destroy_process_group()
 
 
