@@ -178,8 +178,16 @@ struct BmMin {
 // ---------------------------------------------------------------- kernels --
 // inspection + TWC small/medium (warp gather); huge / CTA-bin vertices are
 // queued with their snapshot label
+// resident CTAs per SM the TWC kernel is compiled for (the register cap that
+// keeps each operator at the occupancy it was measured best with: bfs 40
+// registers / 6 CTAs, 4-byte labels 48 / 5, 8-byte labels 64 / 4)
 template <class Op>
-__global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
+constexpr int twc_min_blocks() {
+  return std::is_same<Op, BmBfs>::value ? 6 : sizeof(typename Op::L) == 8 ? 4 : 5;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kTB, twc_min_blocks<Op>()) k_bm_twc(PushArgs a, Op op) {
   pdl_wait();
   pdl_trigger();
   using L = typename Op::L;
@@ -193,9 +201,19 @@ __global__ void __launch_bounds__(kTB) k_bm_twc(PushArgs a, Op op) {
   const uint32_t lane = lane_id();
   unsigned long long my_edges = 0, my_large = 0;
   const uint32_t nchunks = (src.n + 31) / 32;
+  // a frontier of at most one chunk per warp: warp w takes chunk w and no
+  // warp touches the shared counter (a small round's chunks then run in
+  // parallel instead of kChunkGrab-deep on a few warps); otherwise dynamic
+  // grabs of kChunkGrab chunks
+  const bool small = nchunks <= grid_warps();
   uint32_t c = 0, c_end = 0;
+  if (small) {
+    c = global_warp();
+    c_end = c < nchunks ? c + 1 : c;
+  }
   for (;;) {
     if (c == c_end) {
+      if (small) break;
       uint32_t g = 0;
       if (lane == 0) g = atomicAdd(&ctl->chunk_head, 1u);
       g = __shfl_sync(kFull, g, 0);
@@ -308,8 +326,9 @@ __global__ void __launch_bounds__(kTB) k_bm_large(PushArgs a, Op op) {
   __shared__ L bsv[kBatch];
   __shared__ uint32_t bhead;
   const uint32_t nb = (n + kBatch - 1) / kBatch;
+  bool first_grab = true;
   for (;;) {
-    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    if (threadIdx.x == 0) bhead = cta_grab(&ctl->large_head, first_grab);
     __syncthreads();
     const uint32_t bidx = bhead;
     if (bidx >= nb) break;
@@ -389,8 +408,9 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
   const long long wstep = 32 * kPV, step = (long long)kTB * kPV;
   const long long woff = (long long)(threadIdx.x >> 5) * wstep;
   const uint32_t lane = threadIdx.x & 31u;
+  bool first_grab = true;
   for (;;) {
-    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    if (threadIdx.x == 0) bhead = cta_grab(&ctl->large_head, first_grab);
     __syncthreads();
     const uint32_t bidx = bhead;
     if (bidx >= nb) break;
@@ -467,8 +487,9 @@ __global__ void __launch_bounds__(kTB) k_bm_large_classic(PushArgs a, Op op) {
   if (!n) return;
   op.begin(ctl->round);
   unsigned long long my_proc = 0;
+  bool first_grab = true;
   for (;;) {
-    if (threadIdx.x == 0) item = atomicAdd(&ctl->large_head, 1u);
+    if (threadIdx.x == 0) item = cta_grab(&ctl->large_head, first_grab);
     __syncthreads();
     const uint32_t idx = item;
     __syncthreads();

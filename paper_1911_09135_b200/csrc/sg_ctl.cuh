@@ -48,6 +48,24 @@ __device__ __forceinline__ int owner_of(const Cuts &k, uint32_t v) {
   return d;
 }
 
+// Dynamic work fetch of the persistent grids: a unit's (warp's / CTA's) first
+// grab is its own index, only later grabs go through the round's shared
+// counter (offset by the number of units).  At a small frontier most of a
+// 740-CTA grid then exits without touching the counter: thousands of warps
+// serialising on one atomic cost ~10-15 us per launch.
+constexpr uint32_t kNoGrab = 0xffffffffu;
+__device__ __forceinline__ uint32_t global_warp() {
+  return (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ uint32_t grid_warps() { return (gridDim.x * blockDim.x) >> 5; }
+__device__ __forceinline__ uint32_t cta_grab(uint32_t *ctr, bool &first) {
+  if (first) {
+    first = false;
+    return blockIdx.x;
+  }
+  return atomicAdd(ctr, 1u) + gridDim.x;
+}
+
 // one record per round, layout == sg_round (include/simtgraph_cuda.h)
 struct RoundStat {
   long long frontier_size, active_edges, huge_count, huge_edges, large_count, large_edges,

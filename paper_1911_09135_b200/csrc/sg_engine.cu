@@ -208,8 +208,10 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
       L.go("init", k_set1<uint32_t>, 1, 1, s, prev, src >> 5, 1u << (src & 31));
     };
     set_round(BmBfs{lab, vis, prev});
-    P.finish = [=](Launcher &L, cudaStream_t s) {
-      L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
+    P.unpermuted = P.inv != nullptr;
+    P.finish = [=, inv = P.inv, out = P.out](Launcher &L, cudaStream_t s) {
+      if (inv) L.go("labels", k_labels_u32_inv, grid_n(nv), 256, s, (const uint32_t *)lab, inv, nv, out);
+      else L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
     };
     return;
   }
@@ -242,8 +244,10 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
     if (cc) set_round(BmMin<0>{lab, nullptr, nullptr, snap, nb});
     else if (!weighted) set_round(BmMin<1>{lab, nullptr, nullptr, snap, nb});
     else set_round(BmMin<2>{lab, g.w32.p, nullptr, snap, nb});
-    P.finish = [=](Launcher &L, cudaStream_t s) {
-      L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
+    P.unpermuted = P.inv != nullptr;
+    P.finish = [=, inv = P.inv, out = P.out](Launcher &L, cudaStream_t s) {
+      if (inv) L.go("labels", k_labels_u32_inv, grid_n(nv), 256, s, (const uint32_t *)lab, inv, nv, out);
+      else L.go("labels", k_labels_u32, grid_n(nv), 256, s, lab, nv, labels_d);
     };
   } else {
     using U = unsigned long long;
@@ -513,6 +517,10 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
   rb.want_cta = cta != nullptr;
   Program P;
   double *labels_d = P.buf<double>(g.nv);
+  // the run's output -- float64 labels in the reference's numbering -- is
+  // produced on the device inside the timed region; only the D2H is outside
+  double *lab_out_d = lay.inv ? P.buf<double>(g.nv) : labels_d;
+  P.inv = lay.inv, P.out = lab_out_d;
   switch (p.app) {
     case SG_APP_BFS:
     case SG_APP_SSSP:
@@ -560,9 +568,6 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
       SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     }
     Launcher &L = prof ? *prof : plain;
-    // the run's output -- float64 labels in the reference's numbering -- is
-    // produced on the device inside the timed region; only the D2H is outside
-    double *lab_out_d = lay.inv ? P.buf<double>(g.nv) : labels_d;
     SG_CUDA(cudaEventRecord(e0, s));
     if (rb.cta.p)
       SG_CUDA(cudaMemsetAsync(rb.cta.p, 0, rb.cta.bytes(), s));
@@ -583,7 +588,7 @@ void run_app_on(Graph &g, const sg_params &p, double *labels_out, sg_round *roun
       }
     }
     P.finish(L, s);
-    if (lay.inv) L.go("labels", k_unpermute, grid_n(g.nv), 256, s, (const double *)labels_d, lay.inv,
+    if (lay.inv && !P.unpermuted) L.go("labels", k_unpermute, grid_n(g.nv), 256, s, (const double *)labels_d, lay.inv,
                       g.nv, lab_out_d);
     SG_CUDA(cudaEventRecord(e1, s));
     SG_CUDA(cudaEventSynchronize(e1));

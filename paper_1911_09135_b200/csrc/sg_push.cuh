@@ -249,9 +249,19 @@ __global__ void __launch_bounds__(kTB) k_push_twc(PushArgs a, Op op) {
   unsigned long long my_edges = 0, my_large = 0;
   // dynamic fetch: a warp grabs kChunkGrab chunks of 32 frontier items at a time
   const uint32_t nchunks = (src.n + 31) / 32;
+  // a frontier of at most one chunk per warp: warp w takes chunk w and no
+  // warp touches the shared counter (a small round's chunks then run in
+  // parallel instead of kChunkGrab-deep on a few warps); otherwise dynamic
+  // grabs of kChunkGrab chunks
+  const bool small = nchunks <= grid_warps();
   uint32_t c = 0, c_end = 0;
+  if (small) {
+    c = global_warp();
+    c_end = c < nchunks ? c + 1 : c;
+  }
   for (;;) {
     if (c == c_end) {
+      if (small) break;
       uint32_t g = 0;
       if (lane == 0) g = atomicAdd(&ctl->chunk_head, 1u);
       g = __shfl_sync(kFull, g, 0);
@@ -337,8 +347,9 @@ __global__ void __launch_bounds__(kTB) k_push_large(PushArgs a, Op op) {
   // batch b takes queue entries b, b+NB, b+2NB, ... so that batches mix the
   // (degree-correlated) queue order and carry similar edge totals
   const uint32_t nb = (n + kBatch - 1) / kBatch;
+  bool first_grab = true;
   for (;;) {
-    if (threadIdx.x == 0) bhead = atomicAdd(&ctl->large_head, 1u);
+    if (threadIdx.x == 0) bhead = cta_grab(&ctl->large_head, first_grab);
     __syncthreads();
     const uint32_t bidx = bhead;
     if (bidx >= nb) break;

@@ -148,6 +148,17 @@ __global__ void k_labels_u32(const uint32_t *lab, int64_t n, double *out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
     out[i] = lab[i] == kInf32 ? INFINITY : (double)lab[i];
 }
+// u32 labels of the relabeled store -> float64 in the reference's numbering,
+// one pass: out[v] = lab[inv[v]] (inv is mostly monotone: the cold vertices
+// keep their relative order, so the gather is nearly sequential)
+__global__ void k_labels_u32_inv(const uint32_t *__restrict__ lab, const uint32_t *__restrict__ inv,
+                                 int64_t n, double *__restrict__ out) {
+  int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    const uint32_t x = lab[inv[i]];
+    out[i] = x == kInf32 ? INFINITY : (double)x;
+  }
+}
 __global__ void k_iota_pairs(uint32_t *p, int64_t n) {
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
@@ -557,6 +568,11 @@ struct Program {
   std::function<void(Launcher &, cudaStream_t)> init;  // device state init (timed)
   std::function<void(RoundCtx &)> round;              // one BSP round
   std::function<void(Launcher &, cudaStream_t)> finish;  // labels -> out (untimed)
+  // relabeled store: a finish that maps the labels back to the reference's
+  // numbering itself (gathering through `inv` into `out`) sets `unpermuted`
+  const uint32_t *inv = nullptr;
+  double *out = nullptr;
+  bool unpermuted = false;
   std::vector<std::shared_ptr<void>> keep;
   template <class T>
   T *buf(int64_t n) {
