@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--app", default="sssp", choices=["bfs", "sssp", "cc", "pr", "kcore"])
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--uniform", action="store_true", help="uniform RMAT probabilities")
+    ap.add_argument("--probs", default=None,
+                    help="RMAT probabilities a,b,c,d (the reference's --rmat-probs), e.g. 0.8,0.1,0.05,0.05")
     ap.add_argument("--sched", default="alb", choices=["alb", "twc"])
     ap.add_argument("--threshold", type=int, default=DEFAULT_THRESHOLD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -425,7 +427,8 @@ def main():
         else:
             dist.init_process_group("gloo")
 
-    g, g_base = make_graph_device(sg, a.app, a.scale, a.uniform)
+    probs = tuple(float(x) for x in a.probs.split(",")) if a.probs else None
+    g, g_base = make_graph_device(sg, a.app, a.scale, a.uniform, probs)
     dev = g.device()
     nv, ne, _ = dev.info()
     sched, params = run_params(sg, a.app, a.sched, a.threshold, nv, a.cta_bin == "classic")
@@ -455,7 +458,7 @@ def main():
         warm_ms.append(ms)
     edges = int(log["active_edges"].sum())
     rounds = len(log)
-    workload = workload_name(a.app, a.scale, (0.25,) * 4 if a.uniform else SKEWED)
+    workload = workload_name(a.app, a.scale, probs or ((0.25,) * 4 if a.uniform else SKEWED))
 
     # ---------------- timed region (device-resident inputs) ----------------
     if world > 1:

@@ -23,6 +23,7 @@
 //     libnccl is dlopen'ed (preferring the copy torch already loaded), so the
 //     single-GPU library has no NCCL dependency.
 // bfs runs as unit-weight relaxation (OpPair<1>): identical labels and rounds.
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -667,17 +668,57 @@ namespace {
 // communicator (its root listener serves one init), and init costs far more
 // than a BSP run.  Deliberately leaked at exit (destroying communicators after
 // the CUDA runtime has torn down is unsafe); sg_nccl_release frees them.
+// Entries are created OUTSIDE the map lock (ncclCommInitRank blocks until
+// every rank of the id joined, and ranks driven from threads of one process
+// must not serialise on it): a per-key slot with its own once-flag.  The key
+// holds the device, so one id used on two devices gives two communicators.
+struct CommSlot {
+  std::once_flag once;
+  std::unique_ptr<NcclComm> comm;
+  std::exception_ptr err;
+};
 std::mutex g_comm_mu;
-std::map<std::string, std::unique_ptr<NcclComm>> *g_comms = new std::map<std::string, std::unique_ptr<NcclComm>>();
+std::map<std::string, std::shared_ptr<CommSlot>> *g_comms =
+    new std::map<std::string, std::shared_ptr<CommSlot>>();
 
-NcclComm &cached_comm(const uint8_t id[128], int rank, int world) {
+void evict_comm(const std::string &key);
+
+std::string comm_key(const uint8_t id[128], int rank, int world) {
+  int dev = 0;
+  SG_CUDA(cudaGetDevice(&dev));
   std::string key(reinterpret_cast<const char *>(id), 128);
-  key += ":" + std::to_string(rank) + "/" + std::to_string(world);
+  return key + ":" + std::to_string(rank) + "/" + std::to_string(world) + "@" + std::to_string(dev);
+}
+
+NcclComm &cached_comm(const std::string &key, const uint8_t id[128], int rank, int world) {
+  std::shared_ptr<CommSlot> slot;
+  {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    auto &p = (*g_comms)[key];
+    if (!p) p = std::make_shared<CommSlot>();
+    slot = p;
+  }
+  std::call_once(slot->once, [&] {
+    try {
+      slot->comm = std::make_unique<NcclComm>(id, rank, world);
+    } catch (...) {
+      slot->err = std::current_exception();
+    }
+  });
+  if (slot->err) {
+    evict_comm(key);
+    std::rethrow_exception(slot->err);
+  }
+  return *slot->comm;
+}
+
+// a run that threw mid-collective leaves its communicator out of step with
+// the peers: drop it so the next run with that id fails cleanly at init
+void evict_comm(const std::string &key) {
+  std::shared_ptr<CommSlot> old;
   std::lock_guard<std::mutex> lk(g_comm_mu);
   auto it = g_comms->find(key);
-  if (it == g_comms->end())
-    it = g_comms->emplace(key, std::make_unique<NcclComm>(id, rank, world)).first;
-  return *it->second;
+  if (it != g_comms->end()) old = it->second, g_comms->erase(it);
 }
 }  // namespace
 }  // namespace sg
@@ -702,8 +743,14 @@ int sg_dist_run(sg_graph *gh, const sg_params *p, const uint8_t nccl_id[128], in
   return sg::guard([&] {
     if (world < 1 || world > sg::kMaxParts || rank < 0 || rank >= world)
       throw Error(SG_ECONFIG, "bad rank / world size");
-    sg::NcclComm &comm = sg::cached_comm(nccl_id, rank, world);
-    sg::dist_run_rank(*gh->g, *p, comm, labels_out, rounds_out, rounds_cap, nrounds, ms_out);
+    const std::string key = sg::comm_key(nccl_id, rank, world);
+    sg::NcclComm &comm = sg::cached_comm(key, nccl_id, rank, world);
+    try {
+      sg::dist_run_rank(*gh->g, *p, comm, labels_out, rounds_out, rounds_cap, nrounds, ms_out);
+    } catch (...) {
+      sg::evict_comm(key);
+      throw;
+    }
   });
 }
 

@@ -32,9 +32,10 @@
 //   * pr: owners fold their CSC rows with the exact-order pull (sg_prx.cuh)
 //     and store the new aux of each row into its mirror holders; max |delta|
 //     and the counters go through the slots, the stop test is the reference's;
-//   * kcore: owners count, kill (stores alive = 0 into the mirror holders),
-//     barrier, mark alive neighbours of the dying (remote stores of the round
-//     stamp into the owner's mark array), barrier, owners collect their marks.
+//   * kcore: owners count, kill, mark the neighbours of the dying (remote
+//     stores of the round stamp into the owners' mark arrays), barrier, then
+//     store the deaths into the mirror holders and collect their stamped rows
+//     that are still alive.
 //
 // The whole BSP loop of a rank is ONE CUDA-graph launch (WHILE node): no host
 // round trip and no collective library inside the loop.  The barrier spins
@@ -365,9 +366,12 @@ __global__ void k_px_kill(TeamDev t, Layout lay, const Ctl *ctl, const uint32_t 
   __threadfence_system();
 }
 
-// kcore mark phase over the peers: an alive neighbour of a dying vertex gets
-// the round's stamp in its OWNER's mark array (a remote store when another
-// rank owns it); owners collect their stamped rows after the barrier
+// kcore mark phase over the peers: a neighbour of a dying vertex gets the
+// round's stamp in its OWNER's mark array (a remote store when another rank
+// owns it); after the barrier owners collect their stamped rows that are
+// still alive (apps.py:226-231: alive = neighbours[values > 0] after the kill)
+// -- the owner's alive flag is authoritative, so the mark phase needs no
+// peer's deaths and the count phase never sees a death of its own round
 struct OpMarkPeer {
   using L = uint32_t;
   static constexpr bool kCarry = false;
@@ -389,16 +393,31 @@ struct OpMarkPeer {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       act[u] = false;
-      if (!ok[u] || !alive[dst[u]]) continue;
+      if (!ok[u]) continue;
       const uint32_t v = dst[u];
       if ((long long)v >= lo && (long long)v < hi) {
-        if (mark[v] != stamp) act[u] = atomicExch(mark + v, stamp) != stamp;
-      } else {
+        if (alive[v] && mark[v] != stamp) act[u] = atomicExch(mark + v, stamp) != stamp;
+      } else {  // the owner knows whether v is alive: it filters at collection
         at<uint32_t>(t, owner_of(cuts, v), o_mark)[v] = stamp;
       }
     }
   }
 };
+
+// kcore: owned rows stamped this round and still alive -> next local frontier
+__global__ void k_px_kc_compact(const Ctl *ctl, const uint32_t *mark, const uint8_t *alive,
+                                uint32_t lo, uint32_t hi, uint32_t *q0, uint32_t *q1,
+                                uint32_t *nsize) {
+  if (ctl->done) return;
+  const uint32_t round = ctl->round, stamp = round + 1;
+  uint32_t *q = (round & 1) ? q0 : q1;
+  const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < hi - lo; b += st) {
+    const uint64_t i = b + threadIdx.x;
+    const bool m = i < hi - lo && mark[lo + i] == stamp && alive[lo + i];
+    warp_append(m, lo + (uint32_t)i, q, nsize);
+  }
+}
 
 // ---------------------------------------------------------- label gather --
 // every rank's owned block -> this rank's full output (remote loads)
@@ -868,16 +887,17 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
     L.go("kcore_kill", k_kcore_kill, grid_n(nv), 256, s, a, alive);
     L.go("dist", k_dist_kc_collect, 1, 32, s, a, acc.p);
     L.go("kcore_stats", k_kcore_reset, 1, 1, s, a);
-    L.go("peer_kill", k_px_kill, grid_n(hi - lo), 256, s, td, T.lay, (const Ctl *)ctl,
-         (const uint32_t *)rb.dying.p, (int64_t)lo, (const uint32_t *)mi.mask.p);
-    L.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
     L.go("mark_twc", k_push_twc<OpMarkPeer>, occupancy_grid(k_push_twc<OpMarkPeer>, kTB), kTB, s,
          w, mop);
     L.go("mark_large", k_push_large<OpMarkPeer>, occupancy_grid(k_push_large<OpMarkPeer>, kTB),
          kTB, s, w, mop);
+    // every rank has counted (reads of mirrors' alive flags) and marked
     L.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    L.go("dist", k_dist_kc_compact, grid_n(hi - lo), 256, s, (const Ctl *)ctl,
-         (const uint32_t *)mark, lo, hi, rb.q0.p, rb.q1.p, &ctl->nsize);
+    // the round's deaths -> the mirror holders (read by the next round's count)
+    L.go("peer_kill", k_px_kill, grid_n(hi - lo), 256, s, td, T.lay, (const Ctl *)ctl,
+         (const uint32_t *)rb.dying.p, (int64_t)lo, (const uint32_t *)mi.mask.p);
+    L.go("dist", k_px_kc_compact, grid_n(hi - lo), 256, s, (const Ctl *)ctl,
+         (const uint32_t *)mark, (const uint8_t *)alive, lo, hi, rb.q0.p, rb.q1.p, &ctl->nsize);
     L.go("dist", k_dist_kc_next, 1, 32, s, (const Ctl *)ctl, acc.p);
     L.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)ctl, (const long long *)acc.p,
          kDistN);

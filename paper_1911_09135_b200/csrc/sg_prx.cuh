@@ -262,12 +262,35 @@ __device__ __forceinline__ void split_walk(const PrxArgs &a, PrFold &op, uint32_
       g = __ldcg(a.ck_guess + j);
     }
     const uint32_t m = min(32u, c1 - base);
-    for (uint32_t tt = 0; tt < m; ++tt) {
+    uint32_t tt = 0;
+    while (tt < m) {
+      const int es = s > 0.0 ? dexp(s) : kNoGuess;
+      // bulk: the longest run of chunks tt.. whose sums were formed on the
+      // current binade's grid (no tie, guess == es) -- inside one binade the
+      // sequential sum is the integer sum N0 + T_tt + T_tt+1 + ..., so the
+      // run is one warp prefix sum instead of one dependent step per chunk
+      const bool mine = lane >= tt && lane < m;
+      const bool ok = mine && s > 0.0 && exp_ok(es) && (meta & 1u) && !(meta & 2u) && g == es;
+      const uint32_t bad = __ballot_sync(kFull, mine && !ok);
+      uint32_t end = bad ? (uint32_t)(__ffs(bad) - 1) : m;
+      if (end > tt) {
+        const long long N0 = (long long)(s * pow2(52 - es));
+        const long long pre = warp_incl_scan(lane >= tt && lane < end ? T : 0ll);
+        // ... and stays inside the binade (the T are >= 0: prefixes only grow)
+        const uint32_t over = __ballot_sync(kFull, lane >= tt && lane < end && N0 + pre >= kTwo53);
+        if (over) end = (uint32_t)(__ffs(over) - 1);
+        if (end > tt) {
+          if (lane >= tt && lane < end) a.ck_guess[j] = es;  // the next pass guesses this binade
+          s = (double)(N0 + __shfl_sync(kFull, pre, end - 1)) * pow2(es - 52);
+          tt = end;
+          continue;
+        }
+      }
+      // chunk tt alone: its own sum if it fits, else redone exactly from s
       const long long Tt = __shfl_sync(kFull, T, tt);
       const uint32_t mt = __shfl_sync(kFull, meta, tt);
       const int gt = __shfl_sync(kFull, g, tt);
-      const int es = s > 0.0 ? dexp(s) : kNoGuess;
-      if (lane == tt) a.ck_guess[j] = es;  // the next pass guesses this binade
+      if (lane == tt) a.ck_guess[j] = es;
       bool done = false;
       if (s > 0.0 && (mt & 1u) && !(mt & 2u) && es == gt && exp_ok(es)) {
         const long long N0 = (long long)(s * pow2(52 - es));
@@ -284,6 +307,7 @@ __device__ __forceinline__ void split_walk(const PrxArgs &a, PrFold &op, uint32_
         gather_val(op.aux, src, x);
         s = ex_step(s, x);
       }
+      ++tt;
     }
   }
   if (lane == 0) row_end(a, op, v, f, s);

@@ -79,6 +79,14 @@ def max_over_ranks(dist, value: float) -> float:
     return float(t.item())
 
 
+def release():
+    """Free the NCCL communicators the nccl transport cached (sg_nccl_release);
+    call before destroy_process_group.  A communicator is reused by every run
+    with the same id, so a caller that passes a fresh id per run should
+    release after each."""
+    native.nccl_release()
+
+
 def run_app(graph, app_name: str, scheduler: Scheduler = Scheduler("alb"),
             config: KernelConfig = KernelConfig(), *, rank: int, world: int, nccl_id: bytes,
             max_rounds=None, **params) -> RunResult:

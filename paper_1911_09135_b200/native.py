@@ -346,6 +346,12 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def nccl_release():
+    """Destroy the NCCL communicators sg_dist_run cached (one per id / rank /
+    world / device); call before tearing down the process group."""
+    load().sg_nccl_release()
+
+
 def dist_run(dev: DeviceGraph, params: Params, nccl_id: bytes, rank: int, world: int,
              rounds_cap=1 << 16):
     """One edge-cut partition per rank over NCCL (sg_dist_run); every rank gets

@@ -239,6 +239,7 @@ def test_nccl_edge_cut_single_rank(sg, golden, app):
     params = sg.engine.device_params(sg.apps.make_app(app), sg.Scheduler("alb"),
                                       sg.KernelConfig(), 1, 10 * g.num_vertices + 256)
     labels, log, ms = native.dist_run(g.device(), params, native.nccl_unique_id(), 0, 1)
+    native.nccl_release()  # a fresh id per call: free its communicator
     if app == "pr":
         ref = sg.run_app(g, "pr")
         assert np.max(np.abs(labels - ref.labels)) <= PR_ATOL
