@@ -216,8 +216,10 @@ void run_dist_push(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds
                               cudaMemcpyHostToDevice, s));
       Lc.go("dist", k_dp_pack<L>, grid_n(nw), 256, s, (const uint32_t *)nb.p, (const L *)lab.p, nv,
             cuts, R, cursor.p, sids.p, svals.p);
+      cm.group_begin();  // ids and labels in ONE grouped NCCL launch
       cm.alltoallv(sids.p, sc.data(), sd.data(), rids.p, rc.data(), rd.data(), CType::U32, s);
       cm.alltoallv(svals.p, sc.data(), sd.data(), rvals.p, rc.data(), rd.data(), LT, s);
+      cm.group_end();
       if (roff)
         Lc.go("dist", k_dp_apply<L>, grid_n((int64_t)roff), 256, s, (const uint32_t *)rids.p,
               (const L *)rvals.p, (int64_t)roff, lab.p);
@@ -243,8 +245,10 @@ void run_dist_push(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds
         sc[q] = q == R ? 0 : nch, sd[q] = 0;
         rc[q] = q == R ? 0 : (size_t)per[q], rd[q] = roff, roff += rc[q];
       }
+      cm.group_begin();
       cm.alltoallv(uids.p, sc.data(), sd.data(), rids.p, rc.data(), rd.data(), CType::U32, s);
       cm.alltoallv(uvals.p, sc.data(), sd.data(), rvals.p, rc.data(), rd.data(), LT, s);
+      cm.group_end();
       if (roff)
         Lc.go("dist", k_dp_apply<L>, grid_n((int64_t)roff), 256, s, (const uint32_t *)rids.p,
               (const L *)rvals.p, (int64_t)roff, lab.p);

@@ -14,6 +14,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "sg_graph.cuh"
 
@@ -472,6 +473,7 @@ int64_t Graph::relabel_bytes(bool in_first) const {
   b += nv * 4 * 5 + nv * 8;                         // build temporaries
   if (weighted) b += ne * 4;
   if (in_first) b += (nv + 1) * 8 + ne * 4;         // the permuted CSC
+  else b += ne * 8;                                 // row sort: keys + weights out
   return b;
 }
 
@@ -493,6 +495,78 @@ void Graph::release_views() {
   cov_k_ = -1;
   top1_ = -1.0;
   dev_release_cached();
+}
+
+// batch boundaries of a row-sorted pass: rows [cut[k], cut[k+1]) hold about
+// ne / nb edges (CUB's segmented sort counts items in int)
+__global__ void k_row_batches(const int64_t *off, int64_t nv, int nb, int64_t *cut) {
+  if (threadIdx.x || blockIdx.x) return;
+  const int64_t E = off[nv];
+  cut[0] = 0;
+  for (int k = 1; k < nb; ++k) {
+    const int64_t target = E / nb * k;
+    int64_t lo = 0, hi = nv;  // first row r with off[r] >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    cut[k] = lo > cut[k - 1] ? lo : cut[k - 1];
+  }
+  cut[nb] = nv;
+}
+__global__ void k_rebase(const int64_t *off, int64_t n, int64_t base, int *out) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    out[i] = (int)(off[i] - base);
+}
+
+// Sort every row of a push layout by target id (weights carried along).  The
+// min-relaxation apps are indifferent to the order of a row's edges (BSP: the
+// round's result is the min over all of them), and ascending targets let the
+// lanes of one gather instruction share 32-byte label sectors where a row is
+// dense -- in the relabeled store's hot set, where most edges of a skewed
+// graph point.  Only the relabeled copy is sorted: the graph's own CSR keeps
+// the caller's order (downloads, pr's summation order).
+void sort_rows(View &v, DBuf<uint32_t> *w32) {
+  if (v.ne <= 1 || v.nv == 0) return;
+  const int64_t kMaxItems = (int64_t)1 << 30;
+  const int nb = (int)((v.ne + kMaxItems - 1) / kMaxItems) + (v.ne > kMaxItems ? 1 : 0);
+  DBuf<int64_t> cut(nb + 1);
+  SG_LAUNCH(k_row_batches, 1, 1, 0, 0, v.off.p, v.nv, nb, cut.p);
+  std::vector<int64_t> hc(nb + 1);
+  SG_CUDA(cudaMemcpy(hc.data(), cut.p, sizeof(int64_t) * (nb + 1), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> ho(nb + 1);
+  for (int k = 0; k <= nb; ++k)
+    SG_CUDA(cudaMemcpy(&ho[k], v.off.p + hc[k], sizeof(int64_t), cudaMemcpyDeviceToHost));
+  DBuf<uint32_t> kout(v.ne), vout(w32 ? v.ne : 0);
+  for (int k = 0; k < nb; ++k) {
+    const int64_t r0 = hc[k], r1 = hc[k + 1], e0 = ho[k], n = ho[k + 1] - ho[k];
+    if (r1 <= r0 || n <= 0) continue;
+    if (n > 0x7fffffffLL) throw Error(SG_ERANGE, "row batch too large to sort");
+    DBuf<int> ro(r1 - r0 + 1);
+    SG_LAUNCH(k_rebase, grid_for(r1 - r0 + 1), 256, 0, 0, v.off.p + r0, r1 - r0 + 1, e0, ro.p);
+    size_t tb = 0;
+    if (w32)
+      SG_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, v.col.p + e0, kout.p + e0,
+                                                  w32->p + e0, vout.p + e0, (int)n, (int)(r1 - r0),
+                                                  ro.p, ro.p + 1));
+    else
+      SG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, v.col.p + e0, kout.p + e0, (int)n,
+                                                 (int)(r1 - r0), ro.p, ro.p + 1));
+    DBuf<char> t(std::max<size_t>(tb, 1));
+    if (w32)
+      SG_CUDA(cub::DeviceSegmentedSort::SortPairs(t.p, tb, v.col.p + e0, kout.p + e0,
+                                                  w32->p + e0, vout.p + e0, (int)n, (int)(r1 - r0),
+                                                  ro.p, ro.p + 1));
+    else
+      SG_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tb, v.col.p + e0, kout.p + e0, (int)n,
+                                                 (int)(r1 - r0), ro.p, ro.p + 1));
+    g_launches.fetch_add(1);
+    SG_CUDA(cudaDeviceSynchronize());
+  }
+  v.col = std::move(kout);
+  if (w32) *w32 = std::move(vout);
 }
 
 Relabel &Graph::hot(int64_t K, bool in_first) {
@@ -588,6 +662,13 @@ Relabel &Graph::hot(int64_t K, bool in_first) {
     SG_LAUNCH(k_perm_rows, grid_for(nv * 32), 256, 0, 0, csr.off.p, csr.col.p, w64.p, w32.p,
               R->perm.p, R->inv.p, h->csr.off.p, nv, nbig, K, spread, h->csr.col.p, nw64, nw32);
     SG_CUDA(cudaDeviceSynchronize());
+    static const bool sort_env = [] {
+      const char *x = std::getenv("SG_HOT_SORT");
+      return x ? std::atoi(x) != 0 : true;
+    }();
+    // push layout only (pr's in-edge order is its summation order); the
+    // int64-weight path is rare and keeps its order
+    if (sort_env && !in_first && !want64) sort_rows(h->csr, nw32 ? &h->w32 : nullptr);
   } else {
     SG_CUDA(cudaMemset(h->csr.off.p, 0, sizeof(int64_t)));
     if (weighted) h->weighted = true, h->w64.alloc(1);

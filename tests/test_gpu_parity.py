@@ -518,3 +518,19 @@ def test_nccl_communicator_reused_across_runs(sg, golden):
     native.load().sg_nccl_release()
     labels, log, _ = native.dist_run(g.device(), p, native.nccl_unique_id(), 0, 1)
     assert sg.engine.labels_sha256(labels) == info["labels_sha256"]
+
+
+def test_long_path_round_log_not_truncated(sg):
+    """A BFS / SSSP on a 70,000-vertex path runs 70,000 rounds -- more than the
+    65,536-record log a run fetches first: the run is repeated with a log for
+    all of it (runs are deterministic), never truncated."""
+    n = 70_000
+    off = np.arange(n + 1, dtype=np.int64)
+    off[-1] = n - 1
+    tgt = np.arange(1, n, dtype=np.int32)
+    g = sg.Graph(off, tgt)
+    res = sg.run_app(g, "bfs", sg.Scheduler("alb"))
+    assert res.rounds == n
+    assert np.array_equal(res.labels, np.arange(n, dtype=np.float64))
+    assert [r.frontier_size for r in res.records[:3]] == [1, 1, 1]
+    assert sg.report(res)["totals"]["edges_processed"] == n - 1
