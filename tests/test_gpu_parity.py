@@ -534,3 +534,20 @@ def test_long_path_round_log_not_truncated(sg):
     assert np.array_equal(res.labels, np.arange(n, dtype=np.float64))
     assert [r.frontier_size for r in res.records[:3]] == [1, 1, 1]
     assert sg.report(res)["totals"]["edges_processed"] == n - 1
+
+
+@pytest.mark.parametrize("app", ["sssp", "pr", "kcore"])
+def test_cli_compare_and_sweep(sg, tmp_path, app):
+    """The reference CLI's compare / sweep-threshold (cli.py:207-290) over the
+    device engine: every scheduler and threshold gives identical labels,
+    reports and CSV tables are written."""
+    from paper_1911_09135_b200 import cli
+    base = ["--format", "rmat", "--scale", "12", "--app", app, "--weights", "64",
+            "--out-dir", str(tmp_path)]
+    assert cli.main(["compare", *base, "--schedulers", "twc,alb,alb-blocked,lb,vertex,edge"]) == 0
+    rows = (tmp_path / f"{app}_compare.csv").read_text().splitlines()
+    assert len(rows) == 7 and rows[0].startswith("scheduler,rounds,edges")
+    assert cli.main(["sweep-threshold", *base, "--thresholds", "1,256,auto,inf"]) == 0
+    assert len((tmp_path / f"{app}_threshold_sweep.csv").read_text().splitlines()) == 5
+    assert cli.main(["run", *base, "--scheduler", "alb"]) == 0
+    assert list(tmp_path.glob(f"{app}_alb-cyclic.summary.json"))

@@ -204,3 +204,23 @@ def test_edge_cut_bounds_match_oracle():
 def test_convergence_error_carries_log():
     e = ConvergenceError("x", metrics_log=[1, 2])
     assert e.metrics_log == [1, 2] and isinstance(e, SimtGraphError)
+
+
+def test_cli_parsing_and_scheduler_tokens():
+    """CLI (reference cli.py:173-290 commands): scheduler tokens, thresholds,
+    usage errors -> exit code 2 without touching the device."""
+    from paper_1911_09135_b200 import cli
+    from paper_1911_09135_b200.errors import ConfigError
+    s = cli.scheduler_of("alb-blocked", None, "4096")
+    assert (s.kind, s.distribution, s.threshold) == ("alb", "blocked", 4096)
+    assert cli.scheduler_of("alb", None, "inf").threshold == cli.INT64_MAX
+    assert cli.scheduler_of("lb", "cyclic", "auto").describe() == "lb-cyclic"
+    with pytest.raises(ConfigError):
+        cli.scheduler_of("alb-diagonal")
+    with pytest.raises(ConfigError):
+        cli._threshold("many")
+    assert cli.main(["compare", "--app", "nope"]) == 2
+    assert cli.main(["sweep-threshold", "--thresholds", ""]) == 2  # empty list: ConfigError
+    a = cli.parser().parse_args(["compare", "--format", "rmat", "--scale", "10",
+                                 "--schedulers", "twc,alb,lb"])
+    assert a.func is cli.cmd_compare and a.schedulers == "twc,alb,lb"
