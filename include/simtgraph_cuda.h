@@ -204,6 +204,11 @@ int sg_dist_run_threads(sg_graph *g, const sg_params *p, int32_t world, double *
  * Only the block's edges are stored, so g can be destroyed afterwards.
  * sg_graph_part_info: kind / rank / world, cuts_out[world + 1], edges of the
  * full view.  A partition is run only through sg_team_run.
+ * kind may carry SG_PART_RELABEL / SG_PART_NO_RELABEL: the block-local
+ * hot-vertex relabeling (every block renumbered onto itself by descending
+ * degree, rows sorted -- the kernel layout of the single-device relabeled
+ * store, under the reference's cuts; labels come back in the original
+ * numbering).  Neither: relabel skewed graphs of >= 2^20 vertices.
  *
  * sg_team_create allocates this rank's symmetric region for nv vertices and
  * exports it (handle_out: 64-byte CUDA IPC handle); after exchanging the
@@ -216,6 +221,8 @@ int sg_dist_run_threads(sg_graph *g, const sg_params *p, int32_t world, double *
  * the team size.  labels_out gets the merged labels on every rank, rounds_out
  * the global round log (comm_sent / comm_broadcast as engine.py:105-109,
  * 232-234). */
+#define SG_PART_RELABEL 0x100
+#define SG_PART_NO_RELABEL 0x200
 int sg_graph_partition(sg_graph *g, int32_t kind, int32_t world, int32_t rank, sg_graph **out);
 int sg_graph_part_info(sg_graph *g, int32_t *kind, int32_t *rank, int32_t *world,
                        int64_t *cuts_out, int64_t *full_ne);

@@ -87,6 +87,12 @@ struct Graph {
     int64_t lo = 0, hi = 0;
     int64_t full_ne = 0;          // edges of the full view
     std::shared_ptr<void> mirrors;  // the peer transport's mirror masks (sg_peer.cu)
+    // block-local hot-vertex relabeling (sg_peer.cu): every block [c[k], c[k+1])
+    // is renumbered onto itself in descending total degree, so the cuts,
+    // owners, mirror sets and comm counters are the reference's; perm: new ->
+    // old id, inv: old -> new (all V vertices, every rank holds both)
+    bool relabeled = false;
+    DBuf<uint32_t> perm, inv;
   } part;
   bool is_part() const { return part.kind >= 0; }
   bool weighted = false;
@@ -152,6 +158,8 @@ struct Relabel {
 };
 
 // builders (sg_graph.cu)
+// sort every row of a push layout by target id, u32 weights carried (sg_graph.cu)
+void sort_rows(View &v, DBuf<uint32_t> *w32);
 void build_csr_from_pairs(View &v, int64_t nv, uint32_t *src, uint32_t *dst, int64_t ne,
                           int key_bits);
 void build_transpose(View &out, const View &in);

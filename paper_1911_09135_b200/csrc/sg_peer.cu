@@ -51,6 +51,9 @@
 #include <string>
 #include <thread>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "sg_distk.cuh"
 #include "sg_prx.cuh"
 
@@ -154,6 +157,13 @@ __global__ void k_team_barrier(TeamDev t, Ctl *ctl) {
 __global__ void k_loop_guard(const Ctl *ctl, Loop lp) {
   if (threadIdx.x || !lp.use_cond) return;
   if (ctl->done) cudaGraphSetConditional(lp.cond, 0u);
+}
+
+template <class L>
+__global__ void k_copy_as(const uint32_t *src, int64_t n, L *dst) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    dst[i] = (L)src[i];
 }
 
 // bits of word w that are vertices in [lo, hi)
@@ -421,12 +431,16 @@ __global__ void k_px_kc_compact(const Ctl *ctl, const uint32_t *mark, const uint
 
 // ---------------------------------------------------------- label gather --
 // every rank's owned block -> this rank's full output (remote loads)
+// (a relabeled partition: out[v] = the owner's value of inv[v]; the owner of
+// v and of inv[v] is the same rank, the relabeling is block-local)
 template <class T, class Conv>
-__global__ void k_px_gather(TeamDev t, size_t off, Cuts cuts, int64_t nv, double *out, Conv cv) {
+__global__ void k_px_gather(TeamDev t, size_t off, Cuts cuts, int64_t nv, const uint32_t *inv,
+                            double *out, Conv cv) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st) {
     const int o = owner_of(cuts, (uint32_t)v);
-    out[v] = cv(*(const volatile T *)(at<T>(t, o, off) + v));
+    const int64_t x = inv ? (int64_t)inv[v] : v;
+    out[v] = cv(*(const volatile T *)(at<T>(t, o, off) + x));
   }
 }
 struct ConvU32 {
@@ -660,6 +674,7 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   const View &v = part_view(g);
   const int64_t nv = v.nv;
   const Cuts cuts = part_cuts(g);
+  const uint32_t *inv = g.part.relabeled ? g.part.inv.p : nullptr;
   const int R = T.rank;
   const uint32_t lo = (uint32_t)cuts.c[R], hi = (uint32_t)cuts.c[R + 1];
   Stream S;
@@ -680,7 +695,13 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   const bool weighted = p.app == SG_APP_SSSP && g.weighted;
   const Op op{lab, KIND == 2 ? g.w32.p : nullptr, KIND == 3 && weighted ? g.w64.p : nullptr,
               snap.p, nb};
-  const bool owns_src = !cc && p.source >= lo && p.source < hi;
+  int64_t src = p.source;  // in the partition's numbering
+  if (!cc && inv) {
+    uint32_t x = 0;
+    SG_CUDA(cudaMemcpy(&x, inv + p.source, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    src = x;
+  }
+  const bool owns_src = !cc && src >= lo && src < hi;
   const L inf = sizeof(L) == 4 ? (L)kInf32 : (L)0x7ff0000000000000ull;
   Ctl *ctl = rb.ctl.p;
   const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
@@ -708,14 +729,18 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   Lc.go("init", k_ctl_init, 1, 1, s, ctl, (int32_t)cc, cc ? hi - lo : (owns_src ? 1u : 0u));
   fill<uint32_t>(Lc, nb, (int64_t)T.lay.nw, 0u, s);
   fill<long long>(Lc, acc.p, kSlot, 0ll, s);
-  if (cc) {  // cc: label = id; round 0 is every owned row (dense), snapshot = id
+  if (cc && inv) {  // relabeled: a vertex's label is its original id (perm)
+    Lc.go("init", k_copy_as<L>, grid_n(nv), 256, s, (const uint32_t *)g.part.perm.p, nv, lab);
+    Lc.go("init", k_copy_as<L>, grid_n(hi - lo), 256, s, (const uint32_t *)g.part.perm.p + lo,
+          (int64_t)(hi - lo), snap.p);
+  } else if (cc) {  // cc: label = id; round 0 is every owned row (dense), snapshot = id
     Lc.go("init", k_iota_from<L>, grid_n(nv), 256, s, lab, nv, (int64_t)0);
     Lc.go("init", k_iota_from<L>, grid_n(hi - lo), 256, s, snap.p, (int64_t)(hi - lo), (int64_t)lo);
   } else {
     fill<L>(Lc, lab, nv, inf, s);
-    Lc.go("init", k_set1<L>, 1, 1, s, lab, p.source, (L)0);
+    Lc.go("init", k_set1<L>, 1, 1, s, lab, src, (L)0);
     if (owns_src) {
-      Lc.go("init", k_set1<uint32_t>, 1, 1, s, rb.q0.p, (int64_t)0, (uint32_t)p.source);
+      Lc.go("init", k_set1<uint32_t>, 1, 1, s, rb.q0.p, (int64_t)0, (uint32_t)src);
       Lc.go("init", k_set1<L>, 1, 1, s, snap.p, (int64_t)0, (L)0);
     }
   }
@@ -723,10 +748,11 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   SG_CUDA(cudaGraphLaunch(W.exec, s));
   barrier(T, s);
   if (sizeof(L) == 4)
-    k_px_gather<uint32_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, out.p, ConvU32{});
+    k_px_gather<uint32_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv, out.p,
+                                                     ConvU32{});
   else
-    k_px_gather<unsigned long long><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, out.p,
-                                                              ConvF64Bits{});
+    k_px_gather<unsigned long long><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv,
+                                                              out.p, ConvF64Bits{});
   SG_CUDA(cudaGetLastError());
   barrier(T, s);  // nobody re-initialises its region while a peer still gathers from it
   SG_CUDA(cudaEventRecord(S.e1, s));
@@ -739,6 +765,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
   const View &v = part_view(g);  // this rank's CSC rows
   const int64_t nv = v.nv;
   const Cuts cuts = part_cuts(g);
+  const uint32_t *pinv = g.part.relabeled ? g.part.inv.p : nullptr;  // old -> new id
   const int R = T.rank;
   const uint32_t lo = (uint32_t)cuts.c[R], hi = (uint32_t)cuts.c[R + 1];
   // everything that may synchronise the device (layout builds) comes before
@@ -838,7 +865,8 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
   barrier(T, s);  // gain slots read everywhere, every region initialised
   SG_CUDA(cudaGraphLaunch(W.exec, s));
   barrier(T, s);
-  k_px_gather<double><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[2], cuts, nv, out.p, ConvF64{});
+  k_px_gather<double><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[2], cuts, nv, pinv, out.p,
+                                                  ConvF64{});
   SG_CUDA(cudaGetLastError());
   barrier(T, s);
   SG_CUDA(cudaEventRecord(S.e1, s));
@@ -852,6 +880,7 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
   const View &v = part_view(g);  // this rank's symmetrized rows
   const int64_t nv = v.nv;
   const Cuts cuts = part_cuts(g);
+  const uint32_t *inv = g.part.relabeled ? g.part.inv.p : nullptr;
   const int R = T.rank;
   const uint32_t lo = (uint32_t)cuts.c[R], hi = (uint32_t)cuts.c[R + 1];
   Stream S;
@@ -915,7 +944,8 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
   barrier(T, s);
   SG_CUDA(cudaGraphLaunch(W.exec, s));
   barrier(T, s);
-  k_px_gather<uint8_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, out.p, ConvAlive{});
+  k_px_gather<uint8_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv, out.p,
+                                                   ConvAlive{});
   SG_CUDA(cudaGetLastError());
   barrier(T, s);
   SG_CUDA(cudaEventRecord(S.e1, s));
@@ -972,6 +1002,74 @@ void team_run(Team &T, Graph &g, const sg_params &p, const Out &o) {
   return run_peer_push<3>(T, g, p, thr, max_rounds, o);
 }
 
+// ------------------------------------------ block-local relabel (partition) --
+__global__ void k_px_indeg(const uint32_t *col, int64_t ne, uint32_t *cnt) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += st)
+    atomicAdd(cnt + col[e], 1u);
+}
+// key = block << 32 | ~total degree: an ascending stable sort puts every block
+// onto itself, highest degree first, ties by id
+__global__ void k_px_key(const int64_t *off, const uint32_t *indeg, int64_t nv, Cuts cuts,
+                         unsigned long long *key, uint32_t *ids) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += st) {
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]) + indeg[v];
+    const unsigned long long dd = d > 0xffffffffull ? 0xffffffffull : d;
+    key[v] = ((unsigned long long)owner_of(cuts, (uint32_t)v) << 32) | (0xffffffffull - dd);
+    ids[v] = (uint32_t)v;
+  }
+}
+// second pass: the first kb vertices of each block (by degree) keep their
+// degree order, the rest follow in id order (a full degree order also
+// reorders the frontier and loses ~10 % on rmat24: profiles/r2x_hotk_sweep)
+__global__ void k_px_key2(const uint32_t *perm0, int64_t nv, Cuts cuts, int64_t kb,
+                          unsigned long long *key, uint32_t *ids) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += st) {
+    const uint32_t v = perm0[i];
+    const int b = owner_of(cuts, v);
+    const long long pos = i - cuts.c[b];
+    key[i] = ((unsigned long long)b << 33) |
+             (pos < kb ? (unsigned long long)pos : (1ull << 32) | (unsigned long long)v);
+    ids[i] = v;
+  }
+}
+__global__ void k_px_invert(const uint32_t *perm, int64_t nv, uint32_t *inv) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += st)
+    inv[perm[i]] = (uint32_t)i;
+}
+// len[i] = degree of old row perm[i] for new rows i in [lo, hi), 0 elsewhere
+__global__ void k_px_len(const int64_t *off, const uint32_t *perm, int64_t nv, int64_t lo,
+                         int64_t hi, int64_t *len) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nv; i += st) {
+    int64_t d = 0;
+    if (i >= lo && i < hi) {
+      const uint32_t o = perm[i];
+      d = off[o + 1] - off[o];
+    }
+    len[i] = d;
+  }
+}
+// new row i = old row perm[i], ids renamed, in-row order kept (pr sums in it);
+// one warp per row
+__global__ void k_px_copy_rows(const int64_t *off, const uint32_t *col, const int64_t *w64,
+                               const uint32_t *perm, const uint32_t *inv, int64_t lo, int64_t hi,
+                               const int64_t *noff, uint32_t *ncol, int64_t *nw64) {
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < hi;
+       i += warps) {
+    const uint32_t o = perm[i];
+    const int64_t s = off[o], d = off[o + 1] - s, t = noff[i];
+    for (int64_t j = lane_id(); j < d; j += 32) {
+      ncol[t + j] = inv[col[s + j]];
+      if (nw64) nw64[t + j] = w64[s + j];
+    }
+  }
+}
+
 // ------------------------------------------------------------ partition --
 __global__ void k_part_off(const int64_t *off, int64_t nv, int64_t lo, int64_t hi, int64_t *out) {
   const int64_t base = off[lo], top = off[hi];
@@ -996,7 +1094,95 @@ void slice_view(View &out, const View &in, int64_t lo, int64_t hi, int64_t *e0, 
                        cudaMemcpyDeviceToDevice));
 }
 
-std::unique_ptr<Graph> make_partition(Graph &g, int kind, int world, int rank) {
+// default: relabel skewed graphs of >= 2^20 vertices (as the single-device store)
+bool want_part_relabel(Graph &g, int mode) {
+  if (mode > 0) return true;
+  if (mode < 0) return false;
+  return g.nv >= ((int64_t)1 << 20) && g.top1_share() >= 0.10;
+}
+
+// the block-local relabeled rows [lo, hi) of view v (+ weights for kind 0)
+void relabeled_slice(Graph &g, const View &v, int kind, const Cuts &c, Graph &P) {
+  const int64_t nv = g.nv, lo = P.part.lo, hi = P.part.hi;
+  P.part.relabeled = true;
+  P.part.perm.alloc((size_t)std::max<int64_t>(nv, 1));
+  P.part.inv.alloc((size_t)std::max<int64_t>(nv, 1));
+  {
+    DBuf<uint32_t> indeg(nv), ids(nv);
+    DBuf<unsigned long long> key(nv), key2(nv);
+    SG_CUDA(cudaMemset(indeg.p, 0, sizeof(uint32_t) * nv));
+    if (v.ne) k_px_indeg<<<grid_n(v.ne), 256>>>(v.col.p, v.ne, indeg.p);
+    k_px_key<<<grid_n(nv), 256>>>(v.off.p, indeg.p, nv, c, key.p, ids.p);
+    SG_CUDA(cudaGetLastError());
+    int bbits = 0;
+    while ((1ll << bbits) < c.D) ++bbits;
+    size_t tb = 0, tb2 = 0;
+    DBuf<uint32_t> perm0(nv);
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, ids.p, perm0.p, (int)nv,
+                                            0, 32 + bbits));
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key.p, key2.p, ids.p, P.part.perm.p,
+                                            (int)nv, 0, 33 + bbits));
+    DBuf<char> t(std::max<size_t>(std::max(tb, tb2), 1));
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, key.p, key2.p, ids.p, perm0.p, (int)nv, 0,
+                                            32 + bbits));
+    // hot set per block: the single-device store's 2^16 spread over the ranks
+    const int64_t kb = std::max<int64_t>(1024, ((int64_t)1 << 16) / c.D);
+    k_px_key2<<<grid_n(nv), 256>>>(perm0.p, nv, c, kb, key.p, ids.p);
+    SG_CUDA(cudaGetLastError());
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb2, key.p, key2.p, ids.p, P.part.perm.p,
+                                            (int)nv, 0, 33 + bbits));
+    k_px_invert<<<grid_n(nv), 256>>>(P.part.perm.p, nv, P.part.inv.p);
+    SG_CUDA(cudaGetLastError());
+  }
+  auto scan_len = [&](const int64_t *off, int64_t rlo, int64_t rhi, DBuf<int64_t> &out) {
+    DBuf<int64_t> len(nv + 1);
+    k_px_len<<<grid_n(nv + 1), 256>>>(off, P.part.perm.p, nv, rlo, rhi, len.p);
+    SG_CUDA(cudaGetLastError());
+    out.alloc((size_t)nv + 1);
+    size_t tb = 0;
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, out.p, (int)(nv + 1)));
+    DBuf<char> t(std::max<size_t>(tb, 1));
+    SG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, len.p, out.p, (int)(nv + 1)));
+  };
+  auto view = std::make_unique<View>();
+  view->nv = nv;
+  scan_len(v.off.p, lo, hi, view->off);
+  int64_t ne = 0;
+  SG_CUDA(cudaMemcpy(&ne, view->off.p + nv, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  view->ne = ne;
+  view->col.alloc((size_t)std::max<int64_t>(ne, 1));
+  const bool w = kind == 0 && g.weighted;
+  if (w) {
+    P.weighted = true;
+    P.w64.alloc((size_t)std::max<int64_t>(ne, 1));
+  }
+  k_px_copy_rows<<<grid_n(std::max<int64_t>(hi - lo, 1) * 32), 256>>>(
+      v.off.p, v.col.p, w ? g.w64.p : nullptr, P.part.perm.p, P.part.inv.p, lo, hi, view->off.p,
+      view->col.p, w ? P.w64.p : nullptr);
+  SG_CUDA(cudaGetLastError());
+  SG_CUDA(cudaDeviceSynchronize());
+  P.ne = ne;
+  if (w) {
+    weights_finalize(P);
+    P.wmin = g.wmin, P.wmax = g.wmax;
+    if (!g.w32.p) P.w32.release();
+  }
+  if (kind == 1) {  // pr: out-degrees of every vertex in the new numbering
+    P.csr.nv = nv;
+    scan_len(g.csr.off.p, 0, nv, P.csr.off);
+    P.csc_ = std::move(view);
+  } else {
+    // push / symmetrized rows: ascending targets (min and count apps do not
+    // depend on the order; pr's CSC keeps it -- it is the summation order)
+    const bool f64path = w && (!P.w32.p || (double)P.wmax * (double)std::max<int64_t>(nv - 1, 1) >= 4294967295.0);
+    if (!f64path) sort_rows(*view, w && P.w32.p ? &P.w32 : nullptr);
+    if (kind == 0) P.csr = std::move(*view);
+    else P.sym_ = std::move(view);
+  }
+  SG_CUDA(cudaDeviceSynchronize());
+}
+
+std::unique_ptr<Graph> make_partition(Graph &g, int kind, int world, int rank, int relabel = 0) {
   if (g.is_part()) throw Error(SG_ECONFIG, "graph is already a partition");
   if (kind < 0 || kind > 2) throw Error(SG_ECONFIG, "partition kind must be 0 (CSR), 1 (CSC) or 2 (symmetrized)");
   if (world < 1 || world > kMaxParts || rank < 0 || rank >= world)
@@ -1010,6 +1196,10 @@ std::unique_ptr<Graph> make_partition(Graph &g, int kind, int world, int rank) {
   P->part.cuts.assign(c.c, c.c + world + 1);
   P->part.lo = c.c[rank], P->part.hi = c.c[rank + 1];
   P->part.full_ne = v.ne;
+  if (want_part_relabel(g, relabel)) {
+    relabeled_slice(g, v, kind, c, *P);
+    return P;
+  }
   int64_t e0 = 0, e1 = 0;
   auto slice = std::make_unique<View>();
   slice_view(*slice, v, P->part.lo, P->part.hi, &e0, &e1);
@@ -1048,7 +1238,8 @@ std::unique_ptr<Graph> make_partition(Graph &g, int kind, int world, int rank) {
 void run_peer_threads(Graph &g, const sg_params &p, int world, const Out &o) {
   const int kind = part_kind_of(p.app);
   std::vector<std::unique_ptr<Graph>> parts;
-  for (int r = 0; r < world; ++r) parts.push_back(make_partition(g, kind, world, r));
+  const int relabel = (p.flags & SG_FLAG_RELABEL) ? 1 : (p.flags & SG_FLAG_NO_RELABEL) ? -1 : 0;
+  for (int r = 0; r < world; ++r) parts.push_back(make_partition(g, kind, world, r, relabel));
   int dev = 0;
   SG_CUDA(cudaGetDevice(&dev));
   std::vector<std::unique_ptr<Team>> teams;
@@ -1110,7 +1301,8 @@ extern "C" {
 int sg_graph_partition(sg_graph *gh, int32_t kind, int32_t world, int32_t rank, sg_graph **out) {
   return sg::guard([&] {
     if (!gh || !out) throw Error(SG_ECONFIG, "null argument");
-    auto P = sg::make_partition(*gh->g, kind, world, rank);
+    const int relabel = (kind & SG_PART_RELABEL) ? 1 : (kind & SG_PART_NO_RELABEL) ? -1 : 0;
+    auto P = sg::make_partition(*gh->g, kind & 0xff, world, rank, relabel);
     *out = new sg_graph{std::shared_ptr<sg::Graph>(P.release())};
   });
 }

@@ -126,14 +126,16 @@ class Partition:
     outgoing edge cut, the reference's make_partition cuts): only the block's
     edges (and weights) are stored in HBM, so the full graph may be dropped."""
 
-    def __init__(self, graph, app_name: str, rank: int, world: int):
+    def __init__(self, graph, app_name: str, rank: int, world: int, relabel=None):
         if app_name not in PART_KIND:
             raise ConfigError(f"unknown app {app_name!r}")
         self.app_name = app_name
         self.num_vertices = graph.num_vertices
         self.num_edges = graph.num_edges
         self.rank, self.world = rank, world
-        self._dev = native.DevicePartition.of(graph.device(), PART_KIND[app_name], world, rank)
+        kind = PART_KIND[app_name] | (0 if relabel is None else
+                                      native.PART_RELABEL if relabel else native.PART_NO_RELABEL)
+        self._dev = native.DevicePartition.of(graph.device(), kind, world, rank)
         info = self._dev.part_info()
         self.kind, self.cuts, self.view_edges = info["kind"], info["cuts"], info["full_edges"]
         self.local_edges = self._dev.info()[1]
@@ -146,10 +148,12 @@ class Partition:
         return int(self.cuts[self.rank]), int(self.cuts[self.rank + 1])
 
 
-def partition(graph, app_name: str, rank: int, world: int) -> Partition:
+def partition(graph, app_name: str, rank: int, world: int, relabel=None) -> Partition:
     """This rank's edge-cut rows for ``app_name`` (CSR for bfs / sssp, CSC for
-    pr, symmetrized for cc / kcore)."""
-    return Partition(graph, app_name, rank, world)
+    pr, symmetrized for cc / kcore).  ``relabel``: the block-local hot-vertex
+    layout (True / False; None = automatic: skewed graphs of >= 2^20
+    vertices); labels are returned in the original numbering either way."""
+    return Partition(graph, app_name, rank, world, relabel)
 
 
 def _all_gather_bytes(dist, data: bytes) -> list:
@@ -191,13 +195,15 @@ def run_app_peer(part: Partition, app_name: str, scheduler: Scheduler = Schedule
 
 def run_app_peer_threads(graph, app_name: str, scheduler: Scheduler = Scheduler("alb"),
                          config: KernelConfig = KernelConfig(), *, world: int, max_rounds=None,
-                         **params) -> RunResult:
+                         relabel=None, **params) -> RunResult:
     """The peer transport with `world` ranks as threads on this GPU (each with
     its own partition and region): the multi-GPU kernels on one device."""
     app = make_app(app_name, **params)
     if max_rounds is None:
         max_rounds = 10 * max(graph.num_vertices, 1) + 256
     p = device_params(app, scheduler, config, world, max_rounds)
+    if relabel is not None:
+        p.flags |= native.FLAG_RELABEL if relabel else native.FLAG_NO_RELABEL
     labels, log, ms = native.peer_run_threads(graph.device(), p, world)
     return RunResult(labels=labels, records=records_from_log(log, scheduler, config),
                      app_name=app.name, scheduler=scheduler, config=config, devices=world,

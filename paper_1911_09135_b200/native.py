@@ -403,6 +403,8 @@ def _run_with_log(call, nv, rounds_cap):
 
 
 PART_CSR, PART_CSC, PART_SYM = 0, 1, 2
+PART_RELABEL, PART_NO_RELABEL = 0x100, 0x200  # block-local hot relabeling on / off
+FLAG_RELABEL, FLAG_NO_RELABEL = 8, 16          # sg_params.flags
 
 
 class DevicePartition(DeviceGraph):

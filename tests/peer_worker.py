@@ -27,13 +27,14 @@ def main():
     gw = sg.attach_random_weights(g, 2)
     team = dist.make_team(tdist, g.num_vertices)
     result = {}
-    for app in ("bfs", "sssp", "cc", "pr", "kcore"):
-        part = dist.partition(gw if app == "sssp" else g, app, rank, world)
+    for app, relabel in [(a, r) for r in (False, True)
+                         for a in ("bfs", "sssp", "cc", "pr", "kcore")]:
+        part = dist.partition(gw if app == "sssp" else g, app, rank, world, relabel=relabel)
         res = dist.run_app_peer(part, app, sg.Scheduler("alb"), team=team)
         info = golden["runs"]["rmat12"][f"{app}/alb/d{world}"]
         rounds = [[r.frontier_size, r.active_edges()] for r in res.records]
         comm = [[r.comm_sent, r.comm_broadcast] for r in res.records]
-        result[app] = {
+        result[f"{app}{'/relabel' if relabel else ''}"] = {
             "labels": sg.engine.labels_sha256(res.labels) == info["labels_sha256"],
             "rounds": rounds == [x[:2] for x in info["per_round"]],
             "comm_sent": [c[0] for c in comm] == [x[2] for x in info["per_round"]],

@@ -38,7 +38,10 @@ def sg():
                                        ("rmat10", "twc/d4"), ("rmat10", "alb-t64/d2"),
                                        ("uniform10", "alb/d3")])
 @pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
-def test_peer_ranks_as_threads(sg, golden, app, gname, key):
+@pytest.mark.parametrize("relabel", [False, True])
+def test_peer_ranks_as_threads(sg, golden, app, gname, key, relabel):
+    """relabel: the block-local hot-vertex layout (each rank's block renumbered
+    onto itself, rows sorted) -- same labels, logs and counters."""
     from paper_1911_09135_b200 import dist
     info = golden["runs"][gname][f"{app}/{key}"]
     g = _graph(sg, gname)
@@ -46,7 +49,7 @@ def test_peer_ranks_as_threads(sg, golden, app, gname, key):
         g = sg.attach_random_weights(g, 2)
     world = int(key.split("/d")[1])
     res = dist.run_app_peer_threads(g, app, _sched(sg, "x/" + key.split("/")[0] + "/x"),
-                                    world=world)
+                                    world=world, relabel=relabel)
     _check(sg, res, info, app)
     if app == "pr":  # the exact-order pull: bit-identical to the reference
         assert [r.comm_broadcast for r in res.records] == [x[3] for x in info["per_round"]]
@@ -95,8 +98,9 @@ def test_peer_world1_matches_single_device(sg, golden, app):
         g = sg.attach_random_weights(g, 2)
     team = native.Team(0, 1, g.num_vertices)
     part = dist.partition(g, app, 0, 1)
-    for _ in range(2):  # the team and the cached mirror masks are reused
-        res = dist.run_app_peer(part, app, sg.Scheduler("alb"), team=team)
+    part2 = dist.partition(g, app, 0, 1, relabel=True)
+    for pp in (part, part, part2):  # the team and the cached mirror masks are reused
+        res = dist.run_app_peer(pp, app, sg.Scheduler("alb"), team=team)
         assert sg.engine.labels_sha256(res.labels) == info["labels_sha256"]
         assert [[r.frontier_size, r.active_edges()] for r in res.records] == \
             [x[:2] for x in info["per_round"]]
