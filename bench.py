@@ -95,6 +95,9 @@ def parse():
                     help="skip the BASELINE configs C3-C5 at their own scales")
     ap.add_argument("--no-heavy", action="store_true",
                     help="skip the heavy-skew ALB vs TWC-only ablation")
+    ap.add_argument("--peer", action="store_true",
+                    help="N=1: run the multi-GPU code path (partition + NVLink peer team of one "
+                         "rank, device barrier, label gather) instead of sg_run")
     return ap.parse_args()
 
 
@@ -411,6 +414,9 @@ def run_reference(a):
 
 def main():
     a = parse()
+    if a.peer:  # the multi-GPU code path alone: no single-device sections
+        a.no_cpu_baseline = a.no_ablation = a.no_configs = a.no_heavy = True
+        a.extra = ""
     if a.impl == "reference":
         return run_reference(a)
     rank, local_rank, world = dist_env()
@@ -435,7 +441,7 @@ def main():
     params.reserved = a.pr_block if a.pr_block > 0 else (1 << 31) - 1 if a.pr_block < 0 else 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     team = part = None
-    if world > 1:
+    if world > 1 or a.peer:
         # edge cut over NVLink peer memory: this rank keeps only its rows (the
         # full graph is generated, sliced and dropped), the label exchange is
         # done by the round's kernels in the peers' HBM (sg_peer.cu)
@@ -444,11 +450,14 @@ def main():
         host_csr = None if a.no_e2e else dev.download(0, weights=(a.app == "sssp"))
         del g, g_base, dev
         native.release_cached()
-        team = sgdist.make_team(torch.distributed, nv)
+        if world > 1:
+            team = sgdist.make_team(torch.distributed, nv)
+        else:
+            team = native.Team(0, 1, nv)
         dev = part.device()
 
     def step(d):
-        if world > 1:
+        if team is not None:
             return team.run(d, params)
         return d.run(params)
 
@@ -486,14 +495,14 @@ def main():
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
     if not a.no_e2e:
-        off, tgt, w = host_csr if world > 1 else dev.download(0, weights=(a.app == "sssp"))
+        off, tgt, w = host_csr if team is not None else dev.download(0, weights=(a.app == "sssp"))
         pin = lambda x: torch.from_numpy(x).pin_memory().numpy() if x is not None else None
         off_p, tgt_p, w_p = pin(off), pin(tgt), pin(w)
         h2d = off_p.nbytes + tgt_p.nbytes + (w_p.nbytes if w_p is not None else 0)
         d2h = 8 * nv + native.ROUND_DTYPE.itemsize * rounds
         def upload():
             dg = native.DeviceGraph.from_csr(off_p, tgt_p, w_p)
-            if world == 1:
+            if team is None:
                 return dg
             kind = sgdist.PART_KIND[a.app]
             return native.DevicePartition.of(dg, kind, world, rank)
@@ -517,7 +526,7 @@ def main():
                "ms_per_step": 1e3 * e2e_tot / len(e2e_s), "steps": len(e2e_s),
                "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights), sg_run "
                        "(original numbering: a fresh graph's first run), labels + round log D2H"
-                       if world == 1 else
+                       if team is None else
                        "per step and rank: sg_graph_create of the full CSR (+ int64 weights) "
                        "from pinned host memory, sg_graph_partition (this rank's rows), "
                        "sg_team_run, labels + round log D2H; max over ranks"}
@@ -525,7 +534,7 @@ def main():
 
     # ---------------- roofline from a profiled run ----------------
     roofline, kernels = None, {}
-    if world == 1:
+    if team is None:
         _, plog, pms, kernels = dev.run(params, profile=True)
         roofline = roofline_of(a.app, kernels, plog, statistics.median(step_ms), workload)
 
@@ -644,7 +653,7 @@ def main():
                    "rounds": rounds,
                    "parallelism": f"edge-cut x{world}: per-rank partitions, label exchange by "
                                   "the round's kernels over NVLink peer memory, device "
-                                  "barrier + quiescence (sg_peer.cu)" if world > 1
+                                  "barrier + quiescence (sg_peer.cu)" if team is not None
                    else "single",
                    "l2": "flushed (512 MB write) before every step",
                    "timing": "sum of per-step CUDA-event durations of sg_run (one graph launch "

@@ -71,12 +71,13 @@ struct Hdr {
 };
 
 // Byte layout of every rank's region (identical on all ranks of a team):
-// header, next-frontier bitmap, mirror-holding bitmap (setup), three 8 B/V
-// slabs (push: labels; pr: aux0 / aux1 / rank; kcore: alive / mark).
+// header, next-frontier bitmap (bfs: visited), mirror-holding bitmap (setup),
+// bfs round-start visited bitmap, three 8 B/V slabs (push: labels; pr: aux0 /
+// aux1 / rank; kcore: alive / mark).
 struct Layout {
   int64_t nv = 0;
   size_t nw = 0;
-  size_t o_nb = 0, o_held = 0, o_d[3] = {0, 0, 0}, bytes = 0;
+  size_t o_nb = 0, o_held = 0, o_prev = 0, o_d[3] = {0, 0, 0}, bytes = 0;
   static Layout of(int64_t nv) {
     auto al = [](size_t x) { return (x + 511) & ~(size_t)511; };
     Layout L;
@@ -85,6 +86,7 @@ struct Layout {
     size_t o = al(sizeof(Hdr));
     L.o_nb = o, o = al(o + 4 * L.nw);
     L.o_held = o, o = al(o + 4 * L.nw);
+    L.o_prev = o, o = al(o + 4 * L.nw);  // bfs: visited bits as of the round start
     const size_t slab = al(8 * (size_t)std::max<int64_t>(nv, 1));
     for (int i = 0; i < 3; ++i) L.o_d[i] = o, o += slab;
     L.bytes = o;
@@ -267,7 +269,10 @@ __global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts c
 }
 
 // compact (after the barrier): owned marked rows -> next local frontier with
-// their snapshot labels; each changed label is stored into its mirror holders
+// their snapshot labels; each changed label is stored into its mirror holders.
+// A warp takes 32 bitmap words and emits their set bits cooperatively (lane
+// l emits slot l, l + 32, ...: a dense hot-set word block is 32 vertices per
+// step, not 32 dependent steps of one lane)
 template <class L>
 __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts cuts, Ctl *ctl,
                                                     const uint32_t *mask, uint32_t *q, L *snap,
@@ -278,12 +283,14 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
   uint32_t *nb = at<uint32_t>(t, self, lay.o_nb);
   const L *lab = at<L>(t, self, lay.o_d[0]);
   const int64_t lo = cuts.c[self], hi = cuts.c[self + 1];
+  const uint32_t lane = lane_id();
   unsigned long long bc = 0;
   if (hi > lo) {
     const int64_t w0 = lo / 32, w1 = (hi - 1) / 32 + 1;
-    const int64_t st = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t b = w0 + (int64_t)blockIdx.x * blockDim.x; b < w1; b += st) {
-      const int64_t w = b + threadIdx.x;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = w0 + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32;
+         b < w1; b += warps * 32) {
+      const int64_t w = b + lane;
       uint32_t x = 0;
       if (w < w1) {
         x = nb[w] & owned_bits(w, lo, hi);
@@ -291,17 +298,22 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
       }
       const uint32_t n = (uint32_t)__popc(x);
       const uint32_t incl = warp_incl_scan(n);
+      const uint32_t total = __shfl_sync(kFull, incl, 31);
+      if (!total) continue;
       uint32_t base = 0;
-      if (lane_id() == 31 && incl) base = atomicAdd(&ctl->nsize, incl);
-      base = __shfl_sync(kFull, base, 31);
-      uint32_t slot = base + incl - n;
-      while (x) {
-        const uint32_t v = (uint32_t)(w * 32) + (uint32_t)(__ffs(x) - 1);
-        x &= x - 1;
+      if (lane == 0) base = atomicAdd(&ctl->nsize, total);
+      base = __shfl_sync(kFull, base, 0);
+      const uint32_t excl = incl - n;
+      for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+        const uint32_t slot = k0 + lane;
+        const int o = warp_owner(incl, slot);
+        const uint32_t xo = __shfl_sync(kFull, x, o);
+        const uint32_t eo = __shfl_sync(kFull, excl, o);
+        if (slot >= total) continue;
+        const uint32_t v = (uint32_t)((b + o) * 32) + __fns(xo, 0, (int)(slot - eo) + 1);
         const L val = lab[v];
-        q[slot] = v;
-        snap[slot] = val;
-        ++slot;
+        q[base + slot] = v;
+        snap[base + slot] = val;
         uint32_t m = mask[v - lo];
         bc += (unsigned long long)__popc(m);
         while (m) {
@@ -317,9 +329,164 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
   __threadfence_system();
 }
 
-__global__ void k_px_next(const Ctl *ctl, long long *acc) {
-  if (threadIdx.x || ctl->done) return;
-  acc[10] = ctl->nsize;
+// ---- bfs: the visited-bitmap operator (BmBfs) over the peers.  vis (the nb
+// slot) and prev (round-start vis) are full-length on every rank; a rank's
+// mirror bits are exact at a round start (owners broadcast new vertices into
+// both bitmaps of the mirror holders), so vis & ~prev on a mirror word is
+// exactly what this rank discovered this round (`out_d != baseline`).
+__global__ void __launch_bounds__(256) k_px_bfs_reduce(TeamDev t, Layout lay, Cuts cuts,
+                                                       const Ctl *ctl, long long *acc) {
+  __shared__ unsigned long long red[32];
+  if (ctl->done) return;
+  const int self = t.rank;
+  const uint32_t *vis = at<uint32_t>(t, self, lay.o_nb);
+  uint32_t *prev = at<uint32_t>(t, self, lay.o_prev);
+  const int64_t lo = cuts.c[self], hi = cuts.c[self + 1];
+  const int64_t nw = (lay.nv + 31) / 32, st = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long sent = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += st) {
+    const uint32_t own = owned_bits(w, lo, hi);
+    if (own == kFull) continue;
+    const uint32_t x = vis[w] & ~prev[w] & ~own;
+    if (!x) continue;
+    if (own) atomicOr(prev + w, x);  // peers may set owned bits of a boundary word
+    else prev[w] |= x;
+    sent += (unsigned long long)__popc(x);
+    uint32_t y = x;
+    while (y) {
+      const uint32_t v = (uint32_t)(w * 32) + (uint32_t)(__ffs(y) - 1);
+      y &= y - 1;
+      atomicOr_system(at<uint32_t>(t, owner_of(cuts, v), lay.o_nb) + (v >> 5), 1u << (v & 31u));
+    }
+  }
+  sent = block_sum(sent, red);
+  if (threadIdx.x == 0 && sent) atomicAdd((unsigned long long *)&acc[6], sent);
+  __threadfence_system();
+}
+
+// owners: new owned bits -> next frontier, label round + 1; the vertex is
+// marked visited in both bitmaps of its mirror holders
+__global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, Cuts cuts,
+                                                        Ctl *ctl, const uint32_t *mask,
+                                                        uint32_t *q, long long *acc) {
+  __shared__ unsigned long long red[32];
+  if (ctl->done) return;
+  const int self = t.rank;
+  const uint32_t *vis = at<uint32_t>(t, self, lay.o_nb);
+  uint32_t *prev = at<uint32_t>(t, self, lay.o_prev);
+  uint32_t *lab = at<uint32_t>(t, self, lay.o_d[0]);
+  const uint32_t level = ctl->round + 1;
+  const int64_t lo = cuts.c[self], hi = cuts.c[self + 1];
+  const uint32_t lane = lane_id();
+  unsigned long long bc = 0;
+  if (hi > lo) {
+    const int64_t w0 = lo / 32, w1 = (hi - 1) / 32 + 1;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = w0 + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32;
+         b < w1; b += warps * 32) {
+      const int64_t w = b + lane;
+      uint32_t x = 0;
+      if (w < w1) {
+        x = vis[w] & ~prev[w] & owned_bits(w, lo, hi);
+        if (x) atomicOr(prev + w, x);
+      }
+      const uint32_t n = (uint32_t)__popc(x);
+      const uint32_t incl = warp_incl_scan(n);
+      const uint32_t total = __shfl_sync(kFull, incl, 31);
+      if (!total) continue;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&ctl->nsize, total);
+      base = __shfl_sync(kFull, base, 0);
+      const uint32_t excl = incl - n;
+      for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+        const uint32_t slot = k0 + lane;
+        const int o = warp_owner(incl, slot);
+        const uint32_t xo = __shfl_sync(kFull, x, o);
+        const uint32_t eo = __shfl_sync(kFull, excl, o);
+        if (slot >= total) continue;
+        const uint32_t v = (uint32_t)((b + o) * 32) + __fns(xo, 0, (int)(slot - eo) + 1);
+        q[base + slot] = v;
+        lab[v] = level;
+        uint32_t m = mask[v - lo];
+        bc += (unsigned long long)__popc(m);
+        const uint32_t bit = 1u << (v & 31u);
+        while (m) {
+          const int r = __ffs(m) - 1;
+          m &= m - 1;
+          atomicOr_system(at<uint32_t>(t, r, lay.o_nb) + (v >> 5), bit);
+          atomicOr_system(at<uint32_t>(t, r, lay.o_prev) + (v >> 5), bit);
+        }
+      }
+    }
+  }
+  bc = block_sum(bc, red);
+  if (threadIdx.x == 0 && bc) atomicAdd((unsigned long long *)&acc[7], bc);
+  __threadfence_system();
+}
+
+// the round's counter block (k_dp_collect + the next-frontier size; sent and
+// bcast were added by reduce / compact) -> every peer's slot
+__global__ void k_px_push_publish(PushArgs a, TeamDev t, long long *acc) {
+  const Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  if (threadIdx.x == 0) {
+    const long long fs = ctl->dense ? a.dense_n : ctl->fsize;
+    acc[0] = fs;
+    acc[1] = (long long)ctl->edges;
+    acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
+    acc[3] = a.sched >= 2 ? 0 : (long long)ctl->huge_edges;
+    acc[4] = a.sched >= 2 ? 0 : ctl->nlarge;
+    acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
+    acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
+    acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
+    acc[10] = ctl->nsize;
+  }
+  __syncthreads();
+  const int par = ctl->round & 1;
+  for (int i = threadIdx.x; i < t.world * kDP; i += blockDim.x)
+    hdr(t, i / kDP)->cnt[par][t.rank][i % kDP] = acc[i % kDP];
+  __threadfence_system();
+}
+
+// after the barrier: sum the slots, write the round log, decide quiescence
+// (identically on every rank), reset the round state; leaves the WHILE loop
+// when the run is done for any reason (a barrier timeout included)
+__global__ void k_px_push_advance(PushArgs a, TeamDev t, long long *acc, Loop lp) {
+  Ctl *ctl = a.ctl;
+  if (threadIdx.x) return;
+  if (ctl->done) {
+    if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+    return;
+  }
+  const int par = ctl->round & 1;
+  const Hdr *me = hdr(t, t.rank);
+  long long x[kDP];
+  for (int j = 0; j < kDP; ++j) {
+    long long sum = 0;
+    for (int q = 0; q < t.world; ++q) sum += ld_volatile(&me->cnt[par][q][j]);
+    x[j] = sum;
+  }
+  const uint32_t round = ctl->round;
+  RoundStat &s = a.stats[round];
+  s.frontier_size = x[0];
+  s.active_edges = x[1];
+  s.huge_count = x[2];
+  s.huge_edges = x[3];
+  s.large_count = x[4];
+  s.large_edges = x[5];
+  s.updated = x[10];
+  s.comm_sent = x[6];
+  s.comm_broadcast = x[7];
+  s.launches_twc = x[8];
+  s.launches_lb = x[9];
+  ctl->fsize = ctl->nsize;
+  ctl->nsize = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
+  ctl->dense = 0;
+  ctl->round = round + 1;
+  for (int j = 0; j < kDP; ++j) acc[j] = 0;
+  loop_test(ctl, round, x[10] == 0, lp);
 }
 
 // ------------------------------------------------------------- pr, kcore --
@@ -711,19 +878,14 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
     const Loop lp{limit, max_rounds, cond, 1};
     RoundCtx c{Lc, s, cond, 1};
     bm_round(c, a, op, p.blocked != 0, classic, tsum.p, /*compact=*/false);
-    Lc.go("dist", k_dp_collect, 1, 32, s, a, acc.p);
     Lc.go("peer_reduce", k_px_reduce<L>, grid_n((int64_t)T.lay.nw), 256, s, td, T.lay, cuts,
           (const Ctl *)ctl, acc.p);
     Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    Lc.go("peer_compact", k_px_compact<L>, grid_n(std::max<int64_t>((hi - lo) / 32 + 2, 1)), 256,
-          s, td, T.lay, cuts, ctl, (const uint32_t *)mi.mask.p, rb.q0.p, snap.p, acc.p);
-    Lc.go("dist", k_px_next, 1, 32, s, (const Ctl *)ctl, acc.p);
-    Lc.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)ctl, (const long long *)acc.p,
-          kDP);
+    Lc.go("peer_compact", k_px_compact<L>, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
+          T.lay, cuts, ctl, (const uint32_t *)mi.mask.p, rb.q0.p, snap.p, acc.p);
+    Lc.go("peer_publish", k_px_push_publish, 1, 256, s, a, td, acc.p);
     Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    Lc.go("peer_sum", k_px_reduce_slots, 1, 32, s, td, (const Ctl *)ctl, acc.p, kDP, 0u);
-    Lc.go("advance", k_dp_advance, 1, 32, s, a, acc.p, lp);
-    Lc.go("guard", k_loop_guard, 1, 32, s, (const Ctl *)ctl, lp);
+    Lc.go("advance", k_px_push_advance, 1, 32, s, a, td, acc.p, lp);
   });
   SG_CUDA(cudaEventRecord(S.e0, s));
   Lc.go("init", k_ctl_init, 1, 1, s, ctl, (int32_t)cc, cc ? hi - lo : (owns_src ? 1u : 0u));
@@ -755,6 +917,79 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
                                                               out.p, ConvF64Bits{});
   SG_CUDA(cudaGetLastError());
   barrier(T, s);  // nobody re-initialises its region while a peer still gathers from it
+  SG_CUDA(cudaEventRecord(S.e1, s));
+  finish_run(T, S, rb, out.p, nv, o, max_rounds, W.nodes);
+}
+
+// ---------------------------------------------------------- bfs driver --
+void run_peer_bfs(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds,
+                  const Out &o) {
+  const bool classic = (p.flags & SG_FLAG_TWC_CLASSIC) != 0;
+  const View &v = part_view(g);
+  const int64_t nv = v.nv;
+  const Cuts cuts = part_cuts(g);
+  const uint32_t *inv = g.part.relabeled ? g.part.inv.p : nullptr;
+  const int R = T.rank;
+  const uint32_t lo = (uint32_t)cuts.c[R], hi = (uint32_t)cuts.c[R + 1];
+  Stream S;
+  cudaStream_t s = S.s;
+  MirrorInfo &mi = mirrors(T, g, s);
+  RunBufs rb;
+  rb.alloc_common(nv, stats_cap(max_rounds));
+  PushArgs a = rb.push_args(v, thr);
+  a.q[1] = a.q[0];  // the frontier is rebuilt by k_px_bfs_compact after the relaxations
+  a.sched = p.sched == SG_SCHED_LB ? 1 : p.sched == SG_SCHED_VERTEX ? 2 : p.sched == SG_SCHED_EDGE ? 3 : 0;
+  const TeamDev td = T.dev();
+  uint32_t *lab = reinterpret_cast<uint32_t *>(T.base + T.lay.o_d[0]);
+  uint32_t *vis = reinterpret_cast<uint32_t *>(T.base + T.lay.o_nb);
+  uint32_t *prev = reinterpret_cast<uint32_t *>(T.base + T.lay.o_prev);
+  DBuf<long long> acc(kSlot), tsum((nv + kFT - 1) / kFT + 1);
+  DBuf<double> out(std::max<int64_t>(nv, 1));
+  int64_t src = p.source;
+  if (inv) {
+    uint32_t x = 0;
+    SG_CUDA(cudaMemcpy(&x, inv + p.source, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    src = x;
+  }
+  const bool owns_src = src >= lo && src < hi;
+  // prev is the round-start copy the operator's compaction would advance; the
+  // peer compaction advances it instead (BmBfs::take is not used)
+  const BmBfs op{lab, vis, prev};
+  Ctl *ctl = rb.ctl.p;
+  const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
+  Launcher Lc;
+  WhileGraph W;
+  W.build(s, [&](cudaGraphConditionalHandle cond) {
+    const Loop lp{limit, max_rounds, cond, 1};
+    RoundCtx c{Lc, s, cond, 1};
+    bm_round(c, a, op, p.blocked != 0, classic, tsum.p, /*compact=*/false);
+    Lc.go("peer_reduce", k_px_bfs_reduce, grid_n((int64_t)T.lay.nw), 256, s, td, T.lay, cuts,
+          (const Ctl *)ctl, acc.p);
+    Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
+    Lc.go("peer_compact", k_px_bfs_compact, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
+          T.lay, cuts, ctl, (const uint32_t *)mi.mask.p, rb.q0.p, acc.p);
+    Lc.go("peer_publish", k_px_push_publish, 1, 256, s, a, td, acc.p);
+    Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
+    Lc.go("advance", k_px_push_advance, 1, 32, s, a, td, acc.p, lp);
+  });
+  SG_CUDA(cudaEventRecord(S.e0, s));
+  Lc.go("init", k_ctl_init, 1, 1, s, ctl, 0, owns_src ? 1u : 0u);
+  fill<uint32_t>(Lc, vis, (int64_t)T.lay.nw, 0u, s);
+  fill<uint32_t>(Lc, prev, (int64_t)T.lay.nw, 0u, s);
+  fill<long long>(Lc, acc.p, kSlot, 0ll, s);
+  fill<uint32_t>(Lc, lab, nv, kInf32, s);
+  // every rank knows the source is visited (its label 0 is final)
+  Lc.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
+  Lc.go("init", k_set1<uint32_t>, 1, 1, s, vis, src >> 5, 1u << (src & 31));
+  Lc.go("init", k_set1<uint32_t>, 1, 1, s, prev, src >> 5, 1u << (src & 31));
+  if (owns_src) Lc.go("init", k_set1<uint32_t>, 1, 1, s, rb.q0.p, (int64_t)0, (uint32_t)src);
+  barrier(T, s);
+  SG_CUDA(cudaGraphLaunch(W.exec, s));
+  barrier(T, s);
+  k_px_gather<uint32_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv, out.p,
+                                                   ConvU32{});
+  SG_CUDA(cudaGetLastError());
+  barrier(T, s);
   SG_CUDA(cudaEventRecord(S.e1, s));
   finish_run(T, S, rb, out.p, nv, o, max_rounds, W.nodes);
 }
@@ -996,7 +1231,8 @@ void team_run(Team &T, Graph &g, const sg_params &p, const Out &o) {
   if (p.app == SG_APP_KCORE) return run_peer_kcore(T, g, p, thr, max_rounds, o);
   if (p.app == SG_APP_CC) return run_peer_push<0>(T, g, p, thr, max_rounds, o);
   const bool weighted = p.app == SG_APP_SSSP && g.weighted;
-  if (!weighted) return run_peer_push<1>(T, g, p, thr, max_rounds, o);  // bfs == unit weights
+  if (p.app == SG_APP_BFS) return run_peer_bfs(T, g, p, thr, max_rounds, o);
+  if (!weighted) return run_peer_push<1>(T, g, p, thr, max_rounds, o);  // unit-weight sssp
   const double bound = (double)g.wmax * (double)std::max<int64_t>(g.nv - 1, 1);
   if (g.w32.p && bound < 4294967295.0) return run_peer_push<2>(T, g, p, thr, max_rounds, o);
   return run_peer_push<3>(T, g, p, thr, max_rounds, o);
