@@ -515,10 +515,17 @@ __global__ void k_row_batches(const int64_t *off, int64_t nv, int nb, int64_t *c
   }
   cut[nb] = nv;
 }
-__global__ void k_rebase(const int64_t *off, int64_t n, int64_t base, int *out) {
+// rebased segment bounds; rows of >= max_len edges become empty segments
+// (left unsorted: a hub row's sorted targets are dense runs of ids, and 32
+// lanes reducing into one bitmap word / label sector serialise at the L2)
+__global__ void k_rebase(const int64_t *off, int64_t n, int64_t base, int64_t max_len, int *beg,
+                         int *end) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
-    out[i] = (int)(off[i] - base);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += st) {
+    const int64_t b = off[i] - base, e = off[i + 1] - base;
+    beg[i] = (int)b;
+    end[i] = e - b >= max_len ? (int)b : (int)e;
+  }
 }
 
 // Sort every row of a push layout by target id (weights carried along).  The
@@ -540,28 +547,33 @@ void sort_rows(View &v, DBuf<uint32_t> *w32) {
   for (int k = 0; k <= nb; ++k)
     SG_CUDA(cudaMemcpy(&ho[k], v.off.p + hc[k], sizeof(int64_t), cudaMemcpyDeviceToHost));
   DBuf<uint32_t> kout(v.ne), vout(w32 ? v.ne : 0);
+  // the unsorted (hub) rows keep their order: start from a copy
+  SG_CUDA(cudaMemcpy(kout.p, v.col.p, sizeof(uint32_t) * v.ne, cudaMemcpyDeviceToDevice));
+  if (w32) SG_CUDA(cudaMemcpy(vout.p, w32->p, sizeof(uint32_t) * v.ne, cudaMemcpyDeviceToDevice));
+  const int64_t max_len = (int64_t)1 << 16;
   for (int k = 0; k < nb; ++k) {
     const int64_t r0 = hc[k], r1 = hc[k + 1], e0 = ho[k], n = ho[k + 1] - ho[k];
     if (r1 <= r0 || n <= 0) continue;
     if (n > 0x7fffffffLL) throw Error(SG_ERANGE, "row batch too large to sort");
-    DBuf<int> ro(r1 - r0 + 1);
-    SG_LAUNCH(k_rebase, grid_for(r1 - r0 + 1), 256, 0, 0, v.off.p + r0, r1 - r0 + 1, e0, ro.p);
+    DBuf<int> rb(r1 - r0), re(r1 - r0);
+    SG_LAUNCH(k_rebase, grid_for(r1 - r0 + 1), 256, 0, 0, v.off.p + r0, r1 - r0 + 1, e0, max_len,
+              rb.p, re.p);
     size_t tb = 0;
     if (w32)
       SG_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, v.col.p + e0, kout.p + e0,
                                                   w32->p + e0, vout.p + e0, (int)n, (int)(r1 - r0),
-                                                  ro.p, ro.p + 1));
+                                                  rb.p, re.p));
     else
       SG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, v.col.p + e0, kout.p + e0, (int)n,
-                                                 (int)(r1 - r0), ro.p, ro.p + 1));
+                                                 (int)(r1 - r0), rb.p, re.p));
     DBuf<char> t(std::max<size_t>(tb, 1));
     if (w32)
       SG_CUDA(cub::DeviceSegmentedSort::SortPairs(t.p, tb, v.col.p + e0, kout.p + e0,
                                                   w32->p + e0, vout.p + e0, (int)n, (int)(r1 - r0),
-                                                  ro.p, ro.p + 1));
+                                                  rb.p, re.p));
     else
       SG_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tb, v.col.p + e0, kout.p + e0, (int)n,
-                                                 (int)(r1 - r0), ro.p, ro.p + 1));
+                                                 (int)(r1 - r0), rb.p, re.p));
     g_launches.fetch_add(1);
     SG_CUDA(cudaDeviceSynchronize());
   }
