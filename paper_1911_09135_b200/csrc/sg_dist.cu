@@ -491,7 +491,7 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
                           keep.emplace_back(new DBuf<char>(bytes));
                           return (void *)keep.back()->p;
                         });
-  const int gx = occupancy_grid(k_prx, kTB);
+  const int gx = occupancy_grid(k_prx<0>, kTB);
   DistLoop dl;
   cudaStream_t s = dl.s;
   Launcher L;
@@ -516,7 +516,7 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
   if (v.ne) {  // gain: exact sums of this rank's rows, then the max over ranks
     PrxArgs xg = xa;
     xg.gain = 1;
-    L.go("pr_gain", k_prx, gx, kTB, s, xg, fold);
+    L.go("pr_gain", k_prx<0>, gx, kTB, s, xg, fold);
     cm.allreduce(gmax.p, 1, CType::U64, COp::Max, s);
   }
   fill<uint32_t>(L, head.p, 1, 0u, s);
@@ -528,7 +528,7 @@ void run_pr_dist(Graph &g, const sg_params &p, int64_t thr, int64_t max_rounds, 
   L.go("init", k_static_bins, grid_n(hi - lo), 256, s, v.off.p, lo, hi - lo, thr, rb.largeq.p,
        rb.hugeq.p, ctl, one);
   for (int64_t r = 0; r <= limit; ++r) {
-    L.go("pr_pull", k_prx, gx, kTB, s, xa, fold);
+    L.go("pr_pull", k_prx<0>, gx, kTB, s, xa, fold);
     L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
     double *auxn = (r & 1) ? aux0.p : aux1.p;  // round r writes next1 / next0
     cm.group_begin();

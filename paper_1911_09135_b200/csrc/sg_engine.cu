@@ -321,7 +321,8 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
   const int64_t hs = exact_hs();
   const int nb = S > 0 ? (int)((nv + S - 1) / S) : 1;
   double *carry = nb > 1 ? P.buf<double>(nv) : nullptr;
-  uint32_t *heads = P.buf<uint32_t>(nb);
+  // heads[b]: block b's long-row tickets, heads[nb + b]: its SELL groups
+  uint32_t *heads = P.buf<uint32_t>(2 * nb);
   long long *meta = P.buf<long long>(4);  // the reference's bins of the full CSC (round log)
   // SG_PR_SPLIT_ALL (experiments): every long row through the split path
   static const bool split_all = std::getenv("SG_PR_SPLIT_ALL") && std::atoi(std::getenv("SG_PR_SPLIT_ALL"));
@@ -335,13 +336,44 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
     x.cta_edges = rb.cta.p, x.cta_g = rb.cta_g, x.cta_rounds = rb.cta_rounds;
     xa[(size_t)b] = x;
   }
-  const int gx = occupancy_grid(k_prx, kTB);
+  const int gx = occupancy_grid(k_prx<0>, kTB);
+  const int gbig = occupancy_grid(k_prx<1>, kTB), gsell = occupancy_grid(k_prx<2>, kTB);
+  std::vector<PrxArgs> xs = xa;  // the SELL halves count their own tickets
+  for (int b = 0; b < nb; ++b) xs[(size_t)b].head = heads + nb + b;
+  // pass = the long rows (chunks, walkers, walked rows) then the SELL slices
+  // split the pass when the long rows carry little of the work (uniform rmat25:
+  // 106 -> 129 GTEPS); with skew they overlap the SELL slices inside one
+  // launch and splitting them serialises the two (rmat24: 213 -> 173)
+  static const int split_env = [] {
+    const char *e = std::getenv("SG_PR_SPLIT");
+    return e ? std::atoi(e) : -1;
+  }();
+  int64_t long_edges = 0, all_edges = 0;
+  for (int b = 0; b < nb; ++b) {
+    const ExactLayout &L = nb > 1 ? g.tile_exact(S, hs, b) : g.exact(hs);
+    long_edges += L.big_edges, all_edges += L.big_edges + L.sell_edges;
+  }
+  const bool split_pass =
+      split_env >= 0 ? split_env != 0 : long_edges * 4 < std::max<int64_t>(all_edges, 1);
+  auto pass = [=](Launcher &L, cudaStream_t s, const char *name, int gain) {
+    for (int b = 0; b < nb && !split_pass; ++b) {  // one launch over every ticket
+      PrxArgs x = xa[(size_t)b];
+      x.gain = gain;
+      L.go(name, k_prx<0>, gx, kTB, s, x, fold);
+    }
+    for (int b = 0; b < nb && split_pass; ++b) {
+      PrxArgs x = xa[(size_t)b], y = xs[(size_t)b];
+      x.gain = y.gain = gain;
+      if (x.nchunks + x.nsplit + x.nself) L.go(name, k_prx<1>, gbig, kTB, s, x, fold);
+      if (y.ngroups) L.go(name, k_prx<2>, gsell, kTB, s, y, fold);
+    }
+  };
   P.init = [=](Launcher &L, cudaStream_t s) {
     L.go("init", k_ctl_init, 1, 1, s, ctl, 1, (uint32_t)nv);
     L.go("init", k_pr_init, grid_n(nv), 256, s, csr_off, nv, omd, inv, labels_d, aux0);
     L.go("init", k_copy_f64, grid_n(nv), 256, s, (const double *)aux0, nv, aux1);
     fill<unsigned long long>(L, gmax, 1, 0ull, s);
-    fill<uint32_t>(L, heads, nb, 0u, s);
+    fill<uint32_t>(L, heads, 2 * nb, 0u, s);
     // the reference's bins of the full CSC, for the round log (schedulers.py:144-167)
     L.go("init", k_static_bins, grid_n(nv), 256, s, voff, 0u, (uint32_t)nv, thr, largeq, hugeq,
          ctl, cuts);
@@ -358,13 +390,8 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
       }
     }
     // eps_stop's gain (apps.py:163-171): one exact pass with aux = inv_outdeg
-    if (ne)
-      for (int b = 0; b < nb; ++b) {
-        PrxArgs x = xa[(size_t)b];
-        x.gain = 1;
-        L.go("pr_gain", k_prx, gx, kTB, s, x, fold);
-      }
-    fill<uint32_t>(L, heads, nb, 0u, s);
+    if (ne) pass(L, s, "pr_gain", 1);
+    fill<uint32_t>(L, heads, 2 * nb, 0u, s);
     for (int b = 0; b < nb; ++b) {  // round 0's binades (aux0 = (1-d) * inv_outdeg)
       const PrxArgs &x = xa[(size_t)b];
       if (x.nsplit) {
@@ -389,11 +416,11 @@ void prep_pr(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double *labe
     };
   } else {
     P.round = [=](RoundCtx &c) {
-      for (int b = 0; b < nb; ++b) c.L.go("pr_pull", k_prx, gx, kTB, c.s, xa[(size_t)b], fold);
+      pass(c.L, c.s, "pr_pull", 0);
       PrStop st = stop;
       st.cond = c.cond, st.use_cond = c.use_cond;
       c.L.go("pr_finish", k_prx_finish, 1, 32, c.s, ctl, stats, (uint32_t)nv, st, cuts.D, heads,
-             nb);
+             2 * nb);
     };
   }
   P.finish = [](Launcher &, cudaStream_t) {};

@@ -1037,7 +1037,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
                           keep.emplace_back(new DBuf<char>(bytes));
                           return (void *)keep.back()->p;
                         });
-  const int gx = occupancy_grid(k_prx, kTB);
+  const int gx = occupancy_grid(k_prx<0>, kTB);
   const int64_t limit = std::min<int64_t>(max_rounds, rb.stats_cap);
   Launcher L;
   WhileGraph W;
@@ -1046,7 +1046,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
     // acc = {twc launches, lb launches, nhuge, huge_edges, nlarge, large_edges}, then
     // acc[6] = max |delta| bits, acc[7] = comm_broadcast -- summed / maxed over ranks
     PrStop st2{gmax.p, d, p.tol, g.part.full_ne, limit, max_rounds, cond, 1, 1, 2, acc.p};
-    L.go("pr_pull", k_prx, gx, kTB, s, xa, fold);
+    L.go("pr_pull", k_prx<0>, gx, kTB, s, xa, fold);
     L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
     // round r writes aux1 when r is even, aux0 when odd (PrFold)
     L.go("peer_rows", k_px_rows<double>, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
@@ -1081,7 +1081,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
   if (v.ne) {  // gain: exact sums of this rank's rows
     PrxArgs xg = xa;
     xg.gain = 1;
-    L.go("pr_gain", k_prx, gx, kTB, s, xg, fold);
+    L.go("pr_gain", k_prx<0>, gx, kTB, s, xg, fold);
   }
   // ... then the maximum over ranks (eps_stop, apps.py:164-171)
   L.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)nullptr,

@@ -347,10 +347,20 @@ __device__ __forceinline__ void sell_slice(const PrxArgs &a, PrFold &op, uint32_
   if (v != ExactLayout::kEmpty) row_end(a, op, v, f, acc);
 }
 
+#ifndef SG_PRX_SELL_MINB
+#define SG_PRX_SELL_MINB 4  // the SELL-only pass (register cap 64; 6 CTAs / 40 regs measured -3 %)
+#endif
 #ifndef SG_PRX_MINB
 #define SG_PRX_MINB 1  // min resident CTAs per SM (register cap) for k_prx
 #endif
-__global__ void __launch_bounds__(kTB, SG_PRX_MINB) k_prx(PrxArgs a, PrFold op) {
+// PART 0: every ticket (huge-row chunks, walkers, long rows, SELL groups);
+// PART 1: the long rows only; PART 2: the SELL groups only.  The single-device
+// pr splits a pass into PART 1 + PART 2: the SELL code alone needs a third of
+// the registers, so its launch keeps ~3x the warps in flight (the short rows'
+// gathers are latency-bound: ncu on uniform rmat25, 107 registers = 2 CTAs/SM)
+template <int PART>
+__global__ void __launch_bounds__(kTB, PART == 2 ? SG_PRX_SELL_MINB : SG_PRX_MINB)
+    k_prx(PrxArgs a, PrFold op) {
   __shared__ double redd[kWarpsTB];
   __shared__ unsigned long long redb[kWarpsTB];
   Ctl *ctl = a.ctl;
@@ -361,13 +371,16 @@ __global__ void __launch_bounds__(kTB, SG_PRX_MINB) k_prx(PrxArgs a, PrFold op) 
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   unsigned long long proc = 0;
   const uint32_t n1 = a.nchunks, n2 = n1 + a.nsplit, n3 = n2 + a.nself;
-  const uint32_t ntick = n3 + a.ngroups;
+  const uint32_t ntick = PART == 2 ? a.ngroups : n3 + (PART == 1 ? 0u : a.ngroups);
   for (;;) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(a.head, 1u);
     t = __shfl_sync(kFull, t, 0);
     if (t >= ntick) break;
-    if (t < n1) {
+    if (PART == 2) {
+      const uint32_t g0 = a.gfirst[t], g1 = a.gfirst[t + 1];
+      for (uint32_t s = g0; s < g1; ++s) sell_slice(a, op, s, proc);
+    } else if (t < n1) {
       split_chunk(a, op, t, stamp, proc);
     } else if (t < n2) {
       split_walk(a, op, t - n1, stamp, proc);
@@ -398,6 +411,7 @@ __global__ void __launch_bounds__(kTB, SG_PRX_MINB) k_prx(PrxArgs a, PrFold op) 
   if (a.cta_edges && lane == 0 && pc && round < a.cta_rounds && !a.gain)
     atomicAdd(a.cta_edges + (size_t)round * a.cta_g + (sm_id() % a.cta_g), pc);
 }
+
 
 // first pass over a view (no previous binades): guesses from an approximate
 // prefix of the chunk sums of every huge row (any order: only the exponent matters)
