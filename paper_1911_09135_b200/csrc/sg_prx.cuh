@@ -247,20 +247,35 @@ __device__ __forceinline__ void split_walk(const PrxArgs &a, PrFold &op, uint32_
   const int64_t s0 = a.off[v], d = a.off[v + 1] - s0;
   double s = row_start(a, v, f);
   const uint32_t lane = lane_id();
-  for (uint32_t base = c0; base < c1; base += 32) {
-    const uint32_t j = base + lane;
-    long long T = 0;
-    uint32_t meta = 0;
-    int g = kNoGuess;
+  // lane l holds chunk base + l of the current batch; the next batch's
+  // results are loaded while this one is folded (a dependent load per batch
+  // was the walker's critical path on heavy-skew hub rows)
+  auto fetch = [&](uint32_t b, long long &T, uint32_t &meta, int &g) {
+    const uint32_t j = b + lane;
+    T = 0, meta = 0, g = kNoGuess;
     if (j < c1) {
-      for (;;) {
-        meta = ld_acquire_u32(a.ck_meta + j);
-        if ((meta >> 2) == stamp) break;
-        __nanosleep(100);
-      }
+      meta = ld_acquire_u32(a.ck_meta + j);  // then T / g: ordered after it
       T = __ldcg(a.ck_T + j);
       g = __ldcg(a.ck_guess + j);
     }
+  };
+  long long T;
+  uint32_t meta;
+  int g;
+  fetch(c0, T, meta, g);
+  for (uint32_t base = c0; base < c1; base += 32) {
+    const uint32_t j = base + lane;
+    if (j < c1)
+      while ((meta >> 2) != stamp) {  // not this pass's result yet: wait, reload
+        __nanosleep(100);
+        meta = ld_acquire_u32(a.ck_meta + j);
+        T = __ldcg(a.ck_T + j);
+        g = __ldcg(a.ck_guess + j);
+      }
+    long long Tn = 0;
+    uint32_t mn = 0;
+    int gn = kNoGuess;
+    if (base + 32 < c1) fetch(base + 32, Tn, mn, gn);
     const uint32_t m = min(32u, c1 - base);
     uint32_t tt = 0;
     while (tt < m) {
@@ -309,6 +324,7 @@ __device__ __forceinline__ void split_walk(const PrxArgs &a, PrFold &op, uint32_
       }
       ++tt;
     }
+    T = Tn, meta = mn, g = gn;
   }
   if (lane == 0) row_end(a, op, v, f, s);
   (void)proc;
