@@ -470,6 +470,136 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
   cta_flush(a, my_proc, ctl->round);
 }
 
+// ---- CTA bin with the adjacency staged through shared memory.  Each lane
+// issues cp.async copies of its slots' column ids (and u32 weights) for the
+// step kStage - 1 ahead into a per-warp ring, so kStage - 1 steps of
+// adjacency are in flight without holding registers (the register-prefetch
+// loop above keeps one step); the gathers and reductions of a step read the
+// staged ids.  SG_LARGE_STAGE selects it (bm_round); measured in profiles/.
+#ifndef SG_STAGE_DEPTH
+#define SG_STAGE_DEPTH 3
+#endif
+constexpr int kStage = SG_STAGE_DEPTH;
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pred) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int n = pred ? 4 : 0;  // src-size 0: zero-fill, no global access
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_large_staged(PushArgs a, Op op) {
+  pdl_wait();
+  pdl_trigger();
+  using L = typename Op::L;
+  using W = typename Op::W;
+  constexpr bool kW32 = std::is_same<W, uint32_t>::value && !std::is_same<Op, BmBfs>::value;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  if (a.prefix_in_large && blockIdx.x == 0 && ctl->nhuge) huge_prefix_cta(a, op);
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  unsigned long long my_proc = 0;
+  __shared__ int64_t bstart[kBatch];
+  __shared__ long long bexcl[kBatch + 1];
+  __shared__ L bsv[kBatch];
+  __shared__ uint32_t bhead;
+  __shared__ uint32_t scol[kWarpsTB][kStage][kPV][32];
+  __shared__ uint32_t sw[kW32 ? kWarpsTB : 1][kStage][kPV][32];
+  const uint32_t nb = (n + kBatch - 1) / kBatch;
+  const long long wstep = 32 * kPV, step = (long long)kTB * kPV;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const long long woff = (long long)warp * wstep;
+  const uint32_t *w32 = nullptr;
+  if constexpr (kW32) w32 = op.w32;
+  bool first_grab = true;
+  for (;;) {
+    if (threadIdx.x == 0) bhead = cta_grab(&ctl->large_head, first_grab);
+    __syncthreads();
+    const uint32_t bidx = bhead;
+    if (bidx >= nb) break;
+    if (threadIdx.x < 32) {
+      const uint32_t i = bidx + threadIdx.x * nb;  // degree-mixed batch
+      long long d = 0;
+      if (threadIdx.x < kBatch && i < n) {
+        const uint32_t v = a.largeq[i];
+        const int64_t s = a.off[v];
+        d = a.off[v + 1] - s;
+        bstart[threadIdx.x] = s;
+        bsv[threadIdx.x] = (L)a.largesv[i];
+      }
+      const long long incl = warp_incl_scan(d);
+      if (threadIdx.x < kBatch) bexcl[threadIdx.x + 1] = incl;
+      if (threadIdx.x == 0) bexcl[0] = 0;
+    }
+    __syncthreads();
+    const long long total = bexcl[kBatch];
+    const long long nsteps = (total + step - 1) / step;
+    auto slots = [&](long long b, int64_t (&e)[kPV], bool (&ok)[kPV], L (&sv)[kPV]) {
+      const long long wbase = b + woff;
+      uint32_t lo = 0;
+#pragma unroll
+      for (uint32_t st = kBatch / 2; st; st >>= 1) lo = bexcl[lo + st] <= wbase ? lo + st : lo;
+      const long long x0 = bexcl[lo], x1 = bexcl[lo + 1];
+      const int64_t s0 = bstart[lo], s1 = lo + 1 < kBatch ? bstart[lo + 1] : 0;
+      const L v0 = bsv[lo], v1 = lo + 1 < kBatch ? bsv[lo + 1] : L(0);
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) {
+        const long long slot = wbase + u * 32 + lane;
+        ok[u] = slot < total;
+        const bool second = slot >= x1;
+        e[u] = second ? s1 + (slot - x1) : s0 + (slot - x0);
+        sv[u] = second ? v1 : v0;
+      }
+    };
+    auto stage = [&](long long k) {  // step k's adjacency -> ring slot k % kStage
+      int64_t e[kPV];
+      bool ok[kPV];
+      L sv[kPV];
+      if (k < nsteps) slots(k * step, e, ok, sv);
+      const int r = (int)(k % kStage);
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) {
+        const bool p = k < nsteps && ok[u];
+        cp_async4(&scol[warp][r][u][lane], a.col + (p ? e[u] : 0), p);
+        if constexpr (kW32)
+          if (w32) cp_async4(&sw[warp][r][u][lane], w32 + (p ? e[u] : 0), p);
+      }
+      cp_async_commit();  // one group per step (empty past the end: keeps the count)
+    };
+#pragma unroll
+    for (int k = 0; k < kStage - 1; ++k) stage(k);
+    for (long long k = 0; k < nsteps; ++k) {
+      stage(k + kStage - 1);
+      cp_async_wait<kStage - 1>();  // step k's group has landed (this lane's own copies)
+      int64_t e[kPV];
+      bool ok[kPV];
+      L sv[kPV];
+      slots(k * step, e, ok, sv);
+      const int r = (int)(k % kStage);
+      uint32_t d[kPV];
+      W w[kPV];
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) {
+        d[u] = scol[warp][r][u][lane];
+        if constexpr (kW32) w[u] = w32 ? sw[warp][r][u][lane] : 1u;
+        else w[u] = (W)1;
+      }
+      if (a.cta_edges) my_proc += count_ok(ok);
+      op.apply(d, w, sv, ok);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  cta_flush(a, my_proc, ctl->round);
+}
+
 // Classic TWC CTA bin (Merrill; the reference's twc_kernel maps each large
 // vertex to one CTA, _kernels_py.py:140-146): a CTA takes one vertex at a time
 // and strides over its edges.  Used for the TWC-only ablation
