@@ -470,6 +470,119 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
   cta_flush(a, my_proc, ctl->round);
 }
 
+// ---- CTA bin with 128-bit adjacency loads (SG_LARGE_VEC): lane l takes the
+// kPV = 4 CONSECUTIVE slots 4l..4l+3 of the warp's 128-slot step, so when they
+// lie in one row at a 16-byte aligned offset the column ids (and u32 weights)
+// come in one ld.global.nc.v4 each instead of four scalar loads.
+__device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kTB) k_bm_large_vec(PushArgs a, Op op) {
+  static_assert(kPV == 4, "k_bm_large_vec: four consecutive slots per lane");
+  pdl_wait();
+  pdl_trigger();
+  using L = typename Op::L;
+  using W = typename Op::W;
+  constexpr bool kW32 = std::is_same<W, uint32_t>::value && !std::is_same<Op, BmBfs>::value;
+  Ctl *ctl = a.ctl;
+  if (ctl->done) return;
+  if (a.prefix_in_large && blockIdx.x == 0 && ctl->nhuge) huge_prefix_cta(a, op);
+  const uint32_t n = ctl->nlarge;
+  if (!n) return;
+  op.begin(ctl->round);
+  unsigned long long my_proc = 0;
+  __shared__ int64_t bstart[kBatch];
+  __shared__ long long bexcl[kBatch + 1];
+  __shared__ L bsv[kBatch];
+  __shared__ uint32_t bhead;
+  const uint32_t nb = (n + kBatch - 1) / kBatch;
+  const long long wstep = 32 * kPV, step = (long long)kTB * kPV;
+  const uint32_t lane = threadIdx.x & 31u;
+  const long long woff = (long long)(threadIdx.x >> 5) * wstep;
+  const uint32_t *w32 = nullptr;
+  if constexpr (kW32) w32 = op.w32;
+  bool first_grab = true;
+  for (;;) {
+    if (threadIdx.x == 0) bhead = cta_grab(&ctl->large_head, first_grab);
+    __syncthreads();
+    const uint32_t bidx = bhead;
+    if (bidx >= nb) break;
+    if (threadIdx.x < 32) {
+      const uint32_t i = bidx + threadIdx.x * nb;  // degree-mixed batch
+      long long d = 0;
+      if (threadIdx.x < kBatch && i < n) {
+        const uint32_t v = a.largeq[i];
+        const int64_t s = a.off[v];
+        d = a.off[v + 1] - s;
+        bstart[threadIdx.x] = s;
+        bsv[threadIdx.x] = (L)a.largesv[i];
+      }
+      const long long incl = warp_incl_scan(d);
+      if (threadIdx.x < kBatch) bexcl[threadIdx.x + 1] = incl;
+      if (threadIdx.x == 0) bexcl[0] = 0;
+    }
+    __syncthreads();
+    const long long total = bexcl[kBatch];
+    // lane-contiguous slots: 4 lane + u; a warp step spans <= 2 batch vertices
+    auto fetch = [&](long long b, bool (&ok)[kPV], L (&sv)[kPV], uint32_t (&d)[kPV], W (&w)[kPV]) {
+      const long long wbase = b + woff;
+      uint32_t lo = 0;
+#pragma unroll
+      for (uint32_t st = kBatch / 2; st; st >>= 1) lo = bexcl[lo + st] <= wbase ? lo + st : lo;
+      const long long x0 = bexcl[lo], x1 = bexcl[lo + 1];
+      const int64_t s0 = bstart[lo], s1 = lo + 1 < kBatch ? bstart[lo + 1] : 0;
+      const L v0 = bsv[lo], v1 = lo + 1 < kBatch ? bsv[lo + 1] : L(0);
+      int64_t e[kPV];
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) {
+        const long long slot = wbase + 4 * lane + u;
+        ok[u] = slot < total;
+        const bool second = slot >= x1;
+        e[u] = second ? s1 + (slot - x1) : s0 + (slot - x0);
+        sv[u] = second ? v1 : v0;
+      }
+      if (ok[3] && e[3] == e[0] + 3 && (e[0] & 3) == 0) {  // one row, aligned: 128-bit
+        const uint4 c = ld_stream_v4(a.col + e[0]);
+        d[0] = c.x, d[1] = c.y, d[2] = c.z, d[3] = c.w;
+        if constexpr (kW32) {
+          if (w32) {
+            const uint4 x = ld_stream_v4(w32 + e[0]);
+            w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w;
+          } else {
+            w[0] = w[1] = w[2] = w[3] = 1u;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kPV; ++u) w[u] = (W)1;
+        }
+      } else {
+        op.fetch(a, e, ok, d, w);
+      }
+    };
+    bool ok0[kPV], ok1[kPV];
+    L sv0[kPV], sv1[kPV];
+    uint32_t d0[kPV], d1[kPV];
+    W w0[kPV], w1[kPV];
+    fetch(0, ok0, sv0, d0, w0);
+    for (long long b = 0; b < total; b += step) {
+      const bool more = b + step < total;
+      if (more) fetch(b + step, ok1, sv1, d1, w1);
+      if (a.cta_edges) my_proc += count_ok(ok0);
+      op.apply(d0, w0, sv0, ok0);
+#pragma unroll
+      for (int u = 0; u < kPV; ++u) d0[u] = d1[u], w0[u] = w1[u], sv0[u] = sv1[u], ok0[u] = more && ok1[u];
+    }
+    __syncthreads();
+  }
+  cta_flush(a, my_proc, ctl->round);
+}
+
 // ---- CTA bin with the adjacency staged through shared memory.  Each lane
 // issues cp.async copies of its slots' column ids (and u32 weights) for the
 // step kStage - 1 ahead into a per-warp ring, so kStage - 1 steps of

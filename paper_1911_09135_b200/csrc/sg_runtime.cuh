@@ -603,6 +603,9 @@ void push_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked) {
   }
 }
 
+#ifndef SG_LARGE_VEC
+#define SG_LARGE_VEC 0  // 1: CTA bin with 128-bit adjacency loads (k_bm_large_vec)
+#endif
 #ifndef SG_LARGE_STAGE
 #define SG_LARGE_STAGE 0  // 1: CTA bin with cp.async-staged adjacency (k_bm_large_staged)
 #endif
@@ -642,6 +645,9 @@ void bm_round(RoundCtx &c, const PushArgs &a, const Op &op, bool blocked, bool c
   if (classic)
     c.L.go_pdl("push_large", k_bm_large_classic<Op>, occupancy_grid(k_bm_large_classic<Op>, kTB), kTB,
            c.s, a2, op);
+  else if (SG_LARGE_VEC && !std::is_same<typename Op::W, int64_t>::value)
+    c.L.go_pdl("push_large", k_bm_large_vec<Op>, occupancy_grid(k_bm_large_vec<Op>, kTB), kTB,
+               c.s, a2, op);
   else if (SG_LARGE_STAGE && !std::is_same<typename Op::W, int64_t>::value)
     c.L.go_pdl("push_large", k_bm_large_staged<Op>, occupancy_grid(k_bm_large_staged<Op>, kTB),
                kTB, c.s, a2, op);
