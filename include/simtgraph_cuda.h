@@ -217,7 +217,7 @@ int sg_dist_run_threads(sg_graph *g, const sg_params *p, int32_t world, double *
  * sg_team_run: one BSP run of this rank's partition, the whole loop one
  * CUDA-graph launch; the round's kernels store label updates straight into
  * the owners' / mirrors' regions and synchronise with a device-side barrier
- * (20 s timeout -> SG_ECUDA, the team is then unusable).  p->devices must be
+ * (60 s timeout -> SG_ECUDA, the team is then unusable).  p->devices must be
  * the team size.  labels_out gets the merged labels on every rank, rounds_out
  * the global round log (comm_sent / comm_broadcast as engine.py:105-109,
  * 232-234). */

@@ -39,7 +39,7 @@
 //
 // The whole BSP loop of a rank is ONE CUDA-graph launch (WHILE node): no host
 // round trip and no collective library inside the loop.  The barrier spins
-// on the device with a 20 s timeout (a rank that never arrives fails the run
+// on the device with a 60 s timeout (a rank that never arrives fails the run
 // loudly instead of hanging the GPU).  The same code runs with ranks as host
 // threads on one GPU (peers = plain device pointers), which is how the
 // single-GPU tests drive it.
@@ -129,7 +129,7 @@ __device__ __forceinline__ void red_min_sys(unsigned long long *p, unsigned long
   atomicMin_system(p, v);
 }
 
-constexpr unsigned long long kBarrierNs = 20ull * 1000 * 1000 * 1000;
+constexpr unsigned long long kBarrierNs = 60ull * 1000 * 1000 * 1000;
 
 // Cross-GPU barrier: publish this rank's epoch into every peer's slot
 // (release, system scope, after a system fence for the writes of the
@@ -807,7 +807,7 @@ void finish_run(Team &T, Stream &S, RunBufs &rb, double *labels_d, int64_t nv, c
   SG_CUDA(cudaMemcpy(&hh, T.base, sizeof(Hdr), cudaMemcpyDeviceToHost));
   if (hh.err || h.error == SG_ECUDA) {
     T.poisoned = true;
-    throw Error(SG_ECUDA, std::string("peer barrier timed out: a rank did not arrive within 20 s "
+    throw Error(SG_ECUDA, std::string("peer barrier timed out: a rank did not arrive within 60 s "
                           "(the team is unusable; create a new one)") +
                           (T.host ? "; ranks as threads share one GPU's hardware queues: set "
                                     "CUDA_DEVICE_MAX_CONNECTIONS >= world + 2 before CUDA starts"

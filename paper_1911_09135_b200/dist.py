@@ -168,7 +168,8 @@ def _all_gather_bytes(dist, data: bytes) -> list:
 def make_team(dist, num_vertices: int) -> "native.Team":
     """This rank's symmetric region, connected to every peer's (the IPC
     handles travel through the torch process group)."""
-    team = native.Team(dist.get_rank(), dist.get_world_size(), num_vertices)
+    team = native.Team(dist.get_rank(), dist.get_world_size(), num_vertices,
+                       host_sync=dist.barrier)
     team.connect(_all_gather_bytes(dist, team.handle_bytes))
     dist.barrier()
     return team

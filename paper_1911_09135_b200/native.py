@@ -433,7 +433,12 @@ class Team:
     CUDA IPC handle, the handles are exchanged out of band, and each rank maps
     its peers' regions.  Runs are sg_team_run on this rank's partition."""
 
-    def __init__(self, rank: int, world: int, num_vertices: int):
+    def __init__(self, rank: int, world: int, num_vertices: int, host_sync=None):
+        # host_sync: a collective the ranks run before each sg_team_run (e.g. the
+        # process group's barrier), so no rank's device barrier starts spinning
+        # while a peer is still busy on the host (the device barrier gives up
+        # after 60 s and the team is then unusable)
+        self.host_sync = host_sync
         self._h = ctypes.c_void_p()
         buf = (ctypes.c_uint8 * 64)()
         check(load().sg_team_create(rank, world, num_vertices, ctypes.byref(self._h), buf))
@@ -449,6 +454,8 @@ class Team:
 
     def run(self, part: DevicePartition, params: Params, rounds_cap=1 << 16):
         nv, _, _ = part.info()
+        if self.host_sync is not None:
+            self.host_sync()
         return _run_with_log(
             lambda lab, rounds, n, ms: load().sg_team_run(
                 self._h, part.handle, ctypes.byref(params), ptr(lab), ptr(rounds), len(rounds),
