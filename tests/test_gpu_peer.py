@@ -120,3 +120,19 @@ def test_peer_torchrun_two_processes():
     for app, chk in out["apps"].items():
         assert chk["labels"] and chk["rounds"] and chk["comm_sent"] and chk["comm_broadcast"], \
             (app, chk)
+
+
+def test_nccl_torchrun_world2():
+    """The NCCL transport (sg_dist_run) with two processes, one GPU each --
+    skipped on a one-GPU box (NCCL refuses two ranks on one device)."""
+    from paper_1911_09135_b200 import native
+    if native.device_count() < 2:
+        pytest.skip("needs two GPUs (NCCL: one rank per device)")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29537", str(ROOT / "tests" / "nccl_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    out = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    for app, chk in out["apps"].items():
+        assert all(chk.values()), (app, chk)
