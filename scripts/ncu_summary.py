@@ -29,8 +29,10 @@ METRICS = [
 
 
 def short(name):
-    n = name.split("(")[0]
-    return n.replace("void ", "").replace("sg::", "").replace("<unnamed>::", "")
+    n = name.replace("(int)", "").replace("(bool)", "").split("(")[0]
+    for junk in ("void ", "sg::", "<unnamed>::", "(anonymous namespace)::"):
+        n = n.replace(junk, "")
+    return n
 
 
 def launches(tag):
