@@ -233,7 +233,13 @@ def ncu_traffic(kernel, workload):
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get("dram_bytes_per_launch", {}).get(f"{kernel}|{workload}")
+        key = f"{kernel}|{workload}"
+        b = d.get("dram_bytes_per_launch", {}).get(key)
+        if b is None:
+            return None
+        return {"dram_bytes_per_launch": b,
+                "launches_captured": d.get("launches_captured", {}).get(key),
+                "source": d.get("sources", {}).get(key)}
     except (ValueError, OSError):
         return None
 
@@ -276,10 +282,12 @@ def roofline_of(app, kernels, plog, step_ms, workload):
     n_l, ms_l = kernels[dom]
     achieved = ab[dom] / (ms_l / 1e3) / 1e9
     name = NCU_NAME.get(dom, dom)
+    tr = ncu_traffic(name, workload)
     ke = kernel_edges(plog).get("pull" if dom == "pr_pull" else dom.split("_")[-1], 0)
     return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_kind,
-            "traffic": ncu_traffic(name, workload),
+            "traffic": (tr or {}).get("dram_bytes_per_launch"),
+            "traffic_launches_captured": (tr or {}).get("launches_captured"),
             "algorithmic_bytes_per_launch": ab[dom] / max(n_l, 1),
             "avg_launch_ms": ms_l / max(n_l, 1), "launches": n_l,
             "share_of_step": ms_l / sum(v[1] for v in kernels.values()),
