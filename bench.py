@@ -182,8 +182,17 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def algorithmic_bytes(app, log):
-    """Per-kernel algorithmic bytes from the round log."""
+def algorithmic_bytes(app, log, dense0=False):
+    """Per-kernel algorithmic bytes from the round log.
+    dense0: cc's round 0 ran as the streaming pull k_cc_dense (col 4 B / edge,
+    offsets 16 B / row, label + bitmap 8 B / changed vertex)."""
+    if app == "cc" and dense0 and len(log):
+        rest = algorithmic_bytes(app, log[1:])
+        m0, n0, u0 = (int(log["active_edges"][0]), int(log["frontier_size"][0]),
+                      int(log["updated"][0]))
+        rest["cc_dense"] = 4 * m0 + 16 * n0 + UPDATE_BYTES * u0
+        rest["compact"] = rest.get("compact", 0) + UPDATE_BYTES * u0
+        return rest
     eb = EDGE_BYTES[app]
     n = log["frontier_size"].astype(np.int64)
     m = log["active_edges"].astype(np.int64)
@@ -213,7 +222,7 @@ def kernel_edges(log):
 # profiled-run kernel names -> the CUDA kernels ncu lists
 NCU_NAME = {"push_twc": "k_bm_twc", "push_large": "k_bm_large_pipe", "push_lb": "k_bm_lb",
             "compact": "k_bm_compact", "pull_twc": "k_pull_twc", "pull_large": "k_pull_large",
-            "pull_lb": "k_pull_lb", "pr_pull": "k_prx"}
+            "pull_lb": "k_pull_lb", "pr_pull": "k_prx", "cc_dense": "k_cc_dense"}
 # random 4-byte gathers per second the chip sustains (scripts/micro/gather.cu on
 # B200: 272-275 G/s, one L1TEX wavefront per scattered lane)
 GATHER_CEILING = 272e9
@@ -273,7 +282,7 @@ def label_check(key, labels, log):
 
 def roofline_of(app, kernels, plog, step_ms, workload):
     """Dominant kernel of a profiled run vs the measured HBM peak."""
-    ab = algorithmic_bytes(app, plog)
+    ab = algorithmic_bytes(app, plog, dense0="cc_dense" in kernels)
     timed = {k: v for k, v in kernels.items() if k in ab}
     if not timed:
         return None
@@ -283,7 +292,8 @@ def roofline_of(app, kernels, plog, step_ms, workload):
     achieved = ab[dom] / (ms_l / 1e3) / 1e9
     name = NCU_NAME.get(dom, dom)
     tr = ncu_traffic(name, workload)
-    ke = kernel_edges(plog).get("pull" if dom == "pr_pull" else dom.split("_")[-1], 0)
+    ke = (int(plog["active_edges"][0]) if dom == "cc_dense" else
+          kernel_edges(plog).get("pull" if dom == "pr_pull" else dom.split("_")[-1], 0))
     return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_kind,
             "traffic": (tr or {}).get("dram_bytes_per_launch"),

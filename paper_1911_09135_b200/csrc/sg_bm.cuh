@@ -470,6 +470,92 @@ __global__ void __launch_bounds__(kTB) k_bm_large_pipe(PushArgs a, Op op) {
   cta_flush(a, my_proc, ctl->round);
 }
 
+// ---- cc round 0 as one stream over the edges.  Round 0 of cc has every
+// vertex in the frontier and every label equal to its id (apps.py:114-127),
+// so the round's push relaxations lab[v] = min(lab[v], u) over the
+// symmetrized edges (u, v) are, per row, new[v] = min(v, min of the row's
+// ids): one pass streaming the column ids and their row ids (Graph::sym_src)
+// of the graph in its original numbering -- every edge is read, no label
+// gather, one atomic per row run (results go into the kernel layout through
+// inv).  Changed vertices set their next-frontier bit; the compaction and the
+// advance kernel then close round 0 exactly as after the push kernels (same
+// labels, same round log: frontier V, every edge, the reference's bins).
+namespace {  // non-template kernels: one copy per translation unit
+struct CcDenseArgs {
+  const int64_t *off;   // original-numbering symmetrized rows
+  const uint32_t *col;
+  const uint32_t *src;  // row of every edge (Graph::sym_src)
+  int64_t nv, ne;
+  const uint32_t *inv;  // original -> kernel-layout id (nullptr: the same numbering)
+  uint32_t *lab;        // kernel-layout labels, initialised to the original ids
+  uint32_t *nb;         // next-frontier bitmap (kernel layout)
+  Ctl *ctl;
+  int64_t thr;          // huge threshold (round-log bins)
+};
+constexpr int kDenseV = 8;  // edges per lane in flight
+
+// the edges as one stream (col, src): every warp instruction covers 32
+// consecutive edges; lanes of one row (a contiguous run) take a segmented
+// shuffle minimum, the run's first lane applies it (atomicMin: a row may span
+// several runs) and marks the vertex changed when its minimum beats its id
+__global__ void __launch_bounds__(kTB) k_cc_dense(CcDenseArgs a) {
+  const int64_t W = (int64_t)grid_warps(), step = 32 * kDenseV;
+  const uint32_t lane = lane_id();
+  for (int64_t b = (int64_t)global_warp() * step; b < a.ne; b += W * step) {
+    uint32_t u[kDenseV], r[kDenseV];
+#pragma unroll
+    for (int k = 0; k < kDenseV; ++k) {
+      const int64_t e = b + k * 32 + lane;
+      u[k] = e < a.ne ? ld_stream(a.col + e) : 0xffffffffu;
+      r[k] = e < a.ne ? ld_stream(a.src + e) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int k = 0; k < kDenseV; ++k) {
+      // segmented min over the run of lanes with this lane's row (runs are
+      // contiguous): the run's first lane ends up with the run's minimum
+      uint32_t m = u[k];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_down_sync(kFull, m, d);
+        const uint32_t ry = __shfl_down_sync(kFull, r[k], d);
+        if (lane + d < 32 && ry == r[k]) m = min(m, y);
+      }
+      const uint32_t rp = __shfl_up_sync(kFull, r[k], 1);
+      const bool head = lane == 0 || rp != r[k];
+      if (head && r[k] != 0xffffffffu && m < r[k]) {
+        const uint32_t i = a.inv ? a.inv[r[k]] : r[k];
+        atomicMin(a.lab + i, m);
+        atomicOr(a.nb + (i >> 5), 1u << (i & 31u));
+      }
+    }
+  }
+}
+
+// the round log of the dense round: every row is in the frontier; the
+// reference's bins by degree (schedulers.py:144-167)
+__global__ void __launch_bounds__(kTB) k_cc_dense_bins(CcDenseArgs a) {
+  __shared__ unsigned long long red[32];
+  unsigned long long hedges = 0, ledges = 0, nh = 0, nl = 0;
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.nv; v += st) {
+    const int64_t deg = a.off[v + 1] - a.off[v];
+    const bool huge = deg >= a.thr, large = !huge && deg >= (int64_t)kLarge;
+    nh += huge, nl += large;
+    if (huge) hedges += (unsigned long long)deg;
+    if (large) ledges += (unsigned long long)deg;
+  }
+  unsigned long long x = block_sum(hedges, red);
+  if (threadIdx.x == 0 && x) atomicAdd(&a.ctl->huge_edges, x);
+  x = block_sum(ledges, red);
+  if (threadIdx.x == 0 && x) atomicAdd(&a.ctl->large_edges, x);
+  x = block_sum(nh, red);
+  if (threadIdx.x == 0 && x) atomicAdd(&a.ctl->nhuge, (uint32_t)x);
+  x = block_sum(nl, red);
+  if (threadIdx.x == 0 && x) atomicAdd(&a.ctl->nlarge, (uint32_t)x);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ctl->edges, (unsigned long long)a.ne);
+}
+}  // namespace
+
 // ---- CTA bin with 128-bit adjacency loads (SG_LARGE_VEC): lane l takes the
 // kPV = 4 CONSECUTIVE slots 4l..4l+3 of the warp's 128-slot step, so when they
 // lie in one row at a 16-byte aligned offset the column ids (and u32 weights)

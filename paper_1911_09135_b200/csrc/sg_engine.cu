@@ -10,6 +10,8 @@
 // per round (frontier size, active edges, ... == RoundRecord).
 
 #include <cstdlib>
+#include <cub/device/device_scan.cuh>
+
 #include "sg_runtime.cuh"
 #include "sg_prx.cuh"
 
@@ -141,11 +143,28 @@ namespace {
 
 // old id of every vertex of a relabeled store (nullptr: identity); cc's initial
 // labels are the vertex ids of the reference's numbering (apps.py:121-124)
+// cc's streaming round 0 needs the row id of every symmetrized edge (4 B /
+// edge, cached on the graph): built only when it fits with room to spare
+const uint32_t *maybe_sym_src(Graph &g) {
+  if (g.sym_src_.p) return g.sym_src_.p;
+  if (!g.sym_) return nullptr;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  const size_t need = sizeof(uint32_t) * (size_t)std::max<int64_t>(g.sym_->ne, 1);
+  if (fr < need + need / 2 + ((size_t)2 << 30)) return nullptr;
+  return g.sym_src();
+}
+
 struct Layout {
   const uint32_t *perm = nullptr;  // new -> old
   const uint32_t *inv = nullptr;   // old -> new
   int64_t zout = -1, zsym = -1;    // first id without out-edges (CSR / symmetrized), -1: none known
   int64_t zin = -1;                // first id without in-edges (pull layouts), -1: none known
+  const View *orig_sym = nullptr;  // relabeled cc: the original numbering's symmetrized rows
+  const uint32_t *orig_src = nullptr;  // ... and their edges' row ids
 };
 
 
@@ -244,6 +263,31 @@ void prep_push_min(Program &P, Graph &g, const sg_params &p, RunBufs &rb, double
     if (cc) set_round(BmMin<0>{lab, nullptr, nullptr, snap, nb});
     else if (!weighted) set_round(BmMin<1>{lab, nullptr, nullptr, snap, nb});
     else set_round(BmMin<2>{lab, g.w32.p, nullptr, snap, nb});
+    // cc round 0 as one streaming pull over the original-numbering rows
+    // (k_cc_dense, sg_bm.cuh) when those rows are at hand; SG_CC_DENSE=0: push
+    static const bool cc_dense_env = [] {
+      const char *e = std::getenv("SG_CC_DENSE");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    const View *ov = !cc ? nullptr : lay.perm ? lay.orig_sym : &v;
+    const uint32_t *src0 = !cc || !cc_dense_env || a.sched != 0 ? nullptr
+                           : lay.perm ? lay.orig_src : maybe_sym_src(g);
+    if (cc && ov && src0) {
+      CcDenseArgs ca{ov->off.p, ov->col.p, src0, nv, ov->ne, lay.perm ? lay.inv : nullptr,
+                     lab, nb, ctl, thr};
+      const BmMin<0> op0{lab, nullptr, nullptr, snap, nb};
+      auto base_init = P.init;
+      const int64_t mr = max_rounds;
+      P.init = [=, &rb](Launcher &L, cudaStream_t s) {
+        base_init(L, s);
+        L.go("cc_dense", k_cc_dense_bins, grid_n(nv), kTB, s, ca);
+        L.go("cc_dense", k_cc_dense, occupancy_grid(k_cc_dense, kTB), kTB, s, ca);
+        L.go("compact", k_bm_compact<BmMin<0>>, occupancy_grid(k_bm_compact<BmMin<0>>, kTB), kTB,
+             s, a, op0);
+        L.go("advance", k_push_advance_plain, 1, 32, s, a,
+             Loop{std::min<int64_t>(mr, rb.stats_cap), mr, cudaGraphConditionalHandle{}, 0});
+      };
+    }
     P.unpermuted = P.inv != nullptr;
     P.finish = [=, inv = P.inv, out = P.out](Launcher &L, cudaStream_t s) {
       if (inv) L.go("labels", k_labels_u32_inv, grid_n(nv), 256, s, (const uint32_t *)lab, inv, nv, out);
@@ -747,7 +791,9 @@ void run_app_layout(Graph &g, const sg_params &p, double *labels_out, sg_round *
     q.source = s;
   }
   run_app_on(*R.g, q, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta,
-             Layout{R.perm.p, R.inv.p, R.zout, R.zsym, R.zin});
+             Layout{R.perm.p, R.inv.p, R.zout, R.zsym, R.zin,
+                    p.app == SG_APP_CC && g.sym_ ? g.sym_.get() : nullptr,
+                    p.app == SG_APP_CC ? maybe_sym_src(g) : nullptr});
 }
 
 }  // namespace

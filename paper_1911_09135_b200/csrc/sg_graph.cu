@@ -477,8 +477,27 @@ int64_t Graph::relabel_bytes(bool in_first) const {
   return b;
 }
 
+// src[e] = the row of edge e: one warp per row writes its id over the row
+__global__ void k_row_ids(const int64_t *off, int64_t nv, uint32_t *src) {
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nv; v += warps)
+    for (int64_t e = off[v] + (threadIdx.x & 31); e < off[v + 1]; e += 32) src[e] = (uint32_t)v;
+}
+
+const uint32_t *Graph::sym_src() {
+  if (!sym_src_.p) {
+    const View &s = sym();
+    DBuf<uint32_t> b((size_t)std::max<int64_t>(s.ne, 1));
+    if (s.ne) SG_LAUNCH(k_row_ids, grid_for(s.nv * 32), 256, 0, 0, s.off.p, s.nv, b.p);
+    SG_CUDA(cudaDeviceSynchronize());
+    sym_src_ = std::move(b);
+  }
+  return sym_src_.p;
+}
+
 void Graph::release_views() {
   hot_.clear();
+  sym_src_.release();
   if (is_part()) {  // a partition's view is its data, not a derived layout
     std::lock_guard<std::mutex> lk(exact_mu_);
     exact_.clear();

@@ -101,6 +101,9 @@ struct Graph {
   DBuf<uint32_t> w32; // compact copy used by the sssp kernels when 0 <= w < 2^32
   std::unique_ptr<View> csc_;  // Graph.csc()         (graph.py:95-113), built lazily
   std::unique_ptr<View> sym_;  // Graph.symmetrized() (graph.py:115-128), built lazily
+  // row id of every symmetrized edge (cc's streaming round 0), built lazily
+  DBuf<uint32_t> sym_src_;
+  const uint32_t *sym_src();
   const View &csc();
   const View &sym();
   std::unique_ptr<Tiles> tiles_;  // pr source blocks of the CSC, built lazily per S

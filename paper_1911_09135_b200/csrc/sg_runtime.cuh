@@ -386,9 +386,15 @@ __device__ __forceinline__ void loop_test(Ctl *ctl, uint32_t round, bool empty, 
 }
 
 // round bookkeeping (the parity-paired labels need no commit pass)
+__device__ __forceinline__ void push_advance(const PushArgs &a, const Loop &lp);
 __global__ void k_push_advance(PushArgs a, Loop lp) {
   pdl_wait();
   pdl_trigger();
+  push_advance(a, lp);
+}
+// the same outside the round graph (no programmatic-launch edge to what follows)
+__global__ void k_push_advance_plain(PushArgs a, Loop lp) { push_advance(a, lp); }
+__device__ __forceinline__ void push_advance(const PushArgs &a, const Loop &lp) {
   Ctl *ctl = a.ctl;
   if (threadIdx.x) return;
   if (ctl->done) {
