@@ -494,10 +494,21 @@ struct CcDenseArgs {
 };
 constexpr int kDenseV = 8;  // edges per lane in flight
 
-// the edges as one stream (col, src): every warp instruction covers 32
-// consecutive edges; lanes of one row (a contiguous run) take a segmented
-// shuffle minimum, the run's first lane applies it (atomicMin: a row may span
-// several runs) and marks the vertex changed when its minimum beats its id
+// the edges as one stream (col, src): a warp takes tiles of 32 x kDenseV
+// consecutive edges.  Per instruction, lanes of one row (a contiguous run)
+// reduce with match.any + redux.sync.min and the run's first lane applies the
+// minimum (atomicMin -- a row may continue in other instructions -- and the
+// next-frontier bit when it beats the id).  A hub row spans thousands of
+// instructions: the label is read first (L2) and the atomic skipped when it
+// cannot lower it (a stale read is only ever too high: never a lost update;
+// the bit was set by whoever lowered the label).
+__device__ __forceinline__ void cc_dense_apply(const CcDenseArgs &a, uint32_t r, uint32_t m) {
+  if (r == 0xffffffffu || m >= r) return;
+  const uint32_t i = a.inv ? a.inv[r] : r;
+  if (__ldcg(a.lab + i) <= m) return;
+  atomicMin(a.lab + i, m);
+  atomicOr(a.nb + (i >> 5), 1u << (i & 31u));
+}
 __global__ void __launch_bounds__(kTB) k_cc_dense(CcDenseArgs a) {
   const int64_t W = (int64_t)grid_warps(), step = 32 * kDenseV;
   const uint32_t lane = lane_id();
@@ -511,22 +522,9 @@ __global__ void __launch_bounds__(kTB) k_cc_dense(CcDenseArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < kDenseV; ++k) {
-      // segmented min over the run of lanes with this lane's row (runs are
-      // contiguous): the run's first lane ends up with the run's minimum
-      uint32_t m = u[k];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_down_sync(kFull, m, d);
-        const uint32_t ry = __shfl_down_sync(kFull, r[k], d);
-        if (lane + d < 32 && ry == r[k]) m = min(m, y);
-      }
-      const uint32_t rp = __shfl_up_sync(kFull, r[k], 1);
-      const bool head = lane == 0 || rp != r[k];
-      if (head && r[k] != 0xffffffffu && m < r[k]) {
-        const uint32_t i = a.inv ? a.inv[r[k]] : r[k];
-        atomicMin(a.lab + i, m);
-        atomicOr(a.nb + (i >> 5), 1u << (i & 31u));
-      }
+      const uint32_t grp = __match_any_sync(kFull, r[k]);
+      const uint32_t m = __reduce_min_sync(grp, u[k]);
+      if ((int)lane == __ffs(grp) - 1) cc_dense_apply(a, r[k], m);
     }
   }
 }

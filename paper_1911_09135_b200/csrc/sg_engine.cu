@@ -145,16 +145,22 @@ namespace {
 // labels are the vertex ids of the reference's numbering (apps.py:121-124)
 // cc's streaming round 0 needs the row id of every symmetrized edge (4 B /
 // edge, cached on the graph): built only when it fits with room to spare
+// (a relabeled run also needs the original numbering's symmetrized rows; a
+// graph relabeled before any cc run has not built them yet: build them too
+// when they fit, ~3x their size with the sort's temporaries)
 const uint32_t *maybe_sym_src(Graph &g) {
   if (g.sym_src_.p) return g.sym_src_.p;
-  if (!g.sym_) return nullptr;
+  if (g.is_part()) return nullptr;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  const size_t need = sizeof(uint32_t) * (size_t)std::max<int64_t>(g.sym_->ne, 1);
-  if (fr < need + need / 2 + ((size_t)2 << 30)) return nullptr;
+  const size_t ne2 = (size_t)std::max<int64_t>(2 * g.ne, 1);
+  const size_t src_bytes = sizeof(uint32_t) * ne2;
+  const size_t sym_bytes = g.sym_ ? 0 : 3 * (sizeof(uint32_t) * ne2 + 8 * (size_t)(g.nv + 1));
+  if (fr < src_bytes + src_bytes / 2 + sym_bytes + ((size_t)2 << 30)) return nullptr;
+  g.sym();
   return g.sym_src();
 }
 
@@ -790,10 +796,9 @@ void run_app_layout(Graph &g, const sg_params &p, double *labels_out, sg_round *
     SG_CUDA(cudaMemcpy(&s, R.inv.p + p.source, sizeof(s), cudaMemcpyDeviceToHost));
     q.source = s;
   }
-  run_app_on(*R.g, q, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta,
-             Layout{R.perm.p, R.inv.p, R.zout, R.zsym, R.zin,
-                    p.app == SG_APP_CC && g.sym_ ? g.sym_.get() : nullptr,
-                    p.app == SG_APP_CC ? maybe_sym_src(g) : nullptr});
+  Layout lay{R.perm.p, R.inv.p, R.zout, R.zsym, R.zin};
+  if (p.app == SG_APP_CC && (lay.orig_src = maybe_sym_src(g))) lay.orig_sym = g.sym_.get();
+  run_app_on(*R.g, q, labels_out, rounds_out, cap, nrounds, ms_out, prof, cta, lay);
 }
 
 }  // namespace
