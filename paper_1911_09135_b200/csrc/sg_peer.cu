@@ -20,15 +20,18 @@
 //                  owner's label and red.or into the owner's bitmap, straight
 //                  over NVLink (comm_sent = these marks, exactly the
 //                  reference's `out_d != baseline` pairs, engine.py:105-109);
-//       barrier  — a device-side cross-GPU barrier (release/acquire flags);
+//                  its last block to finish runs the device-side cross-GPU
+//                  barrier (one system fence, relaxed flag stores, acquire
+//                  polls);
 //       compact  — every owner turns its marked rows into the next local
 //                  frontier (+ snapshot labels) and stores each changed
 //                  label into the ranks that hold it as a mirror (its
 //                  mirror mask: only updated mirrors travel,
-//                  comm_broadcast = their count, engine.py:232-234);
-//       publish  — the rank's counter block is stored into every peer's slot;
-//       barrier, advance — every rank sums the slots: round log + the
-//                  device-side quiescence test (all ranks decide alike);
+//                  comm_broadcast = their count, engine.py:232-234); its
+//                  last block publishes the rank's counter block into every
+//                  peer's slot, runs the barrier and advances: every rank
+//                  sums the slots (round log + the device-side quiescence
+//                  test, all ranks decide alike);
 //   * pr: owners fold their CSC rows with the exact-order pull (sg_prx.cuh)
 //     and store the new aux of each row into its mirror holders; max |delta|
 //     and the counters go through the slots, the stop test is the reference's;
@@ -106,8 +109,8 @@ __device__ __forceinline__ Hdr *hdr(const TeamDev &t, int q) {
   return reinterpret_cast<Hdr *>(t.base[q]);
 }
 
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
   unsigned long long v;
@@ -135,24 +138,55 @@ constexpr unsigned long long kBarrierNs = 60ull * 1000 * 1000 * 1000;
 // (release, system scope, after a system fence for the writes of the
 // preceding kernels), then wait until every peer's epoch reached it (acquire).
 // Skipped once the run is done (all ranks decide `done` from the same sums).
-__global__ void k_team_barrier(TeamDev t, Ctl *ctl) {
-  if (threadIdx.x || blockIdx.x) return;
-  if (ctl && ctl->done) return;
+// One system fence, then relaxed flag stores (fence + strong store is the
+// release pattern): st.release.sys carries its own system fence, about 1.4 us
+// each on B200 (scripts/micro/fence.cu), so a store per peer would cost
+// world x 1.4 us per barrier.
+__device__ bool team_barrier_dev(const TeamDev &t, Ctl *ctl) {
   Hdr *me = hdr(t, t.rank);
-  __threadfence_system();
   const unsigned long long e = me->epoch + 1;
   me->epoch = e;
-  for (int q = 0; q < t.world; ++q) st_release_sys(&hdr(t, q)->bar[t.rank], e);
+  __threadfence_system();
+  for (int q = 0; q < t.world; ++q) st_relaxed_sys(&hdr(t, q)->bar[t.rank], e);
   const unsigned long long t0 = globaltimer();
   for (int q = 0; q < t.world; ++q)
     while (ld_acquire_sys(&me->bar[q]) < e) {
       if (globaltimer() - t0 > kBarrierNs) {
         me->err = 1;
         if (ctl) ctl->error = SG_ECUDA, ctl->done = 1;
-        return;
+        return false;
       }
       __nanosleep(40);
     }
+  return true;
+}
+__global__ void k_team_barrier(TeamDev t, Ctl *ctl) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (ctl && ctl->done) return;
+  team_barrier_dev(t, ctl);
+}
+
+// grid of the ticketed exchange kernels: the tickets are same-address atomics
+// (one per block), so the grid stays persistent-sized instead of one thread
+// per word
+inline int ticket_grid(int64_t n, int per_sm) {
+  return std::min(grid_n(n), persistent_grid(per_sm));
+}
+
+// true in every thread of the grid's last block to finish (after all other
+// blocks' writes, device scope); the ticket resets for the next launch.  The
+// exchange kernels end with the barrier / the round's bookkeeping in that
+// block instead of separate single-block launches.
+__device__ __forceinline__ bool last_block(uint32_t *tick) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(tick, 1u) == gridDim.x - 1;
+    if (last) *tick = 0u;
+  }
+  __syncthreads();
+  return last;
 }
 
 // a run that went `done` outside an advance kernel (barrier timeout) leaves the loop
@@ -237,8 +271,8 @@ __global__ void k_px_reduce_slots(TeamDev t, const Ctl *ctl, long long *acc, int
 // ----------------------------------------------------------- push apps --
 // reduce: marked mirrors -> their owners (red.min label, red.or bitmap bit)
 template <class L>
-__global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts cuts,
-                                                   const Ctl *ctl, long long *acc) {
+__global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts cuts, Ctl *ctl,
+                                                   long long *acc, uint32_t *tick) {
   __shared__ unsigned long long red[32];
   if (ctl->done) return;
   const int self = t.rank;
@@ -263,9 +297,81 @@ __global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts c
       atomicOr_system(at<uint32_t>(t, o, lay.o_nb) + (v >> 5), 1u << (v & 31u));
     }
   }
+  if (sent) __threadfence_system();  // only the threads that wrote to peers
   sent = block_sum(sent, red);
   if (threadIdx.x == 0 && sent) atomicAdd((unsigned long long *)&acc[6], sent);
-  __threadfence_system();
+  // every rank's reductions land before any owner compacts
+  if (last_block(tick) && threadIdx.x == 0) team_barrier_dev(t, ctl);
+}
+
+// the round's counter block (k_dp_collect + the next-frontier size; sent and
+// bcast were added by reduce / compact) -> every peer's slot (one thread)
+__device__ void push_publish_dev(const PushArgs &a, const TeamDev &t, long long *acc) {
+  const Ctl *ctl = a.ctl;
+  const long long fs = ctl->dense ? a.dense_n : ctl->fsize;
+  acc[0] = fs;
+  acc[1] = (long long)ctl->edges;
+  acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
+  acc[3] = a.sched >= 2 ? 0 : (long long)ctl->huge_edges;
+  acc[4] = a.sched >= 2 ? 0 : ctl->nlarge;
+  acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
+  acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
+  acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
+  acc[10] = ctl->nsize;
+  const int par = ctl->round & 1;
+  for (int i = 0; i < t.world * kDP; ++i) hdr(t, i / kDP)->cnt[par][t.rank][i % kDP] = acc[i % kDP];
+}
+
+// after the barrier: sum the slots, write the round log, decide quiescence
+// (identically on every rank), reset the round state (one thread)
+__device__ void push_advance_dev(const PushArgs &a, const TeamDev &t, long long *acc,
+                                 const Loop &lp) {
+  Ctl *ctl = a.ctl;
+  const int par = ctl->round & 1;
+  const Hdr *me = hdr(t, t.rank);
+  long long x[kDP];
+  for (int j = 0; j < kDP; ++j) {
+    long long sum = 0;
+    for (int q = 0; q < t.world; ++q) sum += ld_volatile(&me->cnt[par][q][j]);
+    x[j] = sum;
+  }
+  const uint32_t round = ctl->round;
+  RoundStat &s = a.stats[round];
+  s.frontier_size = x[0];
+  s.active_edges = x[1];
+  s.huge_count = x[2];
+  s.huge_edges = x[3];
+  s.large_count = x[4];
+  s.large_edges = x[5];
+  s.updated = x[10];
+  s.comm_sent = x[6];
+  s.comm_broadcast = x[7];
+  s.launches_twc = x[8];
+  s.launches_lb = x[9];
+  ctl->fsize = ctl->nsize;
+  ctl->nsize = 0;
+  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
+  ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
+  ctl->dense = 0;
+  ctl->round = round + 1;
+  for (int j = 0; j < kDP; ++j) acc[j] = 0;
+  loop_test(ctl, round, x[10] == 0, lp);
+}
+
+// the round's tail in the last block of the compaction: publish the counter
+// block, barrier, advance; leaves the WHILE loop when the run is done for any
+// reason (a barrier timeout included)
+__device__ void push_round_tail(const PushArgs &a, const TeamDev &t, long long *acc,
+                                const Loop &lp) {
+  push_publish_dev(a, t, acc);
+  if (team_barrier_dev(t, a.ctl)) push_advance_dev(a, t, acc, lp);
+  else if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+}
+// a compaction launched after the run went done (barrier timeout) only leaves the loop
+__device__ __forceinline__ bool done_exit(const Ctl *ctl, const Loop &lp) {
+  if (!ctl->done) return false;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+  return true;
 }
 
 // compact (after the barrier): owned marked rows -> next local frontier with
@@ -274,11 +380,12 @@ __global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts c
 // l emits slot l, l + 32, ...: a dense hot-set word block is 32 vertices per
 // step, not 32 dependent steps of one lane)
 template <class L>
-__global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts cuts, Ctl *ctl,
+__global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts cuts, PushArgs a,
                                                     const uint32_t *mask, uint32_t *q, L *snap,
-                                                    long long *acc) {
+                                                    long long *acc, uint32_t *tick, Loop lp) {
   __shared__ unsigned long long red[32];
-  if (ctl->done) return;
+  Ctl *ctl = a.ctl;
+  if (done_exit(ctl, lp)) return;
   const int self = t.rank;
   uint32_t *nb = at<uint32_t>(t, self, lay.o_nb);
   const L *lab = at<L>(t, self, lay.o_d[0]);
@@ -324,9 +431,10 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
       }
     }
   }
+  if (bc) __threadfence_system();  // only the threads that wrote to peers
   bc = block_sum(bc, red);
   if (threadIdx.x == 0 && bc) atomicAdd((unsigned long long *)&acc[7], bc);
-  __threadfence_system();
+  if (last_block(tick) && threadIdx.x == 0) push_round_tail(a, t, acc, lp);
 }
 
 // ---- bfs: the visited-bitmap operator (BmBfs) over the peers.  vis (the nb
@@ -335,7 +443,7 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
 // both bitmaps of the mirror holders), so vis & ~prev on a mirror word is
 // exactly what this rank discovered this round (`out_d != baseline`).
 __global__ void __launch_bounds__(256) k_px_bfs_reduce(TeamDev t, Layout lay, Cuts cuts,
-                                                       const Ctl *ctl, long long *acc) {
+                                                       Ctl *ctl, long long *acc, uint32_t *tick) {
   __shared__ unsigned long long red[32];
   if (ctl->done) return;
   const int self = t.rank;
@@ -359,18 +467,22 @@ __global__ void __launch_bounds__(256) k_px_bfs_reduce(TeamDev t, Layout lay, Cu
       atomicOr_system(at<uint32_t>(t, owner_of(cuts, v), lay.o_nb) + (v >> 5), 1u << (v & 31u));
     }
   }
+  if (sent) __threadfence_system();  // only the threads that wrote to peers
   sent = block_sum(sent, red);
   if (threadIdx.x == 0 && sent) atomicAdd((unsigned long long *)&acc[6], sent);
-  __threadfence_system();
+  // every rank's reductions land before any owner compacts
+  if (last_block(tick) && threadIdx.x == 0) team_barrier_dev(t, ctl);
 }
 
 // owners: new owned bits -> next frontier, label round + 1; the vertex is
 // marked visited in both bitmaps of its mirror holders
 __global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, Cuts cuts,
-                                                        Ctl *ctl, const uint32_t *mask,
-                                                        uint32_t *q, long long *acc) {
+                                                        PushArgs a, const uint32_t *mask,
+                                                        uint32_t *q, long long *acc,
+                                                        uint32_t *tick, Loop lp) {
   __shared__ unsigned long long red[32];
-  if (ctl->done) return;
+  Ctl *ctl = a.ctl;
+  if (done_exit(ctl, lp)) return;
   const int self = t.rank;
   const uint32_t *vis = at<uint32_t>(t, self, lay.o_nb);
   uint32_t *prev = at<uint32_t>(t, self, lay.o_prev);
@@ -419,74 +531,10 @@ __global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, C
       }
     }
   }
+  if (bc) __threadfence_system();  // only the threads that wrote to peers
   bc = block_sum(bc, red);
   if (threadIdx.x == 0 && bc) atomicAdd((unsigned long long *)&acc[7], bc);
-  __threadfence_system();
-}
-
-// the round's counter block (k_dp_collect + the next-frontier size; sent and
-// bcast were added by reduce / compact) -> every peer's slot
-__global__ void k_px_push_publish(PushArgs a, TeamDev t, long long *acc) {
-  const Ctl *ctl = a.ctl;
-  if (ctl->done) return;
-  if (threadIdx.x == 0) {
-    const long long fs = ctl->dense ? a.dense_n : ctl->fsize;
-    acc[0] = fs;
-    acc[1] = (long long)ctl->edges;
-    acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
-    acc[3] = a.sched >= 2 ? 0 : (long long)ctl->huge_edges;
-    acc[4] = a.sched >= 2 ? 0 : ctl->nlarge;
-    acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
-    acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
-    acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
-    acc[10] = ctl->nsize;
-  }
-  __syncthreads();
-  const int par = ctl->round & 1;
-  for (int i = threadIdx.x; i < t.world * kDP; i += blockDim.x)
-    hdr(t, i / kDP)->cnt[par][t.rank][i % kDP] = acc[i % kDP];
-  __threadfence_system();
-}
-
-// after the barrier: sum the slots, write the round log, decide quiescence
-// (identically on every rank), reset the round state; leaves the WHILE loop
-// when the run is done for any reason (a barrier timeout included)
-__global__ void k_px_push_advance(PushArgs a, TeamDev t, long long *acc, Loop lp) {
-  Ctl *ctl = a.ctl;
-  if (threadIdx.x) return;
-  if (ctl->done) {
-    if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
-    return;
-  }
-  const int par = ctl->round & 1;
-  const Hdr *me = hdr(t, t.rank);
-  long long x[kDP];
-  for (int j = 0; j < kDP; ++j) {
-    long long sum = 0;
-    for (int q = 0; q < t.world; ++q) sum += ld_volatile(&me->cnt[par][q][j]);
-    x[j] = sum;
-  }
-  const uint32_t round = ctl->round;
-  RoundStat &s = a.stats[round];
-  s.frontier_size = x[0];
-  s.active_edges = x[1];
-  s.huge_count = x[2];
-  s.huge_edges = x[3];
-  s.large_count = x[4];
-  s.large_edges = x[5];
-  s.updated = x[10];
-  s.comm_sent = x[6];
-  s.comm_broadcast = x[7];
-  s.launches_twc = x[8];
-  s.launches_lb = x[9];
-  ctl->fsize = ctl->nsize;
-  ctl->nsize = 0;
-  ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
-  ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
-  ctl->dense = 0;
-  ctl->round = round + 1;
-  for (int j = 0; j < kDP; ++j) acc[j] = 0;
-  loop_test(ctl, round, x[10] == 0, lp);
+  if (last_block(tick) && threadIdx.x == 0) push_round_tail(a, t, acc, lp);
 }
 
 // ------------------------------------------------------------- pr, kcore --
@@ -499,17 +547,19 @@ __global__ void __launch_bounds__(256) k_px_rows(TeamDev t, size_t off0, size_t 
   const size_t off = ((ctl->round & 1) == (uint32_t)parity_sel) ? off0 : off1;
   const T *src = at<T>(t, t.rank, off);
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  bool wrote = false;
   for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += st) {
     uint32_t m = mask[v - lo];
     if (!m) continue;
     const T x = src[v];
+    wrote = true;
     while (m) {
       const int r = __ffs(m) - 1;
       m &= m - 1;
       at<T>(t, r, off)[v] = x;
     }
   }
-  __threadfence_system();
+  if (wrote) __threadfence_system();
 }
 
 // pr: max |delta| and comm_broadcast of this rank join the counter block
@@ -531,16 +581,18 @@ __global__ void k_px_kill(TeamDev t, Layout lay, const Ctl *ctl, const uint32_t 
   if (ctl->done) return;
   const uint32_t nd = ctl->ndying;
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  bool wrote = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += st) {
     const uint32_t v = dying[i];
     uint32_t m = mask[v - lo];
+    wrote |= m != 0;
     while (m) {
       const int r = __ffs(m) - 1;
       m &= m - 1;
       at<uint8_t>(t, r, lay.o_d[0])[v] = 0;
     }
   }
-  __threadfence_system();
+  if (wrote) __threadfence_system();
 }
 
 // kcore mark phase over the peers: a neighbour of a dying vertex gets the
@@ -750,17 +802,30 @@ MirrorInfo &mirrors(Team &T, Graph &g, cudaStream_t s) {
   return *mi;
 }
 
-// the run's loop as one WHILE node (body captured on s)
+// the run's loop as one WHILE node (body captured on s).  SG_PEER_EAGER=1
+// (profiling only: ncu does not see kernels inside conditional nodes) runs
+// the body from a host loop instead, one stream sync per round.
 struct WhileGraph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   size_t nodes = 0;
+  const bool eager = [] {
+    const char *e = std::getenv("SG_PEER_EAGER");
+    return e && std::atoi(e) != 0;
+  }();
+  const int uc = eager ? 0 : 1;  // Loop::use_cond of the body's kernels
+  std::function<void(cudaGraphConditionalHandle)> body_;
   ~WhileGraph() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
   }
   template <class Body>
   void build(cudaStream_t s, Body &&body) {
+    if (eager) {
+      body_ = body;
+      nodes = 0;
+      return;
+    }
     SG_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle cond;
     SG_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
@@ -784,6 +849,19 @@ struct WhileGraph {
     SG_CUDA(cudaStreamEndCapture(s, &b));
     SG_CUDA(cudaGraphGetNodes(b, nullptr, &nodes));
     SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  void launch(cudaStream_t s, const Ctl *ctl) {
+    if (!eager) {
+      SG_CUDA(cudaGraphLaunch(exec, s));
+      return;
+    }
+    for (;;) {
+      body_(cudaGraphConditionalHandle{});
+      int32_t done = 0;
+      SG_CUDA(cudaMemcpyAsync(&done, &ctl->done, sizeof(done), cudaMemcpyDeviceToHost, s));
+      SG_CUDA(cudaStreamSynchronize(s));
+      if (done) break;
+    }
   }
 };
 
@@ -858,6 +936,7 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   uint32_t *nb = reinterpret_cast<uint32_t *>(T.base + T.lay.o_nb);
   DBuf<L> snap(std::max<int64_t>(hi - lo, 1));
   DBuf<long long> acc(kSlot), tsum((nv + kFT - 1) / kFT + 1);
+  DBuf<uint32_t> tick(2);  // last-block tickets of reduce / compact
   DBuf<double> out(std::max<int64_t>(nv, 1));
   const bool weighted = p.app == SG_APP_SSSP && g.weighted;
   const Op op{lab, KIND == 2 ? g.w32.p : nullptr, KIND == 3 && weighted ? g.w64.p : nullptr,
@@ -875,22 +954,20 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   Launcher Lc;
   WhileGraph W;
   W.build(s, [&](cudaGraphConditionalHandle cond) {
-    const Loop lp{limit, max_rounds, cond, 1};
-    RoundCtx c{Lc, s, cond, 1};
+    const Loop lp{limit, max_rounds, cond, W.uc};
+    RoundCtx c{Lc, s, cond, W.uc};
     bm_round(c, a, op, p.blocked != 0, classic, tsum.p, /*compact=*/false);
-    Lc.go("peer_reduce", k_px_reduce<L>, grid_n((int64_t)T.lay.nw), 256, s, td, T.lay, cuts,
-          (const Ctl *)ctl, acc.p);
-    Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    Lc.go("peer_compact", k_px_compact<L>, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
-          T.lay, cuts, ctl, (const uint32_t *)mi.mask.p, rb.q0.p, snap.p, acc.p);
-    Lc.go("peer_publish", k_px_push_publish, 1, 256, s, a, td, acc.p);
-    Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    Lc.go("advance", k_px_push_advance, 1, 32, s, a, td, acc.p, lp);
+    // reduce (+ barrier in its last block), compact (+ publish, barrier, advance)
+    Lc.go("peer_reduce", k_px_reduce<L>, ticket_grid((int64_t)T.lay.nw, 4), 256, s, td, T.lay, cuts,
+          ctl, acc.p, tick.p);
+    Lc.go("peer_compact", k_px_compact<L>, ticket_grid(std::max<int64_t>(hi - lo, 1), 8), 256, s, td,
+          T.lay, cuts, a, (const uint32_t *)mi.mask.p, rb.q0.p, snap.p, acc.p, tick.p + 1, lp);
   });
   SG_CUDA(cudaEventRecord(S.e0, s));
   Lc.go("init", k_ctl_init, 1, 1, s, ctl, (int32_t)cc, cc ? hi - lo : (owns_src ? 1u : 0u));
   fill<uint32_t>(Lc, nb, (int64_t)T.lay.nw, 0u, s);
   fill<long long>(Lc, acc.p, kSlot, 0ll, s);
+  fill<uint32_t>(Lc, tick.p, 2, 0u, s);
   if (cc && inv) {  // relabeled: a vertex's label is its original id (perm)
     Lc.go("init", k_copy_as<L>, grid_n(nv), 256, s, (const uint32_t *)g.part.perm.p, nv, lab);
     Lc.go("init", k_copy_as<L>, grid_n(hi - lo), 256, s, (const uint32_t *)g.part.perm.p + lo,
@@ -907,7 +984,7 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
     }
   }
   barrier(T, s);  // every region initialised before any peer writes into it
-  SG_CUDA(cudaGraphLaunch(W.exec, s));
+  W.launch(s, ctl);
   barrier(T, s);
   if (sizeof(L) == 4)
     k_px_gather<uint32_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv, out.p,
@@ -944,6 +1021,7 @@ void run_peer_bfs(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t ma
   uint32_t *vis = reinterpret_cast<uint32_t *>(T.base + T.lay.o_nb);
   uint32_t *prev = reinterpret_cast<uint32_t *>(T.base + T.lay.o_prev);
   DBuf<long long> acc(kSlot), tsum((nv + kFT - 1) / kFT + 1);
+  DBuf<uint32_t> tick(2);  // last-block tickets of reduce / compact
   DBuf<double> out(std::max<int64_t>(nv, 1));
   int64_t src = p.source;
   if (inv) {
@@ -960,23 +1038,21 @@ void run_peer_bfs(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t ma
   Launcher Lc;
   WhileGraph W;
   W.build(s, [&](cudaGraphConditionalHandle cond) {
-    const Loop lp{limit, max_rounds, cond, 1};
-    RoundCtx c{Lc, s, cond, 1};
+    const Loop lp{limit, max_rounds, cond, W.uc};
+    RoundCtx c{Lc, s, cond, W.uc};
     bm_round(c, a, op, p.blocked != 0, classic, tsum.p, /*compact=*/false);
-    Lc.go("peer_reduce", k_px_bfs_reduce, grid_n((int64_t)T.lay.nw), 256, s, td, T.lay, cuts,
-          (const Ctl *)ctl, acc.p);
-    Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    Lc.go("peer_compact", k_px_bfs_compact, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
-          T.lay, cuts, ctl, (const uint32_t *)mi.mask.p, rb.q0.p, acc.p);
-    Lc.go("peer_publish", k_px_push_publish, 1, 256, s, a, td, acc.p);
-    Lc.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    Lc.go("advance", k_px_push_advance, 1, 32, s, a, td, acc.p, lp);
+    // reduce (+ barrier in its last block), compact (+ publish, barrier, advance)
+    Lc.go("peer_reduce", k_px_bfs_reduce, ticket_grid((int64_t)T.lay.nw, 4), 256, s, td, T.lay, cuts,
+          ctl, acc.p, tick.p);
+    Lc.go("peer_compact", k_px_bfs_compact, ticket_grid(std::max<int64_t>(hi - lo, 1), 8), 256, s, td,
+          T.lay, cuts, a, (const uint32_t *)mi.mask.p, rb.q0.p, acc.p, tick.p + 1, lp);
   });
   SG_CUDA(cudaEventRecord(S.e0, s));
   Lc.go("init", k_ctl_init, 1, 1, s, ctl, 0, owns_src ? 1u : 0u);
   fill<uint32_t>(Lc, vis, (int64_t)T.lay.nw, 0u, s);
   fill<uint32_t>(Lc, prev, (int64_t)T.lay.nw, 0u, s);
   fill<long long>(Lc, acc.p, kSlot, 0ll, s);
+  fill<uint32_t>(Lc, tick.p, 2, 0u, s);
   fill<uint32_t>(Lc, lab, nv, kInf32, s);
   // every rank knows the source is visited (its label 0 is final)
   Lc.go("init", k_set1<uint32_t>, 1, 1, s, lab, src, 0u);
@@ -984,7 +1060,7 @@ void run_peer_bfs(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t ma
   Lc.go("init", k_set1<uint32_t>, 1, 1, s, prev, src >> 5, 1u << (src & 31));
   if (owns_src) Lc.go("init", k_set1<uint32_t>, 1, 1, s, rb.q0.p, (int64_t)0, (uint32_t)src);
   barrier(T, s);
-  SG_CUDA(cudaGraphLaunch(W.exec, s));
+  W.launch(s, ctl);
   barrier(T, s);
   k_px_gather<uint32_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv, out.p,
                                                    ConvU32{});
@@ -1042,10 +1118,10 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
   Launcher L;
   WhileGraph W;
   W.build(s, [&](cudaGraphConditionalHandle cond) {
-    const Loop lp{limit, max_rounds, cond, 1};
+    const Loop lp{limit, max_rounds, cond, W.uc};
     // acc = {twc launches, lb launches, nhuge, huge_edges, nlarge, large_edges}, then
     // acc[6] = max |delta| bits, acc[7] = comm_broadcast -- summed / maxed over ranks
-    PrStop st2{gmax.p, d, p.tol, g.part.full_ne, limit, max_rounds, cond, 1, 1, 2, acc.p};
+    PrStop st2{gmax.p, d, p.tol, g.part.full_ne, limit, max_rounds, cond, W.uc, 1, 2, acc.p};
     L.go("pr_pull", k_prx<0>, gx, kTB, s, xa, fold);
     L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
     // round r writes aux1 when r is even, aux0 when odd (PrFold)
@@ -1098,7 +1174,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
   L.go("init", k_static_bins, grid_n(hi - lo), 256, s, v.off.p, lo, hi - lo, thr, rb.largeq.p,
        rb.hugeq.p, ctl, one);
   barrier(T, s);  // gain slots read everywhere, every region initialised
-  SG_CUDA(cudaGraphLaunch(W.exec, s));
+  W.launch(s, ctl);
   barrier(T, s);
   k_px_gather<double><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[2], cuts, nv, pinv, out.p,
                                                   ConvF64{});
@@ -1143,8 +1219,8 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
   Launcher L;
   WhileGraph W;
   W.build(s, [&](cudaGraphConditionalHandle cond) {
-    const Loop lp{limit, max_rounds, cond, 1};
-    RoundCtx c{L, s, cond, 1};
+    const Loop lp{limit, max_rounds, cond, W.uc};
+    RoundCtx c{L, s, cond, W.uc};
     pull_round(c, a, op, p.blocked != 0, hcnt.p, classic);
     if (thr != kNoHuge)
       L.go("kcore_huge", k_pull_finish<KcOp, false>, 1, 1024, s, a, op, hcnt.p, PrStop{});
@@ -1177,7 +1253,7 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
   fill<uint32_t>(L, hcnt.p, nv, 0u, s);
   fill<long long>(L, acc.p, kSlot, 0ll, s);
   barrier(T, s);
-  SG_CUDA(cudaGraphLaunch(W.exec, s));
+  W.launch(s, ctl);
   barrier(T, s);
   k_px_gather<uint8_t><<<grid_n(nv), 256, 0, s>>>(td, T.lay.o_d[0], cuts, nv, inv, out.p,
                                                    ConvAlive{});
@@ -1191,7 +1267,30 @@ int part_kind_of(int app) {
   return app == SG_APP_PR ? 1 : (app == SG_APP_CC || app == SG_APP_KCORE) ? 2 : 0;
 }
 
+// Load the kernels a rank launches right after passing a barrier before any
+// team runs: under lazy module loading a first launch may wait on the device,
+// where a peer's barrier kernel spins until this rank arrives (seen as a
+// cold-process barrier timeout with ranks as threads on one GPU).  The
+// round kernels are loaded when the run's graph is instantiated.
+void preload_peer_kernels() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncAttributes fa;
+    const void *ks[] = {
+        (const void *)k_team_barrier,
+        (const void *)k_px_held,
+        (const void *)k_px_mask,
+        (const void *)k_px_gather<uint32_t, ConvU32>,
+        (const void *)k_px_gather<unsigned long long, ConvF64Bits>,
+        (const void *)k_px_gather<double, ConvF64>,
+        (const void *)k_px_gather<uint8_t, ConvAlive>,
+    };
+    for (const void *k : ks) SG_CUDA(cudaFuncGetAttributes(&fa, k));
+  });
+}
+
 void team_run(Team &T, Graph &g, const sg_params &p, const Out &o) {
+  preload_peer_kernels();
   if (!T.connected) throw Error(SG_ECONFIG, "team not connected (sg_team_connect)");
   if (T.poisoned) throw Error(SG_ECUDA, "team unusable after a barrier timeout");
   if (!g.is_part()) throw Error(SG_ECONFIG, "sg_team_run needs an edge-cut partition (sg_graph_partition)");
@@ -1493,6 +1592,7 @@ void run_peer_threads(Graph &g, const sg_params &p, int world, const Out &o) {
     T->connected = true;
     T->host = &hb;
   }
+  preload_peer_kernels();
   SG_CUDA(cudaDeviceSynchronize());
   std::vector<std::string> err(world);
   std::vector<int> code(world, SG_OK);
