@@ -93,6 +93,10 @@ struct Graph {
     // old id, inv: old -> new (all V vertices, every rank holds both)
     bool relabeled = false;
     DBuf<uint32_t> perm, inv;
+    // push / symmetrized relabel: the block's vertices without rows in the
+    // view are numbered last, [zlo, hi) -- the compaction counts them instead
+    // of queueing them (as the single-device store's edgeless tail)
+    int64_t zlo = -1;
   } part;
   bool is_part() const { return part.kind >= 0; }
   bool weighted = false;

@@ -212,6 +212,19 @@ __device__ __forceinline__ uint32_t owned_bits(int64_t w, int64_t lo, int64_t hi
 }
 
 // ------------------------------------------------------- mirror masks --
+// ranks holding an owned vertex as a mirror: a bit per owned vertex (any
+// holder) in front of the 4-byte rank mask, so the exchange kernels read the
+// mask only for the vertices that have mirrors
+struct Mirrors {
+  const uint32_t *any;   // by global bitmap word: any[v / 32 - lo / 32] bit v % 32
+  const uint32_t *mask;  // [hi - lo]
+  int64_t lo;
+  __device__ __forceinline__ uint32_t word(int64_t w) const { return any[w - (lo >> 5)]; }
+  __device__ __forceinline__ uint32_t of(uint32_t v) const {
+    return (word(v >> 5) >> (v & 31u)) & 1u ? mask[v - lo] : 0u;
+  }
+};
+
 // setup 1: the vertices this rank's rows point at but does not own (its mirrors)
 __global__ void k_px_held(const uint32_t *col, int64_t ne, int64_t lo, int64_t hi,
                           uint32_t *held) {
@@ -227,7 +240,7 @@ __global__ void k_px_held(const uint32_t *col, int64_t ne, int64_t lo, int64_t h
 // setup 2 (after a barrier): mask[v - lo] = ranks holding owned v as a mirror,
 // mcount[v] = their number (engine.py:84 mirror_count)
 __global__ void k_px_mask(TeamDev t, Layout lay, int64_t lo, int64_t hi, uint32_t *mask,
-                          uint32_t *mcount) {
+                          uint32_t *any, uint32_t *mcount) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += st) {
     uint32_t m = 0;
@@ -237,6 +250,7 @@ __global__ void k_px_mask(TeamDev t, Layout lay, int64_t lo, int64_t hi, uint32_
       if ((w >> (v & 31)) & 1u) m |= 1u << q;
     }
     mask[v - lo] = m;
+    if (m) atomicOr(any + ((v >> 5) - (lo >> 5)), 1u << (v & 31));
     mcount[v] = (uint32_t)__popc(m);
   }
 }
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts c
 // bcast were added by reduce / compact) -> every peer's slot (one thread)
 __device__ void push_publish_dev(const PushArgs &a, const TeamDev &t, long long *acc) {
   const Ctl *ctl = a.ctl;
-  const long long fs = ctl->dense ? a.dense_n : ctl->fsize;
+  const long long fs = ctl->dense ? a.dense_n : (long long)ctl->fsize + ctl->fzero;
   acc[0] = fs;
   acc[1] = (long long)ctl->edges;
   acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
@@ -317,7 +331,7 @@ __device__ void push_publish_dev(const PushArgs &a, const TeamDev &t, long long 
   acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
   acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
   acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
-  acc[10] = ctl->nsize;
+  acc[10] = (long long)ctl->nsize + ctl->nzero;
   const int par = ctl->round & 1;
   for (int i = 0; i < t.world * kDP; ++i) hdr(t, i / kDP)->cnt[par][t.rank][i % kDP] = acc[i % kDP];
 }
@@ -349,7 +363,8 @@ __device__ void push_advance_dev(const PushArgs &a, const TeamDev &t, long long 
   s.launches_twc = x[8];
   s.launches_lb = x[9];
   ctl->fsize = ctl->nsize;
-  ctl->nsize = 0;
+  ctl->fzero = ctl->nzero;
+  ctl->nsize = ctl->nzero = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
   ctl->edges = ctl->huge_edges = ctl->large_edges = 0;
   ctl->dense = 0;
@@ -381,8 +396,9 @@ __device__ __forceinline__ bool done_exit(const Ctl *ctl, const Loop &lp) {
 // step, not 32 dependent steps of one lane)
 template <class L>
 __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts cuts, PushArgs a,
-                                                    const uint32_t *mask, uint32_t *q, L *snap,
-                                                    long long *acc, uint32_t *tick, Loop lp) {
+                                                    Mirrors mm, uint32_t *q, L *snap,
+                                                    long long *acc, uint32_t *tick, Loop lp,
+                                                    uint32_t zlo) {
   __shared__ unsigned long long red[32];
   Ctl *ctl = a.ctl;
   if (done_exit(ctl, lp)) return;
@@ -392,42 +408,74 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
   const int64_t lo = cuts.c[self], hi = cuts.c[self + 1];
   const uint32_t lane = lane_id();
   unsigned long long bc = 0;
-  if (hi > lo) {
-    const int64_t w0 = lo / 32, w1 = (hi - 1) / 32 + 1;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t b = w0 + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32;
-         b < w1; b += warps * 32) {
-      const int64_t w = b + lane;
-      uint32_t x = 0;
-      if (w < w1) {
-        x = nb[w] & owned_bits(w, lo, hi);
-        if (x) nb[w] = 0u;  // the mirror bits of a boundary word were cleared by reduce
-      }
-      const uint32_t n = (uint32_t)__popc(x);
-      const uint32_t incl = warp_incl_scan(n);
-      const uint32_t total = __shfl_sync(kFull, incl, 31);
-      if (!total) continue;
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&ctl->nsize, total);
-      base = __shfl_sync(kFull, base, 0);
-      const uint32_t excl = incl - n;
-      for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-        const uint32_t slot = k0 + lane;
+  // the set bits of the warp's 32 words, lane l taking bit l, l + 32, ... in
+  // word order, kE per lane in flight: queued (next frontier + snapshot) or,
+  // for the edgeless tail [zlo, hi), only counted; both broadcast the label
+  // to the vertex's mirror holders
+  auto emit = [&](int64_t b, uint32_t x, bool queue) {
+    const uint32_t n = (uint32_t)__popc(x);
+    const uint32_t incl = warp_incl_scan(n);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (!total) return;
+    uint32_t base = 0;
+    if (queue && lane == 0) base = atomicAdd(&ctl->nsize, total);
+    base = __shfl_sync(kFull, base, 0);
+    const uint32_t excl = incl - n;
+    constexpr int kE = 4;
+    for (uint32_t k0 = 0; k0 < total; k0 += 32 * kE) {
+      uint32_t v[kE], m[kE];
+      L val[kE];
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        const uint32_t slot = k0 + u * 32 + lane;
         const int o = warp_owner(incl, slot);
         const uint32_t xo = __shfl_sync(kFull, x, o);
         const uint32_t eo = __shfl_sync(kFull, excl, o);
-        if (slot >= total) continue;
-        const uint32_t v = (uint32_t)((b + o) * 32) + __fns(xo, 0, (int)(slot - eo) + 1);
-        const L val = lab[v];
-        q[base + slot] = v;
-        snap[base + slot] = val;
-        uint32_t m = mask[v - lo];
-        bc += (unsigned long long)__popc(m);
-        while (m) {
-          const int r = __ffs(m) - 1;
-          m &= m - 1;
-          at<L>(t, r, lay.o_d[0])[v] = val;
+        v[u] = slot < total ? (uint32_t)((b + o) * 32) + __fns(xo, 0, (int)(slot - eo) + 1) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        m[u] = 0u;
+        if (k0 + u * 32 + lane < total) {
+          m[u] = mm.of(v[u]);
+          if (queue || m[u]) val[u] = lab[v[u]];
         }
+      }
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        const uint32_t slot = k0 + u * 32 + lane;
+        if (slot >= total) continue;
+        if (queue) q[base + slot] = v[u], snap[base + slot] = val[u];
+        bc += (unsigned long long)__popc(m[u]);
+        while (m[u]) {
+          const int r = __ffs(m[u]) - 1;
+          m[u] &= m[u] - 1;
+          at<L>(t, r, lay.o_d[0])[v[u]] = val[u];
+        }
+      }
+    }
+  };
+  if (hi > lo) {
+    const int64_t w0 = lo / 32, w1 = (hi - 1) / 32 + 1;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // warp-major over CTAs (as k_bm_compact): a dense run of frontier bits --
+    // the relabeled hot set -- is spread over the SMs
+    const int64_t gw = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    for (int64_t b = w0 + gw * 32; b < w1; b += warps * 32) {
+      const int64_t w = b + lane;
+      uint32_t x = 0, z = 0;
+      if (w < w1) {
+        x = nb[w] & owned_bits(w, lo, hi);
+        if (x) nb[w] = 0u;  // the mirror bits of a boundary word were cleared by reduce
+        z = x & owned_bits(w, zlo, hi);
+      }
+      emit(b, x & ~z, true);
+      // the edgeless tail: counted; only its members with mirrors travel
+      const uint32_t cz = __reduce_add_sync(kFull, (uint32_t)__popc(z));
+      if (cz) {
+        if (lane == 0) atomicAdd(&ctl->nzero, cz);
+        const uint32_t za = z ? z & mm.word(w) : 0u;
+        if (__any_sync(kFull, za)) emit(b, za, false);
       }
     }
   }
@@ -477,9 +525,9 @@ __global__ void __launch_bounds__(256) k_px_bfs_reduce(TeamDev t, Layout lay, Cu
 // owners: new owned bits -> next frontier, label round + 1; the vertex is
 // marked visited in both bitmaps of its mirror holders
 __global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, Cuts cuts,
-                                                        PushArgs a, const uint32_t *mask,
+                                                        PushArgs a, Mirrors mm,
                                                         uint32_t *q, long long *acc,
-                                                        uint32_t *tick, Loop lp) {
+                                                        uint32_t *tick, Loop lp, uint32_t zlo) {
   __shared__ unsigned long long red[32];
   Ctl *ctl = a.ctl;
   if (done_exit(ctl, lp)) return;
@@ -491,44 +539,63 @@ __global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, C
   const int64_t lo = cuts.c[self], hi = cuts.c[self + 1];
   const uint32_t lane = lane_id();
   unsigned long long bc = 0;
-  if (hi > lo) {
-    const int64_t w0 = lo / 32, w1 = (hi - 1) / 32 + 1;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t b = w0 + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32;
-         b < w1; b += warps * 32) {
-      const int64_t w = b + lane;
-      uint32_t x = 0;
-      if (w < w1) {
-        x = vis[w] & ~prev[w] & owned_bits(w, lo, hi);
-        if (x) atomicOr(prev + w, x);
-      }
-      const uint32_t n = (uint32_t)__popc(x);
-      const uint32_t incl = warp_incl_scan(n);
-      const uint32_t total = __shfl_sync(kFull, incl, 31);
-      if (!total) continue;
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&ctl->nsize, total);
-      base = __shfl_sync(kFull, base, 0);
-      const uint32_t excl = incl - n;
-      for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-        const uint32_t slot = k0 + lane;
+  // as k_px_compact: queued (next frontier) or, for the edgeless tail, only
+  // counted; every new vertex gets its level and is marked in its mirror
+  // holders' bitmaps
+  auto emit = [&](int64_t b, uint32_t x, bool queue) {
+    const uint32_t n = (uint32_t)__popc(x);
+    const uint32_t incl = warp_incl_scan(n);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (!total) return;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(queue ? &ctl->nsize : &ctl->nzero, total);
+    base = __shfl_sync(kFull, base, 0);
+    const uint32_t excl = incl - n;
+    constexpr int kE = 4;
+    for (uint32_t k0 = 0; k0 < total; k0 += 32 * kE) {
+      uint32_t v[kE], m[kE];
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        const uint32_t slot = k0 + u * 32 + lane;
         const int o = warp_owner(incl, slot);
         const uint32_t xo = __shfl_sync(kFull, x, o);
         const uint32_t eo = __shfl_sync(kFull, excl, o);
+        v[u] = slot < total ? (uint32_t)((b + o) * 32) + __fns(xo, 0, (int)(slot - eo) + 1) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kE; ++u)
+        if (k0 + u * 32 + lane < total) m[u] = mm.of(v[u]);
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        const uint32_t slot = k0 + u * 32 + lane;
         if (slot >= total) continue;
-        const uint32_t v = (uint32_t)((b + o) * 32) + __fns(xo, 0, (int)(slot - eo) + 1);
-        q[base + slot] = v;
-        lab[v] = level;
-        uint32_t m = mask[v - lo];
-        bc += (unsigned long long)__popc(m);
-        const uint32_t bit = 1u << (v & 31u);
-        while (m) {
-          const int r = __ffs(m) - 1;
-          m &= m - 1;
-          atomicOr_system(at<uint32_t>(t, r, lay.o_nb) + (v >> 5), bit);
-          atomicOr_system(at<uint32_t>(t, r, lay.o_prev) + (v >> 5), bit);
+        if (queue) q[base + slot] = v[u];
+        lab[v[u]] = level;
+        bc += (unsigned long long)__popc(m[u]);
+        const uint32_t bit = 1u << (v[u] & 31u);
+        while (m[u]) {
+          const int r = __ffs(m[u]) - 1;
+          m[u] &= m[u] - 1;
+          atomicOr_system(at<uint32_t>(t, r, lay.o_nb) + (v[u] >> 5), bit);
+          atomicOr_system(at<uint32_t>(t, r, lay.o_prev) + (v[u] >> 5), bit);
         }
       }
+    }
+  };
+  if (hi > lo) {
+    const int64_t w0 = lo / 32, w1 = (hi - 1) / 32 + 1;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t gw = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    for (int64_t b = w0 + gw * 32; b < w1; b += warps * 32) {
+      const int64_t w = b + lane;
+      uint32_t x = 0, z = 0;
+      if (w < w1) {
+        x = vis[w] & ~prev[w] & owned_bits(w, lo, hi);
+        if (x) atomicOr(prev + w, x);
+        z = x & owned_bits(w, zlo, hi);
+      }
+      emit(b, x & ~z, true);
+      if (__any_sync(kFull, z)) emit(b, z, false);
     }
   }
   if (bc) __threadfence_system();  // only the threads that wrote to peers
@@ -542,14 +609,14 @@ __global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, C
 template <class T>
 __global__ void __launch_bounds__(256) k_px_rows(TeamDev t, size_t off0, size_t off1,
                                                  int parity_sel, const Ctl *ctl, int64_t lo,
-                                                 int64_t hi, const uint32_t *mask) {
+                                                 int64_t hi, Mirrors mm) {
   if (ctl->done) return;
   const size_t off = ((ctl->round & 1) == (uint32_t)parity_sel) ? off0 : off1;
   const T *src = at<T>(t, t.rank, off);
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   bool wrote = false;
   for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += st) {
-    uint32_t m = mask[v - lo];
+    uint32_t m = mm.of((uint32_t)v);
     if (!m) continue;
     const T x = src[v];
     wrote = true;
@@ -577,14 +644,14 @@ __global__ void k_px_pr_unstage(Ctl *ctl, const long long *acc) {
 
 // kcore: this round's dying owned vertices -> alive = 0 at their mirror holders
 __global__ void k_px_kill(TeamDev t, Layout lay, const Ctl *ctl, const uint32_t *dying,
-                          int64_t lo, const uint32_t *mask) {
+                          Mirrors mm) {
   if (ctl->done) return;
   const uint32_t nd = ctl->ndying;
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   bool wrote = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += st) {
     const uint32_t v = dying[i];
-    uint32_t m = mask[v - lo];
+    uint32_t m = mm.of(v);
     wrote |= m != 0;
     while (m) {
       const int r = __ffs(m) - 1;
@@ -738,6 +805,9 @@ struct Team {
 struct MirrorInfo {
   uint64_t team_id = 0;
   DBuf<uint32_t> mask;    // [hi - lo]
+  DBuf<uint32_t> any;     // [(hi - lo) / 32 + 1]
+  int64_t lo = 0;
+  Mirrors dev() const { return Mirrors{any.p, mask.p, lo}; }
   DBuf<uint32_t> mcount;  // [nv]: popc(mask) on owned rows, 0 elsewhere
 };
 
@@ -786,6 +856,9 @@ MirrorInfo &mirrors(Team &T, Graph &g, cudaStream_t s) {
   const int64_t lo = g.part.lo, hi = g.part.hi;
   mi->team_id = T.id;
   mi->mask.alloc((size_t)std::max<int64_t>(hi - lo, 1));
+  mi->any.alloc((size_t)((std::max<int64_t>(hi, lo + 1) - 1) / 32 - lo / 32 + 1));
+  mi->lo = lo;
+  SG_CUDA(cudaMemsetAsync(mi->any.p, 0, 4 * mi->any.n, s));
   mi->mcount.alloc((size_t)std::max<int64_t>(g.nv, 1));
   uint32_t *held = reinterpret_cast<uint32_t *>(T.base + T.lay.o_held);
   SG_CUDA(cudaMemsetAsync(held, 0, 4 * T.lay.nw, s));
@@ -794,7 +867,8 @@ MirrorInfo &mirrors(Team &T, Graph &g, cudaStream_t s) {
   SG_CUDA(cudaGetLastError());
   barrier(T, s);
   k_px_mask<<<grid_n(std::max<int64_t>(hi - lo, 1)), 256, 0, s>>>(T.dev(), T.lay, lo, hi,
-                                                                    mi->mask.p, mi->mcount.p);
+                                                                    mi->mask.p, mi->any.p,
+                                                                    mi->mcount.p);
   SG_CUDA(cudaGetLastError());
   barrier(T, s);
   SG_CUDA(cudaStreamSynchronize(s));
@@ -922,6 +996,8 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
   const uint32_t *inv = g.part.relabeled ? g.part.inv.p : nullptr;
   const int R = T.rank;
   const uint32_t lo = (uint32_t)cuts.c[R], hi = (uint32_t)cuts.c[R + 1];
+  // edgeless tail of the block (relabeled push / symmetrized partitions)
+  const uint32_t zlo = g.part.zlo >= (int64_t)lo && g.part.zlo <= (int64_t)hi ? (uint32_t)g.part.zlo : hi;
   Stream S;
   cudaStream_t s = S.s;
   MirrorInfo &mi = mirrors(T, g, s);
@@ -961,7 +1037,7 @@ void run_peer_push(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t m
     Lc.go("peer_reduce", k_px_reduce<L>, ticket_grid((int64_t)T.lay.nw, 4), 256, s, td, T.lay, cuts,
           ctl, acc.p, tick.p);
     Lc.go("peer_compact", k_px_compact<L>, ticket_grid(std::max<int64_t>(hi - lo, 1), 8), 256, s, td,
-          T.lay, cuts, a, (const uint32_t *)mi.mask.p, rb.q0.p, snap.p, acc.p, tick.p + 1, lp);
+          T.lay, cuts, a, mi.dev(), rb.q0.p, snap.p, acc.p, tick.p + 1, lp, zlo);
   });
   SG_CUDA(cudaEventRecord(S.e0, s));
   Lc.go("init", k_ctl_init, 1, 1, s, ctl, (int32_t)cc, cc ? hi - lo : (owns_src ? 1u : 0u));
@@ -1008,6 +1084,8 @@ void run_peer_bfs(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t ma
   const uint32_t *inv = g.part.relabeled ? g.part.inv.p : nullptr;
   const int R = T.rank;
   const uint32_t lo = (uint32_t)cuts.c[R], hi = (uint32_t)cuts.c[R + 1];
+  // edgeless tail of the block (relabeled push / symmetrized partitions)
+  const uint32_t zlo = g.part.zlo >= (int64_t)lo && g.part.zlo <= (int64_t)hi ? (uint32_t)g.part.zlo : hi;
   Stream S;
   cudaStream_t s = S.s;
   MirrorInfo &mi = mirrors(T, g, s);
@@ -1045,7 +1123,7 @@ void run_peer_bfs(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t ma
     Lc.go("peer_reduce", k_px_bfs_reduce, ticket_grid((int64_t)T.lay.nw, 4), 256, s, td, T.lay, cuts,
           ctl, acc.p, tick.p);
     Lc.go("peer_compact", k_px_bfs_compact, ticket_grid(std::max<int64_t>(hi - lo, 1), 8), 256, s, td,
-          T.lay, cuts, a, (const uint32_t *)mi.mask.p, rb.q0.p, acc.p, tick.p + 1, lp);
+          T.lay, cuts, a, mi.dev(), rb.q0.p, acc.p, tick.p + 1, lp, zlo);
   });
   SG_CUDA(cudaEventRecord(S.e0, s));
   Lc.go("init", k_ctl_init, 1, 1, s, ctl, 0, owns_src ? 1u : 0u);
@@ -1126,8 +1204,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
     L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
     // round r writes aux1 when r is even, aux0 when odd (PrFold)
     L.go("peer_rows", k_px_rows<double>, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
-         T.lay.o_d[1], T.lay.o_d[0], 0, (const Ctl *)ctl, (int64_t)lo, (int64_t)hi,
-         (const uint32_t *)mi.mask.p);
+         T.lay.o_d[1], T.lay.o_d[0], 0, (const Ctl *)ctl, (int64_t)lo, (int64_t)hi, mi.dev());
     L.go("dist", k_px_pr_stage, 1, 32, s, (const Ctl *)ctl, acc.p);
     L.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)ctl, (const long long *)acc.p,
          8);
@@ -1235,7 +1312,7 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
     L.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
     // the round's deaths -> the mirror holders (read by the next round's count)
     L.go("peer_kill", k_px_kill, grid_n(hi - lo), 256, s, td, T.lay, (const Ctl *)ctl,
-         (const uint32_t *)rb.dying.p, (int64_t)lo, (const uint32_t *)mi.mask.p);
+         (const uint32_t *)rb.dying.p, mi.dev());
     L.go("dist", k_px_kc_compact, grid_n(hi - lo), 256, s, (const Ctl *)ctl,
          (const uint32_t *)mark, (const uint8_t *)alive, lo, hi, rb.q0.p, rb.q1.p, &ctl->nsize);
     L.go("dist", k_dist_kc_next, 1, 32, s, (const Ctl *)ctl, acc.p);
@@ -1357,16 +1434,24 @@ __global__ void k_px_key(const int64_t *off, const uint32_t *indeg, int64_t nv, 
 }
 // second pass: the first kb vertices of each block (by degree) keep their
 // degree order, the rest follow in id order (a full degree order also
-// reorders the frontier and loses ~10 % on rmat24: profiles/r2x_hotk_sweep)
+// reorders the frontier and loses ~10 % on rmat24: profiles/r2x_hotk_sweep),
+// and with `off` (push / symmetrized views) the rest without rows go last;
+// nz counts those of block `rank`
 __global__ void k_px_key2(const uint32_t *perm0, int64_t nv, Cuts cuts, int64_t kb,
-                          unsigned long long *key, uint32_t *ids) {
+                          const int64_t *off, int rank, unsigned long long *key, uint32_t *ids,
+                          unsigned long long *nz) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += st) {
     const uint32_t v = perm0[i];
     const int b = owner_of(cuts, v);
     const long long pos = i - cuts.c[b];
-    key[i] = ((unsigned long long)b << 33) |
-             (pos < kb ? (unsigned long long)pos : (1ull << 32) | (unsigned long long)v);
+    unsigned long long cls = 0, low = (unsigned long long)pos;
+    if (pos >= kb) {
+      cls = off && off[v + 1] == off[v] ? 2 : 1;
+      low = v;
+      if (cls == 2 && b == rank) atomicAdd(nz, 1ull);
+    }
+    key[i] = ((unsigned long long)b << 34) | (cls << 32) | low;
     ids[i] = v;
   }
 }
@@ -1456,16 +1541,22 @@ void relabeled_slice(Graph &g, const View &v, int kind, const Cuts &c, Graph &P)
     SG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, ids.p, perm0.p, (int)nv,
                                             0, 32 + bbits));
     SG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key.p, key2.p, ids.p, P.part.perm.p,
-                                            (int)nv, 0, 33 + bbits));
+                                            (int)nv, 0, 34 + bbits));
     DBuf<char> t(std::max<size_t>(std::max(tb, tb2), 1));
     SG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, key.p, key2.p, ids.p, perm0.p, (int)nv, 0,
                                             32 + bbits));
     // hot set per block: the single-device store's 2^16 spread over the ranks
     const int64_t kb = std::max<int64_t>(1024, ((int64_t)1 << 16) / c.D);
-    k_px_key2<<<grid_n(nv), 256>>>(perm0.p, nv, c, kb, key.p, ids.p);
+    DBuf<unsigned long long> nz(1);
+    SG_CUDA(cudaMemset(nz.p, 0, sizeof(unsigned long long)));
+    k_px_key2<<<grid_n(nv), 256>>>(perm0.p, nv, c, kb, kind == 1 ? nullptr : v.off.p,
+                                   P.part.rank, key.p, ids.p, nz.p);
     SG_CUDA(cudaGetLastError());
     SG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb2, key.p, key2.p, ids.p, P.part.perm.p,
-                                            (int)nv, 0, 33 + bbits));
+                                            (int)nv, 0, 34 + bbits));
+    unsigned long long h = 0;
+    SG_CUDA(cudaMemcpy(&h, nz.p, sizeof(h), cudaMemcpyDeviceToHost));
+    P.part.zlo = kind == 1 ? -1 : hi - (int64_t)h;
     k_px_invert<<<grid_n(nv), 256>>>(P.part.perm.p, nv, P.part.inv.p);
     SG_CUDA(cudaGetLastError());
   }
