@@ -142,11 +142,11 @@ constexpr unsigned long long kBarrierNs = 60ull * 1000 * 1000 * 1000;
 // release pattern): st.release.sys carries its own system fence, about 1.4 us
 // each on B200 (scripts/micro/fence.cu), so a store per peer would cost
 // world x 1.4 us per barrier.
-__device__ bool team_barrier_dev(const TeamDev &t, Ctl *ctl) {
+__device__ bool team_barrier_dev(const TeamDev &t, Ctl *ctl, bool fence = true) {
   Hdr *me = hdr(t, t.rank);
   const unsigned long long e = me->epoch + 1;
   me->epoch = e;
-  __threadfence_system();
+  if (fence) __threadfence_system();  // else the caller fenced
   for (int q = 0; q < t.world; ++q) st_relaxed_sys(&hdr(t, q)->bar[t.rank], e);
   const unsigned long long t0 = globaltimer();
   for (int q = 0; q < t.world; ++q)
@@ -318,37 +318,50 @@ __global__ void __launch_bounds__(256) k_px_reduce(TeamDev t, Layout lay, Cuts c
   if (last_block(tick) && threadIdx.x == 0) team_barrier_dev(t, ctl);
 }
 
-// the round's counter block (k_dp_collect + the next-frontier size; sent and
-// bcast were added by reduce / compact) -> every peer's slot (one thread)
-__device__ void push_publish_dev(const PushArgs &a, const TeamDev &t, long long *acc) {
-  const Ctl *ctl = a.ctl;
-  const long long fs = ctl->dense ? a.dense_n : (long long)ctl->fsize + ctl->fzero;
-  acc[0] = fs;
-  acc[1] = (long long)ctl->edges;
-  acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
-  acc[3] = a.sched >= 2 ? 0 : (long long)ctl->huge_edges;
-  acc[4] = a.sched >= 2 ? 0 : ctl->nlarge;
-  acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
-  acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
-  acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
-  acc[10] = (long long)ctl->nsize + ctl->nzero;
-  const int par = ctl->round & 1;
-  for (int i = 0; i < t.world * kDP; ++i) hdr(t, i / kDP)->cnt[par][t.rank][i % kDP] = acc[i % kDP];
-}
-
-// after the barrier: sum the slots, write the round log, decide quiescence
-// (identically on every rank), reset the round state (one thread)
-__device__ void push_advance_dev(const PushArgs &a, const TeamDev &t, long long *acc,
-                                 const Loop &lp) {
+// The round's tail, run by warp 0 of the compaction's last block: the
+// counter block (k_dp_collect + the next-frontier size; sent and bcast were
+// added by reduce / compact) goes into every peer's slot (lanes in parallel),
+// the barrier, then every rank sums the same slots (lane j: slot j over the
+// ranks), writes the same round log, decides quiescence identically and
+// resets the round state; leaves the WHILE loop when the run is done for any
+// reason (a barrier timeout included)
+__device__ void push_round_tail(const PushArgs &a, const TeamDev &t, long long *acc,
+                                const Loop &lp) {
+  const uint32_t lane = lane_id();
   Ctl *ctl = a.ctl;
-  const int par = ctl->round & 1;
-  const Hdr *me = hdr(t, t.rank);
-  long long x[kDP];
-  for (int j = 0; j < kDP; ++j) {
-    long long sum = 0;
-    for (int q = 0; q < t.world; ++q) sum += ld_volatile(&me->cnt[par][q][j]);
-    x[j] = sum;
+  if (lane == 0) {
+    const long long fs = ctl->dense ? a.dense_n : (long long)ctl->fsize + ctl->fzero;
+    acc[0] = fs;
+    acc[1] = (long long)ctl->edges;
+    acc[2] = a.sched >= 2 ? 0 : ctl->nhuge;
+    acc[3] = a.sched >= 2 ? 0 : (long long)ctl->huge_edges;
+    acc[4] = a.sched >= 2 ? 0 : ctl->nlarge;
+    acc[5] = a.sched >= 2 ? 0 : (long long)ctl->large_edges;
+    acc[8] = a.sched == 1 ? 0 : fs > 0;  // run_round only for a non-empty local frontier
+    acc[9] = a.sched == 1 ? ctl->huge_edges > 0 : a.sched == 0 ? ctl->nhuge > 0 : 0;
+    acc[10] = (long long)ctl->nsize + ctl->nzero;
   }
+  __syncwarp();
+  const int par = ctl->round & 1;
+  for (int i = (int)lane; i < t.world * kDP; i += 32)
+    hdr(t, i / kDP)->cnt[par][t.rank][i % kDP] = acc[i % kDP];
+  __threadfence_system();
+  __syncwarp();
+  int ok = 1;
+  if (lane == 0) ok = team_barrier_dev(t, ctl, false);
+  ok = __shfl_sync(kFull, ok, 0);
+  if (!ok) {
+    if (lane == 0 && lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
+    return;
+  }
+  const Hdr *me = hdr(t, t.rank);
+  long long sum = 0;
+  if (lane < (uint32_t)kDP)
+    for (int q = 0; q < t.world; ++q) sum += ld_volatile(&me->cnt[par][q][lane]);
+  long long x[kDP];
+#pragma unroll
+  for (int j = 0; j < kDP; ++j) x[j] = __shfl_sync(kFull, sum, j);
+  if (lane) return;
   const uint32_t round = ctl->round;
   RoundStat &s = a.stats[round];
   s.frontier_size = x[0];
@@ -371,16 +384,6 @@ __device__ void push_advance_dev(const PushArgs &a, const TeamDev &t, long long 
   ctl->round = round + 1;
   for (int j = 0; j < kDP; ++j) acc[j] = 0;
   loop_test(ctl, round, x[10] == 0, lp);
-}
-
-// the round's tail in the last block of the compaction: publish the counter
-// block, barrier, advance; leaves the WHILE loop when the run is done for any
-// reason (a barrier timeout included)
-__device__ void push_round_tail(const PushArgs &a, const TeamDev &t, long long *acc,
-                                const Loop &lp) {
-  push_publish_dev(a, t, acc);
-  if (team_barrier_dev(t, a.ctl)) push_advance_dev(a, t, acc, lp);
-  else if (lp.use_cond) cudaGraphSetConditional(lp.cond, 0u);
 }
 // a compaction launched after the run went done (barrier timeout) only leaves the loop
 __device__ __forceinline__ bool done_exit(const Ctl *ctl, const Loop &lp) {
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(256) k_px_compact(TeamDev t, Layout lay, Cuts 
   if (bc) __threadfence_system();  // only the threads that wrote to peers
   bc = block_sum(bc, red);
   if (threadIdx.x == 0 && bc) atomicAdd((unsigned long long *)&acc[7], bc);
-  if (last_block(tick) && threadIdx.x == 0) push_round_tail(a, t, acc, lp);
+  if (last_block(tick) && threadIdx.x < 32) push_round_tail(a, t, acc, lp);
 }
 
 // ---- bfs: the visited-bitmap operator (BmBfs) over the peers.  vis (the nb
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(256) k_px_bfs_compact(TeamDev t, Layout lay, C
   if (bc) __threadfence_system();  // only the threads that wrote to peers
   bc = block_sum(bc, red);
   if (threadIdx.x == 0 && bc) atomicAdd((unsigned long long *)&acc[7], bc);
-  if (last_block(tick) && threadIdx.x == 0) push_round_tail(a, t, acc, lp);
+  if (last_block(tick) && threadIdx.x < 32) push_round_tail(a, t, acc, lp);
 }
 
 // ------------------------------------------------------------- pr, kcore --
