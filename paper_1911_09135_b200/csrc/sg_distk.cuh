@@ -77,14 +77,15 @@ __global__ void k_dist_pr_collect(const Ctl *ctl, int has_rows, long long *acc) 
 __global__ void k_dist_kc_collect(PullArgs a, long long *acc) {
   const Ctl *ctl = a.ctl;
   if (threadIdx.x || ctl->done) return;
-  const long long fs = ctl->dense ? a.row_n : ctl->fsize;
+  // fzero: isolated rows killed at init (peer relabeled blocks), round 0 only
+  const long long fs = ctl->dense ? (long long)a.row_n + ctl->fzero : ctl->fsize;
   acc[0] = fs;
   acc[1] = (long long)ctl->edges;
   acc[2] = ctl->nhuge;
   acc[3] = (long long)ctl->huge_edges;
   acc[4] = ctl->nlarge;
   acc[5] = (long long)ctl->large_edges;
-  acc[6] = ctl->ndying;
+  acc[6] = (long long)ctl->ndying + ctl->fzero;
   acc[7] = (long long)ctl->comm_bcast;
   acc[8] = fs > 0;            // run_round only for a non-empty local frontier (engine.py:216)
   acc[9] = ctl->nhuge > 0;
@@ -130,7 +131,7 @@ __global__ void k_dist_kc_advance(PullArgs a, long long *acc, Loop lp) {
   const bool stop = acc[6] == 0 || acc[10] == 0;
   ctl->fsize = ctl->nsize;
   ctl->nsize = 0;
-  ctl->ndying = 0;
+  ctl->ndying = ctl->fzero = 0;
   ctl->nlarge = ctl->nhuge = ctl->large_head = ctl->chunk_head = 0;
   ctl->edges = ctl->huge_edges = ctl->large_edges = ctl->comm_bcast = 0;
   ctl->dense = 0;

@@ -687,34 +687,74 @@ struct OpMarkPeer {
                                         const bool (&ok)[kU], const L (&)[kU],
                                         uint32_t (&dst)[kU], bool (&act)[kU]) const {
     const long long lo = cuts.c[t.rank], hi = cuts.c[t.rank + 1];
+    bool live[kU], own[kU];
+    uint32_t cur[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) dst[u] = ok[u] ? ld_stream(a.col + e[u]) : 0u;
+    // this rank's alive copy filters the vertices dead before this round (a
+    // mirror's flag lags its owner by this round's deaths only: the owner
+    // filters those when it collects)
+#pragma unroll
+    for (int u = 0; u < kU; ++u) live[u] = ok[u] && alive[dst[u]];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      own[u] = (long long)dst[u] >= lo && (long long)dst[u] < hi;
+      cur[u] = live[u] && own[u] ? mark[dst[u]] : stamp;
+    }
+    // plain stores (nothing is enqueued here): the owner collects its stamped
+    // rows after the barrier
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       act[u] = false;
-      if (!ok[u]) continue;
-      const uint32_t v = dst[u];
-      if ((long long)v >= lo && (long long)v < hi) {
-        if (alive[v] && mark[v] != stamp) act[u] = atomicExch(mark + v, stamp) != stamp;
-      } else {  // the owner knows whether v is alive: it filters at collection
-        at<uint32_t>(t, owner_of(cuts, v), o_mark)[v] = stamp;
+      if (!live[u]) continue;
+      if (own[u]) {
+        if (cur[u] != stamp) mark[dst[u]] = stamp;
+      } else {
+        at<uint32_t>(t, owner_of(cuts, dst[u]), o_mark)[dst[u]] = stamp;
       }
     }
   }
 };
 
-// kcore: owned rows stamped this round and still alive -> next local frontier
+// kcore: owned rows stamped this round and still alive -> next local frontier.
+// A lane takes 4 vertices (one 16-byte mark load, one 4-byte alive load); one
+// queue reservation per warp step
 __global__ void k_px_kc_compact(const Ctl *ctl, const uint32_t *mark, const uint8_t *alive,
                                 uint32_t lo, uint32_t hi, uint32_t *q0, uint32_t *q1,
                                 uint32_t *nsize) {
   if (ctl->done) return;
   const uint32_t round = ctl->round, stamp = round + 1;
   uint32_t *q = (round & 1) ? q0 : q1;
+  const uint64_t g0 = lo >> 2, g1 = ((uint64_t)hi + 3) >> 2;  // groups of 4 vertices
+  const uint32_t lane = lane_id();
   const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < hi - lo; b += st) {
-    const uint64_t i = b + threadIdx.x;
-    const bool m = i < hi - lo && mark[lo + i] == stamp && alive[lo + i];
-    warp_append(m, lo + (uint32_t)i, q, nsize);
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < g1 - g0; b += st) {
+    const uint64_t gi = g0 + b + threadIdx.x;
+    const uint32_t v0 = (uint32_t)(gi * 4);
+    uint32_t f = 0;
+    if (gi < g1) {
+      const uint4 m = reinterpret_cast<const uint4 *>(mark)[gi];
+      const uint32_t al = reinterpret_cast<const uint32_t *>(alive)[gi];
+      const uint32_t mv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t v = v0 + k;
+        if (v >= lo && v < hi && mv[k] == stamp && ((al >> (8 * k)) & 0xffu)) f |= 1u << k;
+      }
+    }
+    const uint32_t c = (uint32_t)__popc(f);
+    const uint32_t incl = warp_incl_scan(c);
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    if (!tot) continue;
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(nsize, tot);
+    base = __shfl_sync(kFull, base, 31);
+    uint32_t pos = base + incl - c;
+    while (f) {
+      const int k = __ffs(f) - 1;
+      f &= f - 1;
+      q[pos++] = v0 + (uint32_t)k;
+    }
   }
 }
 
@@ -1281,7 +1321,12 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
   rb.alloc_common(nv, stats_cap(max_rounds));
   rb.dying.alloc(std::max<int64_t>(nv, 1));
   PullArgs a = rb.pull_args(v, thr, 1);
-  a.row_lo = lo, a.row_n = hi - lo;
+  // relabeled: [zlo, hi) are the block's isolated vertices -- they die in
+  // round 0 with no neighbour to tell, so they are killed at init and only
+  // counted in round 0's log (Ctl::fzero), as on one GPU; the dense pass
+  // stops at zlo
+  const uint32_t zlo = g.part.zlo >= (int64_t)lo && g.part.zlo <= (int64_t)hi ? (uint32_t)g.part.zlo : hi;
+  a.row_lo = lo, a.row_n = zlo - lo;
   a.mcount = mi.mcount.p;
   PushArgs w = rb.push_args(v, kNoHuge);
   w.src_mode = 1;
@@ -1316,7 +1361,7 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
     // the round's deaths -> the mirror holders (read by the next round's count)
     L.go("peer_kill", k_px_kill, grid_n(hi - lo), 256, s, td, T.lay, (const Ctl *)ctl,
          (const uint32_t *)rb.dying.p, mi.dev());
-    L.go("dist", k_px_kc_compact, grid_n(hi - lo), 256, s, (const Ctl *)ctl,
+    L.go("dist", k_px_kc_compact, grid_n(((int64_t)hi - lo) / 4 + 1), 256, s, (const Ctl *)ctl,
          (const uint32_t *)mark, (const uint8_t *)alive, lo, hi, rb.q0.p, rb.q1.p, &ctl->nsize);
     L.go("dist", k_dist_kc_next, 1, 32, s, (const Ctl *)ctl, acc.p);
     L.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)ctl, (const long long *)acc.p,
@@ -1329,6 +1374,10 @@ void run_peer_kcore(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t 
   SG_CUDA(cudaEventRecord(S.e0, s));
   L.go("init", k_ctl_init, 1, 1, s, ctl, 1, hi - lo);
   fill<uint8_t>(L, alive, nv, (uint8_t)1, s);
+  if (zlo < hi) {
+    fill<uint8_t>(L, alive + zlo, (int64_t)(hi - zlo), (uint8_t)0, s);
+    L.go("init", k_set1<uint32_t>, 1, 1, s, &ctl->fzero, (int64_t)0, hi - zlo);
+  }
   fill<uint32_t>(L, mark, nv, 0u, s);
   fill<uint32_t>(L, hcnt.p, nv, 0u, s);
   fill<long long>(L, acc.p, kSlot, 0ll, s);
