@@ -87,6 +87,26 @@ def test_peer_partition_rejects_wrong_app(sg):
             sg.apps.make_app("bfs"), sg.Scheduler("alb"), sg.KernelConfig(), 1, 100))
 
 
+@pytest.mark.parametrize("gname,world", [("rmat12", 5), ("rmat12", 7), ("rmat14", 6),
+                                         ("uniform10", 5)])
+@pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
+@pytest.mark.parametrize("relabel", [False, True])
+def test_peer_odd_worlds_match_d1(sg, golden, app, gname, world, relabel):
+    """World sizes without goldens (cuts at arbitrary, unaligned ids; relabeled
+    blocks with their edgeless / isolated tails): labels and the per-round
+    frontier / active edges do not depend on D, so they must equal the
+    reference's d1 run."""
+    from paper_1911_09135_b200 import dist
+    info = golden["runs"][gname][f"{app}/alb/d1"]
+    g = _graph(sg, gname)
+    if app == "sssp":
+        g = sg.attach_random_weights(g, 2)
+    res = dist.run_app_peer_threads(g, app, sg.Scheduler("alb"), world=world, relabel=relabel)
+    assert sg.engine.labels_sha256(res.labels) == info["labels_sha256"]
+    assert [[r.frontier_size, r.active_edges()] for r in res.records] == \
+        [x[:2] for x in info["per_round"]]
+
+
 @pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "pr", "kcore"])
 def test_peer_world1_matches_single_device(sg, golden, app):
     """world = 1: one partition holding every row, IPC-exported region, the
