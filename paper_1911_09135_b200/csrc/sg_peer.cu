@@ -613,20 +613,34 @@ template <class T>
 __global__ void __launch_bounds__(256) k_px_rows(TeamDev t, size_t off0, size_t off1,
                                                  int parity_sel, const Ctl *ctl, int64_t lo,
                                                  int64_t hi, Mirrors mm) {
-  if (ctl->done) return;
+  if (ctl->done || hi <= lo) return;
   const size_t off = ((ctl->round & 1) == (uint32_t)parity_sel) ? off0 : off1;
   const T *src = at<T>(t, t.rank, off);
-  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  // a warp takes 32 words of the any-mirror bitmap and walks only the words
+  // with mirrors, one vertex per lane (no work for vertices without holders)
+  const uint32_t lane = lane_id();
+  const int64_t w0 = lo >> 5, w1 = ((hi - 1) >> 5) + 1;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   bool wrote = false;
-  for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += st) {
-    uint32_t m = mm.of((uint32_t)v);
-    if (!m) continue;
-    const T x = src[v];
-    wrote = true;
-    while (m) {
-      const int r = __ffs(m) - 1;
-      m &= m - 1;
-      at<T>(t, r, off)[v] = x;
+  for (int64_t b = w0 + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32;
+       b < w1; b += warps * 32) {
+    const int64_t w = b + lane;
+    const uint32_t word = w < w1 ? mm.word(w) & owned_bits(w, lo, hi) : 0u;
+    uint32_t busy = __ballot_sync(kFull, word != 0u);
+    while (busy) {
+      const int j = __ffs(busy) - 1;
+      busy &= busy - 1;
+      const uint32_t wj = __shfl_sync(kFull, word, j);
+      if (!((wj >> lane) & 1u)) continue;
+      const uint32_t v = (uint32_t)((b + j) * 32) + lane;
+      uint32_t m = mm.mask[v - lo];
+      const T x = src[v];
+      wrote = true;
+      while (m) {
+        const int r = __ffs(m) - 1;
+        m &= m - 1;
+        at<T>(t, r, off)[v] = x;
+      }
     }
   }
   if (wrote) __threadfence_system();
@@ -1246,7 +1260,7 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
     L.go("pr_pull", k_prx<0>, gx, kTB, s, xa, fold);
     L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
     // round r writes aux1 when r is even, aux0 when odd (PrFold)
-    L.go("peer_rows", k_px_rows<double>, grid_n(std::max<int64_t>(hi - lo, 1)), 256, s, td,
+    L.go("peer_rows", k_px_rows<double>, grid_n(std::max<int64_t>(hi - lo, 1) / 32 + 1), 256, s, td,
          T.lay.o_d[1], T.lay.o_d[0], 0, (const Ctl *)ctl, (int64_t)lo, (int64_t)hi, mi.dev());
     L.go("dist", k_px_pr_stage, 1, 32, s, (const Ctl *)ctl, acc.p);
     L.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)ctl, (const long long *)acc.p,
