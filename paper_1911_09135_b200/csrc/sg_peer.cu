@@ -646,18 +646,49 @@ __global__ void __launch_bounds__(256) k_px_rows(TeamDev t, size_t off0, size_t 
   if (wrote) __threadfence_system();
 }
 
-// pr: max |delta| and comm_broadcast of this rank join the counter block
-// (acc[6], acc[7]) and come back reduced over the ranks
-__global__ void k_px_pr_stage(const Ctl *ctl, long long *acc) {
-  if (threadIdx.x || ctl->done) return;
-  acc[6] = (long long)ctl->delta_bits;  // a non-negative double: its bits order like it
-  acc[7] = (long long)ctl->comm_bcast;
+// pr round tail in one warp (after the mirror rows): this rank's counters
+// (k_dist_pr_collect's six, max |delta| bits, comm_broadcast) into every
+// peer's slot, the barrier, then the sums (acc[6]: the max) back into acc and
+// Ctl -- what collect / stage / publish / barrier / reduce_slots / unstage
+// did in six launches
+__global__ void k_px_pr_sync(TeamDev t, Ctl *ctl, int has_rows, long long *acc) {
+  if (threadIdx.x >= 32 || ctl->done) return;
+  const uint32_t lane = threadIdx.x;
+  constexpr int n = 8;
+  if (lane == 0) {
+    acc[0] = has_rows;
+    acc[1] = ctl->nhuge > 0;
+    acc[2] = ctl->nhuge;
+    acc[3] = (long long)ctl->huge_edges;
+    acc[4] = ctl->nlarge;
+    acc[5] = (long long)ctl->large_edges;
+    acc[6] = (long long)ctl->delta_bits;  // a non-negative double: its bits order like it
+    acc[7] = (long long)ctl->comm_bcast;
+  }
+  __syncwarp();
+  const int par = ctl->round & 1;
+  for (int i = (int)lane; i < t.world * n; i += 32) hdr(t, i / n)->cnt[par][t.rank][i % n] = acc[i % n];
+  __threadfence_system();
+  __syncwarp();
+  int ok = 1;
+  if (lane == 0) ok = team_barrier_dev(t, ctl, false);
+  if (!__shfl_sync(kFull, ok, 0)) return;
+  const Hdr *me = hdr(t, t.rank);
+  if (lane < (uint32_t)n) {
+    long long s = 0;
+    for (int q = 0; q < t.world; ++q) {
+      const long long x = ld_volatile(&me->cnt[par][q][lane]);
+      s = lane == 6 ? (q == 0 || x > s ? x : s) : s + x;
+    }
+    acc[lane] = s;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    ctl->delta_bits = (unsigned long long)acc[6];
+    ctl->comm_bcast = (unsigned long long)acc[7];
+  }
 }
-__global__ void k_px_pr_unstage(Ctl *ctl, const long long *acc) {
-  if (threadIdx.x || ctl->done) return;
-  ctl->delta_bits = (unsigned long long)acc[6];
-  ctl->comm_bcast = (unsigned long long)acc[7];
-}
+
 
 // kcore: this round's dying owned vertices -> alive = 0 at their mirror holders
 __global__ void k_px_kill(TeamDev t, Layout lay, const Ctl *ctl, const uint32_t *dying,
@@ -1258,16 +1289,10 @@ void run_peer_pr(Team &T, Graph &g, const sg_params &p, int64_t thr, int64_t max
     // acc[6] = max |delta| bits, acc[7] = comm_broadcast -- summed / maxed over ranks
     PrStop st2{gmax.p, d, p.tol, g.part.full_ne, limit, max_rounds, cond, W.uc, 1, 2, acc.p};
     L.go("pr_pull", k_prx<0>, gx, kTB, s, xa, fold);
-    L.go("dist", k_dist_pr_collect, 1, 32, s, (const Ctl *)ctl, (int)(hi > lo), acc.p);
     // round r writes aux1 when r is even, aux0 when odd (PrFold)
     L.go("peer_rows", k_px_rows<double>, grid_n(std::max<int64_t>(hi - lo, 1) / 32 + 1), 256, s, td,
          T.lay.o_d[1], T.lay.o_d[0], 0, (const Ctl *)ctl, (int64_t)lo, (int64_t)hi, mi.dev());
-    L.go("dist", k_px_pr_stage, 1, 32, s, (const Ctl *)ctl, acc.p);
-    L.go("peer_publish", k_px_publish, 1, 256, s, td, (const Ctl *)ctl, (const long long *)acc.p,
-         8);
-    L.go("peer_barrier", k_team_barrier, 1, 32, s, td, ctl);
-    L.go("peer_sum", k_px_reduce_slots, 1, 32, s, td, (const Ctl *)ctl, acc.p, 8, 1u << 6);
-    L.go("dist", k_px_pr_unstage, 1, 32, s, ctl, (const long long *)acc.p);
+    L.go("peer_sync", k_px_pr_sync, 1, 32, s, td, ctl, (int)(hi > lo), acc.p);
     L.go("pr_finish", k_pull_finish<PrOp, true>, 1, 1024, s, a, op, hacc.p, st2);
     fill<uint32_t>(L, head.p, 1, 0u, s);
     L.go("guard", k_loop_guard, 1, 32, s, (const Ctl *)ctl, lp);
