@@ -518,7 +518,14 @@ def main():
         off, tgt, w = host_csr if team is not None else dev.download(0, weights=(a.app == "sssp"))
         pin = lambda x: torch.from_numpy(x).pin_memory().numpy() if x is not None else None
         off_p, tgt_p, w_p = pin(off), pin(tgt), pin(w)
-        h2d = off_p.nbytes + tgt_p.nbytes + (w_p.nbytes if w_p is not None else 0)
+        # sg_graph_create packs weights in [0, 255] / [0, 65535] into 1 / 2 bytes
+        # on the host before the copy (sg_engine.cu upload_weights)
+        wbytes = 0
+        if w_p is not None and len(w_p):
+            lo_w, hi_w = int(w_p.min()), int(w_p.max())
+            wbytes = len(w_p) * (1 if lo_w >= 0 and hi_w <= 255 else
+                                 2 if lo_w >= 0 and hi_w <= 65535 else 8)
+        h2d = off_p.nbytes + tgt_p.nbytes + wbytes
         d2h = 8 * nv + native.ROUND_DTYPE.itemsize * rounds
         def upload():
             dg = native.DeviceGraph.from_csr(off_p, tgt_p, w_p)
@@ -544,7 +551,8 @@ def main():
         e2e = {"value": edges * len(e2e_s) / e2e_tot / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * e2e_tot / len(e2e_s), "steps": len(e2e_s),
-               "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights), sg_run "
+               "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights, packed "
+                       "to their byte width on the host while the topology is in flight), sg_run "
                        "(original numbering: a fresh graph's first run), labels + round log D2H"
                        if team is None else
                        "per step and rank: sg_graph_create of the full CSR (+ int64 weights) "

@@ -10,6 +10,7 @@
 // per round (frontier size, active edges, ... == RoundRecord).
 
 #include <cstdlib>
+#include <thread>
 #include <cub/device/device_scan.cuh>
 
 #include "sg_runtime.cuh"
@@ -807,6 +808,88 @@ void run_app_layout(Graph &g, const sg_params &p, double *labels_out, sg_round *
 // ====================================================================== C ABI
 using sg::Error;
 
+namespace sg {
+namespace {
+// Weight upload.  The host link (54.5 GB/s pinned, profiles/r2ay) bounds the
+// e2e step and int64 weights are 2/3 of a weighted CSR's bytes: when every
+// weight is in [0, 255] ([0, 65535]) host threads pack them into a pinned
+// staging block -- while the offsets / targets are already in flight -- and
+// 1/8 (1/4) of the bytes cross the link; the device widens them back to the
+// int64 array the graph keeps.  Anything else goes up as int64.
+template <class N>
+__global__ void k_widen(const N *in, int64_t n, int64_t *out) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) out[i] = in[i];
+}
+// width 1 / 2: packed into `dst`; 0: some weight needs more than 16 bits
+template <class N>
+bool pack_weights(const int64_t *w, int64_t n, N *dst, int threads) {
+  std::atomic<bool> ok{true};
+  std::vector<std::thread> th;
+  const int64_t per = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t)
+    th.emplace_back([&, t] {
+      const int64_t a = t * per, b = std::min<int64_t>(n, a + per);
+      uint64_t bad = 0;
+      for (int64_t i = a; i < b; ++i) {
+        const int64_t x = w[i];
+        bad |= (uint64_t)x >> (8 * sizeof(N));  // negative or too wide
+        dst[i] = (N)x;
+      }
+      if (bad) ok = false;
+    });
+  for (auto &x : th) x.join();
+  return ok;
+}
+int g_last_weight_width = 8;  // bytes per weight of the last upload (sg_graph_last_upload)
+void upload_weights(const int64_t *host, int64_t n, int64_t *dev, cudaStream_t s) {
+  g_last_weight_width = 8;
+  if (n <= 0) return;
+  static const int cap = [] {  // SG_PACK_THREADS: host threads packing the weights
+    const char *e = std::getenv("SG_PACK_THREADS");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int threads = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)cap, (int64_t)hw, n >> 20}));
+  void *stage = host_alloc((size_t)n * 2);
+  bool done = false;
+  {
+    // bytes: packed and copied in 8 slices, so each slice crosses the link
+    // while the next one is packed
+    DBuf<uint8_t> d((size_t)n);
+    const int64_t K = 8, per = (n + K - 1) / K;
+    bool ok = true;
+    for (int64_t a = 0; a < n && ok; a += per) {
+      const int64_t len = std::min<int64_t>(per, n - a);
+      ok = pack_weights(host + a, len, (uint8_t *)stage + a, threads);
+      if (ok)
+        SG_CUDA(cudaMemcpyAsync(d.p + a, (uint8_t *)stage + a, (size_t)len, cudaMemcpyHostToDevice, s));
+    }
+    if (ok) {
+      k_widen<uint8_t><<<grid_n(n), 256, 0, s>>>(d.p, n, dev);
+      SG_CUDA(cudaGetLastError());
+      g_last_weight_width = 1, done = true;
+    }
+    SG_CUDA(cudaStreamSynchronize(s));  // the staging block is reused below
+  }
+  if (done) {
+  } else if (pack_weights(host, n, (uint16_t *)stage, threads)) {
+    DBuf<uint16_t> d((size_t)n);
+    SG_CUDA(cudaMemcpyAsync(d.p, stage, (size_t)n * 2, cudaMemcpyHostToDevice, s));
+    k_widen<uint16_t><<<grid_n(n), 256, 0, s>>>(d.p, n, dev);
+    SG_CUDA(cudaGetLastError());
+    SG_CUDA(cudaStreamSynchronize(s));
+    g_last_weight_width = 2, done = true;
+  }
+  host_free(stage);
+  if (!done) {
+    SG_CUDA(cudaMemcpyAsync(dev, host, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+  }
+}
+}  // namespace
+}  // namespace sg
+
 extern "C" {
 
 const char *sg_last_error(void) { return sg::t_last_error.c_str(); }
@@ -846,14 +929,25 @@ int sg_graph_create(const int64_t *offsets, const int32_t *targets, const int64_
     g->csr.nv = nv, g->csr.ne = ne;
     g->csr.off.alloc(nv + 1);
     g->csr.col.alloc(ne ? ne : 1);
-    SG_CUDA(cudaMemcpy(g->csr.off.p, offsets, sizeof(int64_t) * (nv + 1), cudaMemcpyHostToDevice));
+    // the topology goes up asynchronously while host threads pack the weights
+    cudaStream_t s = nullptr;
+    SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamSynchronize(s), cudaStreamDestroy(s); }
+    } sgd{s};
+    SG_CUDA(cudaMemcpyAsync(g->csr.off.p, offsets, sizeof(int64_t) * (nv + 1),
+                            cudaMemcpyHostToDevice, s));
     if (ne)
-      SG_CUDA(cudaMemcpy(g->csr.col.p, targets, sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
+      SG_CUDA(cudaMemcpyAsync(g->csr.col.p, targets, sizeof(int32_t) * ne,
+                              cudaMemcpyHostToDevice, s));
     if (weights) {
       g->w64.alloc(ne ? ne : 1);
-      if (ne)
-        SG_CUDA(cudaMemcpy(g->w64.p, weights, sizeof(int64_t) * ne, cudaMemcpyHostToDevice));
+      sg::upload_weights(weights, ne, g->w64.p, s);
+      SG_CUDA(cudaStreamSynchronize(s));
       sg::weights_finalize(*g);
+    } else {
+      SG_CUDA(cudaStreamSynchronize(s));
     }
     *out = new sg_graph{g};
   });
@@ -914,8 +1008,8 @@ int sg_graph_with_weights(sg_graph *gh, const int64_t *weights, sg_graph **out) 
       SG_CUDA(cudaMemcpy(g->csr.col.p, src.csr.col.p, sizeof(uint32_t) * src.ne,
                          cudaMemcpyDeviceToDevice));
     g->w64.alloc(src.ne ? src.ne : 1);
-    if (src.ne)
-      SG_CUDA(cudaMemcpy(g->w64.p, weights, sizeof(int64_t) * src.ne, cudaMemcpyHostToDevice));
+    SG_CUDA(cudaDeviceSynchronize());
+    sg::upload_weights(weights, src.ne, g->w64.p, nullptr);
     sg::weights_finalize(*g);
     *out = new sg_graph{g};
   });

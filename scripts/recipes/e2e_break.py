@@ -1,4 +1,6 @@
-import time, numpy as np, torch
+import sys, time, numpy as np, torch
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import paper_1911_09135_b200 as sg
 from paper_1911_09135_b200 import native
 g = sg.attach_random_weights(sg.generate_rmat(24, 16, 1), 2)

@@ -210,6 +210,22 @@ def test_sssp_float64_path_big_weights(sg, O):
         [[r.frontier_size, r.active_edges] for r in log]
 
 
+@pytest.mark.parametrize("lo,hi", [(1, 256), (1, 65536), (0, 2), (65535, 65537)])
+def test_sssp_weight_upload_widths(sg, O, lo, hi):
+    """sg_graph_create packs host weights to 1 or 2 bytes when they fit (and
+    falls back to int64 otherwise); every width gives the reference's labels."""
+    off, tgt = O.rmat_csr(11)
+    rng = np.random.default_rng(lo + hi)
+    w = rng.integers(lo, hi, size=len(tgt), dtype=np.int64)
+    g = sg.Graph(off, tgt, w)
+    assert np.array_equal(g.device().download(0, weights=True)[2], w)
+    res = sg.run_app(g, "sssp")
+    lab, log = O.run(off, tgt, w, "sssp")
+    assert O.labels_sha256(res.labels) == O.labels_sha256(lab)
+    assert [[r.frontier_size, r.active_edges()] for r in res.records] == \
+        [[r.frontier_size, r.active_edges] for r in log]
+
+
 @pytest.mark.parametrize("scale,thr", [(18, None), (20, None), (18, 256), (18, 300)])
 @pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "kcore", "pr"])
 def test_larger_scale_vs_c_oracle(sg, scale, thr, app):
