@@ -537,10 +537,11 @@ def main():
         for _ in range(2):  # warm the device / pinned block caches (steady state)
             _warm = step(upload())
         torch.cuda.synchronize()
-        e2e_s = []
+        e2e_s, up_s = [], []
         for _ in range(max(1, a.steps)):
             t0 = time.perf_counter()
             dg = upload()
+            up_s.append(time.perf_counter() - t0)
             lab_e, log_e, _ = step(dg)
             torch.cuda.synchronize()
             e2e_s.append(time.perf_counter() - t0)
@@ -551,6 +552,7 @@ def main():
         e2e = {"value": edges * len(e2e_s) / e2e_tot / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * e2e_tot / len(e2e_s), "steps": len(e2e_s),
+               "upload_ms_median": 1e3 * statistics.median(up_s),
                "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights, packed "
                        "to their byte width on the host while the topology is in flight), sg_run "
                        "(original numbering: a fresh graph's first run), labels + round log D2H"
