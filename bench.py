@@ -534,7 +534,7 @@ def main():
             kind = sgdist.PART_KIND[a.app]
             return native.DevicePartition.of(dg, kind, world, rank)
 
-        for _ in range(2):  # warm the device / pinned block caches (steady state)
+        for _ in range(3):  # warm the device / pinned block caches (steady state)
             _warm = step(upload())
         torch.cuda.synchronize()
         e2e_s, up_s = [], []
@@ -553,6 +553,7 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * e2e_tot / len(e2e_s), "steps": len(e2e_s),
                "upload_ms_median": 1e3 * statistics.median(up_s),
+               "step_ms": [round(1e3 * x, 1) for x in e2e_s],
                "note": "per step: sg_graph_create from pinned host CSR (+ int64 weights, packed "
                        "to their byte width on the host while the topology is in flight), sg_run "
                        "(original numbering: a fresh graph's first run), labels + round log D2H"
