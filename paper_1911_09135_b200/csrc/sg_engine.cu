@@ -849,7 +849,12 @@ void upload_weights(const int64_t *host, int64_t n, int64_t *dev, cudaStream_t s
     const char *e = std::getenv("SG_PACK_THREADS");
     return e ? std::max(1, std::atoi(e)) : 16;
   }();
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  // ranks of one node (torchrun's LOCAL_WORLD_SIZE) share the host's cores
+  static const int local = [] {
+    const char *e = std::getenv("LOCAL_WORLD_SIZE");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency() / (unsigned)local);
   const int threads = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)cap, (int64_t)hw, n >> 20}));
   void *stage = host_alloc((size_t)n * 2);
   bool done = false;
