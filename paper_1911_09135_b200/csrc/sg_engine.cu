@@ -856,40 +856,58 @@ void upload_weights(const int64_t *host, int64_t n, int64_t *dev, cudaStream_t s
   }();
   const int hw = (int)std::max(1u, std::thread::hardware_concurrency() / (unsigned)local);
   const int threads = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)cap, (int64_t)hw, n >> 20}));
-  void *stage = host_alloc((size_t)n * 2);
-  bool done = false;
-  {
-    // bytes: packed and copied in 8 slices, so each slice crosses the link
-    // while the next one is packed
-    DBuf<uint8_t> d((size_t)n);
-    const int64_t K = 8, per = (n + K - 1) / K;
+  // the weights' own stream: their slices cross the link beside the topology
+  // still in flight on the caller's stream
+  cudaStream_t ws = nullptr;
+  SG_CUDA(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
+  struct WsGuard {
+    cudaStream_t s;
+    ~WsGuard() { cudaStreamSynchronize(s), cudaStreamDestroy(s); }
+  } wsg{ws};
+  (void)s;
+  // one width at a time, packed in slices that are copied while the next one
+  // is packed: up to 1 GB packed the whole array stays staged (8 slices, no
+  // reuse); beyond, two alternating 256 MB pinned slots bound the host memory.
+  // A weight too wide for the width abandons it (nothing of it is used).
+  auto try_width = [&](auto zero) -> bool {
+    using N = decltype(zero);
+    const bool whole = sizeof(N) * (uint64_t)n <= ((uint64_t)1 << 30);
+    const int64_t slice = whole ? (n + 7) / 8 : ((int64_t)256 << 20) / (int64_t)sizeof(N);
+    DBuf<N> d((size_t)n);
+    N *slot[2] = {(N *)host_alloc(sizeof(N) * (size_t)(whole ? n : slice)),
+                  whole ? nullptr : (N *)host_alloc(sizeof(N) * (size_t)slice)};
+    cudaEvent_t ev[2];
+    SG_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    SG_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     bool ok = true;
-    for (int64_t a = 0; a < n && ok; a += per) {
-      const int64_t len = std::min<int64_t>(per, n - a);
-      ok = pack_weights(host + a, len, (uint8_t *)stage + a, threads);
-      if (ok)
-        SG_CUDA(cudaMemcpyAsync(d.p + a, (uint8_t *)stage + a, (size_t)len, cudaMemcpyHostToDevice, s));
+    int k = 0;
+    for (int64_t a0 = 0; a0 < n && ok; a0 += slice, k ^= 1) {
+      const int64_t len = std::min<int64_t>(slice, n - a0);
+      N *dst = whole ? slot[0] + a0 : slot[k];
+      if (!whole && a0 >= 2 * slice) SG_CUDA(cudaEventSynchronize(ev[k]));  // slot k free again
+      ok = pack_weights(host + a0, len, dst, threads);
+      if (!ok) break;
+      SG_CUDA(cudaMemcpyAsync(d.p + a0, dst, sizeof(N) * (size_t)len, cudaMemcpyHostToDevice, ws));
+      SG_CUDA(cudaEventRecord(ev[k], ws));
     }
     if (ok) {
-      k_widen<uint8_t><<<grid_n(n), 256, 0, s>>>(d.p, n, dev);
+      k_widen<N><<<grid_n(n), 256, 0, ws>>>(d.p, n, dev);
       SG_CUDA(cudaGetLastError());
-      g_last_weight_width = 1, done = true;
     }
-    SG_CUDA(cudaStreamSynchronize(s));  // the staging block is reused below
-  }
-  if (done) {
-  } else if (pack_weights(host, n, (uint16_t *)stage, threads)) {
-    DBuf<uint16_t> d((size_t)n);
-    SG_CUDA(cudaMemcpyAsync(d.p, stage, (size_t)n * 2, cudaMemcpyHostToDevice, s));
-    k_widen<uint16_t><<<grid_n(n), 256, 0, s>>>(d.p, n, dev);
-    SG_CUDA(cudaGetLastError());
-    SG_CUDA(cudaStreamSynchronize(s));
-    g_last_weight_width = 2, done = true;
-  }
-  host_free(stage);
-  if (!done) {
-    SG_CUDA(cudaMemcpyAsync(dev, host, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
-    SG_CUDA(cudaStreamSynchronize(s));
+    SG_CUDA(cudaStreamSynchronize(ws));  // slots and d are released below
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    host_free(slot[0]);
+    if (slot[1]) host_free(slot[1]);
+    return ok;
+  };
+  if (try_width(uint8_t{})) {
+    g_last_weight_width = 1;
+  } else if (try_width(uint16_t{})) {
+    g_last_weight_width = 2;
+  } else {
+    SG_CUDA(cudaMemcpyAsync(dev, host, sizeof(int64_t) * n, cudaMemcpyHostToDevice, ws));
+    SG_CUDA(cudaStreamSynchronize(ws));
   }
 }
 }  // namespace
