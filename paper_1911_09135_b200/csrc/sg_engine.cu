@@ -871,8 +871,17 @@ void upload_weights(const int64_t *host, int64_t n, int64_t *dev, cudaStream_t s
   // A weight too wide for the width abandons it (nothing of it is used).
   auto try_width = [&](auto zero) -> bool {
     using N = decltype(zero);
-    const bool whole = sizeof(N) * (uint64_t)n <= ((uint64_t)1 << 30);
-    const int64_t slice = whole ? (n + 7) / 8 : ((int64_t)256 << 20) / (int64_t)sizeof(N);
+    // SG_PACK_WHOLE_MAX / SG_PACK_SLICE (bytes; tests): the staging bounds
+    static const uint64_t whole_max = [] {
+      const char *e = std::getenv("SG_PACK_WHOLE_MAX");
+      return e ? (uint64_t)std::atoll(e) : ((uint64_t)1 << 30);
+    }();
+    static const int64_t slice_bytes = [] {
+      const char *e = std::getenv("SG_PACK_SLICE");
+      return e ? std::max<int64_t>(64, std::atoll(e)) : ((int64_t)256 << 20);
+    }();
+    const bool whole = sizeof(N) * (uint64_t)n <= whole_max;
+    const int64_t slice = whole ? (n + 7) / 8 : std::max<int64_t>(1, slice_bytes / (int64_t)sizeof(N));
     DBuf<N> d((size_t)n);
     N *slot[2] = {(N *)host_alloc(sizeof(N) * (size_t)(whole ? n : slice)),
                   whole ? nullptr : (N *)host_alloc(sizeof(N) * (size_t)slice)};

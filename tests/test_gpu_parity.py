@@ -226,6 +226,33 @@ def test_sssp_weight_upload_widths(sg, O, lo, hi):
         [[r.frontier_size, r.active_edges] for r in log]
 
 
+@pytest.mark.parametrize("lo,hi", [(1, 200), (1, 60000)])
+def test_weight_upload_rotating_slots(lo, hi):
+    """The bounded staging path (two alternating pinned slots, used above 1 GB
+    of packed weights) forced at a small size in a fresh process."""
+    import os, subprocess, sys
+    from pathlib import Path
+    ROOT = Path(__file__).resolve().parents[1]
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {str(ROOT)!r})
+import paper_1911_09135_b200 as sg
+from oracle import oracle_c as O
+off, tgt = O.rmat_csr(14)
+w = np.random.default_rng(3).integers({lo}, {hi}, size=len(tgt), dtype=np.int64)
+g = sg.Graph(off, tgt, w)
+assert np.array_equal(g.device().download(0, weights=True)[2], w)
+res = sg.run_app(g, "sssp")
+lab, log, st = O.run("sssp", *O.prepare(off, tgt, w, "sssp"))
+assert st == 0 and np.array_equal(res.labels, lab)
+print("ok")
+"""
+    env = dict(os.environ, SG_PACK_WHOLE_MAX="0", SG_PACK_SLICE="40000")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("scale,thr", [(18, None), (20, None), (18, 256), (18, 300)])
 @pytest.mark.parametrize("app", ["bfs", "sssp", "cc", "kcore", "pr"])
 def test_larger_scale_vs_c_oracle(sg, scale, thr, app):
