@@ -116,7 +116,11 @@ void sg_release_cached(void);
 
 /* --- graph store (graph.py:29-177) ------------------------------------- */
 /* Upload a CSR (graph.py:33-37 dtypes): offsets int64[nv+1], targets int32[ne],
- * weights int64[ne] or NULL.  Validates like Graph._validate (graph.py:44-57). */
+ * weights int64[ne] or NULL.  Validates like Graph._validate (graph.py:44-57).
+ * Weights that all fit 1 (2) bytes cross the host link packed (host threads,
+ * while the topology is in flight) and are widened back on the device; the
+ * graph keeps int64 weights either way.  Pinned host buffers (sg_host_alloc)
+ * give full link speed. */
 int sg_graph_create(const int64_t *offsets, const int32_t *targets, const int64_t *weights,
                     int64_t nv, int64_t ne, sg_graph **out);
 /* generate_rmat on the device (graph.py:274-298), bit-exact to numpy PCG64:
